@@ -1,0 +1,129 @@
+"""Device-resident batched CA-CFAR (the throughput path) over torch CUDA tensors.
+
+One :class:`BatchCfar` owns every device buffer of a batch shape (alpha table,
+bit-packed masks, detection lists, counts, workspace) so repeated calls launch
+kernels only: SAT (kernel c) -> CFAR (kernel d) -> per-map detection sort, on
+the caller's current torch stream. PyTorch is used for allocation and streams
+only; all arithmetic is in libuwbvital_b200.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .api import DETECTION_DTYPE, CfarParams
+from .errors import CapacityError, InputError, raise_for
+
+_DT = {torch.float32: N.UWB_F32, torch.float64: N.UWB_F64}
+_MODES = {"global": N.UWB_SAT_GLOBAL, "slab": N.UWB_SAT_SLAB}
+
+
+class BatchCfar:
+    def __init__(self, n_maps: int, rows: int, cols: int, params: CfarParams,
+                 dtype: torch.dtype = torch.float32, sat_mode: str = "global", slab_rows: int = 0,
+                 det_capacity: int = 1024, device=None, want_mask_u8: bool = False,
+                 want_thresholds: bool = False):
+        if dtype not in _DT:
+            raise ValueError("maps must be float32 or float64")
+        params.validate()
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.n_maps, self.rows, self.cols = int(n_maps), int(rows), int(cols)
+        self.params = params
+        self.dtype = dtype
+        self.sat_mode = _MODES[sat_mode]
+        self.slab_rows = int(slab_rows)
+        self.det_capacity = int(det_capacity)
+        self.words_per_row = (self.cols + 31) // 32
+        dev = self.device
+        self.alpha = torch.from_numpy(params.alpha_table()).to(dev)
+        self.mask_bits = torch.zeros((self.n_maps, self.rows, self.words_per_row), dtype=torch.int32, device=dev)
+        self.dets = torch.zeros((self.n_maps, max(1, self.det_capacity), 32), dtype=torch.uint8, device=dev)
+        self.counts = torch.zeros(self.n_maps, dtype=torch.int64, device=dev)
+        self.first_bad = torch.zeros((self.n_maps, 2), dtype=torch.int64, device=dev)
+        self.mask_u8 = (torch.zeros((self.n_maps, self.rows, self.cols), dtype=torch.uint8, device=dev)
+                        if want_mask_u8 else None)
+        self.thresholds = (torch.zeros((self.n_maps, self.rows, self.cols), dtype=torch.float64, device=dev)
+                           if want_thresholds else None)
+        self._cparams = params.to_c()
+        self._batch = N.uwb_map_batch(None, _DT[dtype], 0, self.n_maps, self.rows, self.cols, self.cols,
+                                      self.rows * self.cols)
+        ws = N.lib.uwb_dev_cfar2d_workspace(C.byref(self._batch), C.byref(self._cparams), self.sat_mode,
+                                            C.c_uint64(self.slab_rows), C.c_uint64(self.det_capacity))
+        self.workspace = torch.empty(int(ws), dtype=torch.uint8, device=dev)
+        self._out = N.uwb_cfar_outputs(
+            self.mask_bits.data_ptr(), self.words_per_row, self.rows * self.words_per_row,
+            self.mask_u8.data_ptr() if self.mask_u8 is not None else None,
+            self.thresholds.data_ptr() if self.thresholds is not None else None,
+            self.dets.data_ptr(), self.det_capacity, self.counts.data_ptr(), self.first_bad.data_ptr())
+
+    def __call__(self, maps: torch.Tensor, sort: bool = True, stream=None, phase_events: bool = False) -> None:
+        """Launch SAT + CFAR (+ sort) for ``maps`` of shape (n_maps, rows, cols).
+        ``phase_events`` records per-phase CUDA events (read with :func:`phase_ms`)."""
+        if maps.dtype != self.dtype or tuple(maps.shape) != (self.n_maps, self.rows, self.cols):
+            raise ValueError(f"expected {(self.n_maps, self.rows, self.cols)} {self.dtype}, got "
+                             f"{tuple(maps.shape)} {maps.dtype}")
+        if not maps.is_cuda or not maps.is_contiguous():
+            raise ValueError("maps must be a contiguous CUDA tensor")
+        self._batch.maps = maps.data_ptr()
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        st = N.lib.uwb_dev_cfar2d(C.byref(self._batch), C.byref(self._cparams), self.alpha.data_ptr(),
+                                  self.sat_mode, C.c_uint64(self.slab_rows), C.byref(self._out),
+                                  self.workspace.data_ptr(), C.c_uint64(self.workspace.numel()),
+                                  (0 if sort else 1) | (2 if phase_events else 0), C.c_void_p(s.cuda_stream))
+        raise_for(st)
+
+    # ---- host views (synchronising) ----
+    def check_inputs(self) -> None:
+        """Raise the reference's InputError for the first map with a bad cell."""
+        fb = self.first_bad.cpu().numpy().astype(np.uint64)
+        for i in range(self.n_maps):
+            if fb[i, 0] != np.uint64(0xFFFFFFFFFFFFFFFF):
+                r, c = divmod(int(fb[i, 0]), self.cols)
+                raise InputError(f"build_sat: non-finite entry at ({r}, {c})", r, c)
+            if fb[i, 1] != np.uint64(0xFFFFFFFFFFFFFFFF):
+                r, c = divmod(int(fb[i, 1]), self.cols)
+                raise InputError(f"cfar2d: cell ({r}, {c}) is not a finite non-negative power", r, c)
+
+    def detection_counts(self) -> np.ndarray:
+        return self.counts.cpu().numpy()
+
+    def detections(self, i: int) -> np.ndarray:
+        n = int(self.counts[i].item())
+        if n > self.det_capacity:
+            raise CapacityError(f"map {i}: {n} detections > capacity {self.det_capacity}", n)
+        raw = self.dets[i, :n].contiguous().cpu().numpy().reshape(-1)
+        return np.frombuffer(raw.tobytes(), dtype=DETECTION_DTYPE, count=n).copy()
+
+    def mask(self, i: int) -> np.ndarray:
+        """Unpack map i's bit mask into a rows x cols uint8 array."""
+        words = self.mask_bits[i].cpu().numpy().view(np.uint32)
+        bits = np.unpackbits(words.view(np.uint8).reshape(self.rows, -1), axis=1, bitorder="little")
+        return bits[:, : self.cols].astype(np.uint8)
+
+
+def phase_ms(max_calls: int = 4096) -> np.ndarray:
+    """(calls, 3) array of {sat, cfar, sort} milliseconds of the calls made with
+    ``phase_events=True`` since the last read (synchronises on them)."""
+    out = np.zeros((max_calls, 3), dtype=np.float32)
+    n = N.lib.uwb_dev_phase_ms(out.ctypes.data_as(C.c_void_p), max_calls)
+    return out[:n].copy()
+
+
+def kernel_launches() -> int:
+    return int(N.lib.uwb_kernel_launches())
+
+
+def host_cfar2d_batch(maps_host: torch.Tensor, params: CfarParams, mask_bits_host: torch.Tensor,
+                      dets_host: torch.Tensor, counts_host: torch.Tensor, det_capacity: int,
+                      sat_mode: str = "global", slab_rows: int = 0, maps_per_chunk: int = 128) -> None:
+    """End-to-end call from (pinned) host buffers: H2D, SAT+CFAR+sort, D2H, streamed in chunks."""
+    n_maps, rows, cols = maps_host.shape
+    b = N.uwb_map_batch(maps_host.data_ptr(), _DT[maps_host.dtype], 0, n_maps, rows, cols, cols, rows * cols)
+    p = params.to_c()
+    st = N.lib.uwb_host_cfar2d_batch(C.byref(b), C.byref(p), _MODES[sat_mode], C.c_uint64(slab_rows),
+                                     mask_bits_host.data_ptr(), dets_host.data_ptr(), C.c_uint64(det_capacity),
+                                     counts_host.data_ptr(), C.c_uint64(maps_per_chunk))
+    raise_for(st)

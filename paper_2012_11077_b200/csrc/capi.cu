@@ -1,0 +1,1039 @@
+// Host side of the C ABI (include/uwbvital_b200.h).
+//
+// Every host-level entry point restates the reference function's validation
+// order and message text (proj/src/{sat,cfar,pipeline}.cpp) and runs the
+// arithmetic on the GPU; there is no host compute fallback. Scalar helpers
+// that the reference evaluates on the host with libm (alpha_factor, the FFT
+// twiddles the oracle's FFTW provider uses, the window clamps) stay on the host
+// so their bits match.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace uwb {
+
+size_t frontend_rows_smem(int64_t n, int64_t L);
+
+namespace {
+
+struct ErrorState {
+    std::string message;
+    int64_t row = -1;
+    int64_t col = -1;
+};
+thread_local ErrorState g_err;
+
+std::string fmt_double(double v) { // std::to_string(double) == "%f"
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "%f", v);
+    return buf;
+}
+std::string S(uint64_t v) { return std::to_string(v); }
+std::string S(int64_t v) { return std::to_string(v); }
+std::string S(int v) { return std::to_string(v); }
+
+uwb_status ok() {
+    g_err.message.clear();
+    g_err.row = g_err.col = -1;
+    return UWB_OK;
+}
+
+uwb_status fail(uwb_status s, const std::string& msg, int64_t row = -1, int64_t col = -1) {
+    g_err.message = msg;
+    g_err.row = row;
+    g_err.col = col;
+    return s;
+}
+
+// Per host thread non-blocking stream for the synchronous host-level calls.
+cudaStream_t host_stream() {
+    thread_local cudaStream_t s = nullptr;
+    if (!s) cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    return s;
+}
+
+// Stream-ordered device buffer.
+struct DevBuf {
+    void* p = nullptr;
+    cudaStream_t s = nullptr;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) cudaFreeAsync(p, s);
+    }
+    cudaError_t alloc(size_t bytes, cudaStream_t stream) {
+        s = stream;
+        return cudaMallocAsync(&p, bytes ? bytes : 16, stream);
+    }
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+bool device_ok() {
+    int n = 0;
+    return cudaGetDeviceCount(&n) == cudaSuccess && n > 0;
+}
+
+uwb_status need_device() {
+    if (!device_ok()) return fail(UWB_CUDA_ERROR, "uwbvital_b200: no CUDA device available (no CPU fallback)");
+    return UWB_OK;
+}
+
+int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+// --- scalar reference logic (cfar.cpp) ---------------------------------------
+
+uwb_status validate_params(const uwb_cfar_params& p) {
+    // cfar.cpp:14-26 (per axis: rows first, then cols)
+    if (p.guard_rows < 0) return fail(UWB_PARAMETER_ERROR, "CfarParams: guard_radius must be >= 0, got " + S(p.guard_rows));
+    if (p.guard_cols < 0) return fail(UWB_PARAMETER_ERROR, "CfarParams: guard_radius must be >= 0, got " + S(p.guard_cols));
+    if (p.background_rows < 1) return fail(UWB_PARAMETER_ERROR, "CfarParams: background_radius must be >= 1, got " + S(p.background_rows));
+    if (p.background_cols < 1) return fail(UWB_PARAMETER_ERROR, "CfarParams: background_radius must be >= 1, got " + S(p.background_cols));
+    if (!(p.pfa > 0.0) || !(p.pfa < 1.0)) return fail(UWB_PARAMETER_ERROR, "CfarParams: pfa must lie in (0,1), got " + fmt_double(p.pfa));
+    return ok();
+}
+
+uint64_t interior_count(const uwb_cfar_params& p) {
+    const uint64_t orr = 2 * static_cast<uint64_t>(p.guard_rows + p.background_rows) + 1;
+    const uint64_t oc = 2 * static_cast<uint64_t>(p.guard_cols + p.background_cols) + 1;
+    const uint64_t gr = 2 * static_cast<uint64_t>(p.guard_rows) + 1;
+    const uint64_t gc = 2 * static_cast<uint64_t>(p.guard_cols) + 1;
+    return orr * oc - gr * gc;
+}
+
+double alpha_value(uint64_t n_train, double pfa) { // cfar.cpp:41-42
+    const double n = static_cast<double>(n_train);
+    return n * (std::pow(pfa, -1.0 / n) - 1.0);
+}
+
+std::vector<double> alpha_table_host(const uwb_cfar_params& p) {
+    const uint64_t n_int = interior_count(p);
+    std::vector<double> a(n_int + 1, 0.0);
+    for (uint64_t n = 1; n <= n_int; ++n) a[n] = alpha_value(n, p.pfa);
+    return a;
+}
+
+bool degenerate(const uwb_cfar_params& p, uint64_t rows, uint64_t cols) { // cfar.cpp:99-107
+    return rows <= 2 * static_cast<uint64_t>(p.guard_rows) + 1 &&
+           cols <= 2 * static_cast<uint64_t>(p.guard_cols) + 1;
+}
+
+std::string degenerate_msg(const uwb_cfar_params& p, uint64_t rows, uint64_t cols) {
+    const uint64_t sr = 2 * static_cast<uint64_t>(p.guard_rows) + 1;
+    const uint64_t sc = 2 * static_cast<uint64_t>(p.guard_cols) + 1;
+    return "cfar2d: " + S(rows) + "x" + S(cols) + " map fits inside the " + S(sr) + "x" + S(sc) +
+           " guard window; no training cells remain";
+}
+
+// --- batch plumbing -----------------------------------------------------------
+
+struct Plan {
+    JobGeometry geo;
+    int64_t n_maps, cols, n_jobs, table_ld, table_stride, strips, max_rows;
+    size_t off_tables, off_edge, off_prog, off_counter, off_scratch, total;
+};
+
+Plan make_plan(const uwb_map_batch& b, const uwb_cfar_params* p, int sat_mode, uint64_t slab_rows,
+               int64_t det_cap) {
+    Plan P{};
+    P.n_maps = static_cast<int64_t>(b.n_maps);
+    P.cols = static_cast<int64_t>(b.cols);
+    P.geo.rows = static_cast<int64_t>(b.rows);
+    if (sat_mode == UWB_SAT_SLAB && slab_rows > 0 && slab_rows < b.rows) {
+        P.geo.slab_rows = static_cast<int64_t>(slab_rows);
+        P.geo.halo = p ? p->guard_rows + p->background_rows : 0;
+    } else {
+        P.geo.slab_rows = P.geo.rows > 0 ? P.geo.rows : 1;
+        P.geo.halo = 0;
+    }
+    P.geo.n_slabs = P.geo.rows > 0 ? (P.geo.rows + P.geo.slab_rows - 1) / P.geo.slab_rows : 0;
+    P.n_jobs = P.n_maps * P.geo.n_slabs;
+    P.max_rows = P.geo.max_table_rows();
+    P.table_ld = round_up(P.cols + 2, 4);
+    P.table_stride = (P.max_rows + 1) * P.table_ld;
+    P.strips = sat_strips(P.cols);
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off += round_up(static_cast<int64_t>(bytes), 256);
+        return o;
+    };
+    P.off_tables = take(sizeof(double) * static_cast<size_t>(P.n_jobs) * P.table_stride);
+    P.off_edge = take(P.strips > 1 ? sizeof(double) * P.n_jobs * P.strips * P.max_rows : 0);
+    P.off_prog = take(sizeof(unsigned) * P.n_jobs * P.strips);
+    P.off_counter = take(sizeof(unsigned) * 4);
+    P.off_scratch = take(det_cap > 2048 ? sizeof(uwb_detection) * P.n_maps * det_cap : 0);
+    P.total = off;
+    return P;
+}
+
+SatLaunch sat_launch(const Plan& P, const uwb_map_batch& b, char* ws, unsigned long long* first_bad) {
+    SatLaunch L{};
+    L.maps = b.maps;
+    L.ld = static_cast<int64_t>(b.ld);
+    L.map_stride = static_cast<int64_t>(b.map_stride);
+    L.cols = P.cols;
+    L.geo = P.geo;
+    L.n_jobs = P.n_jobs;
+    L.table = reinterpret_cast<double*>(ws + P.off_tables);
+    L.table_ld = P.table_ld;
+    L.table_stride = P.table_stride;
+    L.strips = P.strips;
+    L.gedge = reinterpret_cast<double*>(ws + P.off_edge);
+    L.edge_stride = P.max_rows;
+    L.gprog = reinterpret_cast<unsigned*>(ws + P.off_prog);
+    L.tile_counter = reinterpret_cast<unsigned*>(ws + P.off_counter);
+    L.first_bad = first_bad;
+    L.elem_bytes = b.dtype == UWB_F32 ? 4 : 8;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(b.maps);
+    L.vec_ok = (a % 16 == 0) && ((b.ld * L.elem_bytes) % 16 == 0) &&
+               ((b.map_stride * L.elem_bytes) % 16 == 0);
+    return L;
+}
+
+cudaError_t run_sat(const Plan& P, const SatLaunch& L, int dtype, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(L.gprog, 0, sizeof(unsigned) * P.n_jobs * P.strips, s);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(L.tile_counter, 0, sizeof(unsigned), s);
+    if (e != cudaSuccess) return e;
+    return launch_sat(L, dtype, s);
+}
+
+CfarLaunch cfar_launch(const Plan& P, const uwb_map_batch& b, const uwb_cfar_params& p,
+                       const double* alpha, char* ws, const uwb_cfar_outputs& o) {
+    CfarLaunch L{};
+    L.maps = b.maps;
+    L.ld = static_cast<int64_t>(b.ld);
+    L.map_stride = static_cast<int64_t>(b.map_stride);
+    L.cols = P.cols;
+    L.geo = P.geo;
+    L.n_jobs = P.n_jobs;
+    L.table = ws ? reinterpret_cast<const double*>(ws + P.off_tables) : nullptr;
+    L.table_ld = P.table_ld;
+    L.table_stride = P.table_stride;
+    L.gr = p.guard_rows;
+    L.gc = p.guard_cols;
+    L.hr = p.guard_rows + p.background_rows;
+    L.hc = p.guard_cols + p.background_cols;
+    L.alpha = alpha;
+    L.mask_bits = o.mask_bits;
+    L.words_per_row = static_cast<int64_t>(o.words_per_row);
+    L.mask_map_stride = static_cast<int64_t>(o.mask_map_stride);
+    L.mask_u8 = o.mask_u8;
+    L.thresholds = o.thresholds;
+    L.dets = o.dets;
+    L.det_cap = static_cast<int64_t>(o.det_capacity);
+    L.det_counts = reinterpret_cast<unsigned long long*>(o.det_counts);
+    L.first_bad = reinterpret_cast<unsigned long long*>(o.first_bad);
+    return L;
+}
+
+uwb_status check_batch(const uwb_map_batch* b) {
+    if (!b || (!b->maps && b->n_maps && b->rows && b->cols)) return fail(UWB_INVALID_ARGUMENT, "uwb: null batch");
+    if (b->dtype != UWB_F32 && b->dtype != UWB_F64) return fail(UWB_INVALID_ARGUMENT, "uwb: bad dtype");
+    if (b->ld < b->cols || (b->n_maps > 1 && b->map_stride < b->rows * b->ld))
+        return fail(UWB_INVALID_ARGUMENT, "uwb: bad batch layout");
+    return UWB_OK;
+}
+
+
+// Phase-event ring (flags bit 1 of uwb_dev_cfar2d).
+struct PhaseRing {
+    static constexpr int kSlots = 4096;
+    std::mutex mu;
+    std::vector<cudaEvent_t> ev; // 4 per slot
+    int used = 0;
+    cudaEvent_t* slot() {
+        std::lock_guard<std::mutex> lk(mu);
+        if (ev.empty()) {
+            ev.resize(static_cast<size_t>(kSlots) * 4);
+            for (auto& e : ev) cudaEventCreate(&e);
+        }
+        if (used >= kSlots) return nullptr;
+        return &ev[static_cast<size_t>(used++) * 4];
+    }
+};
+PhaseRing g_phase;
+
+// Device-resident CFAR of a batch (no validation beyond layout; see uwb_dev_cfar2d).
+uwb_status dev_cfar(const uwb_map_batch& b, const uwb_cfar_params& p, const double* alpha,
+                    int backend, int sat_mode, uint64_t slab_rows, const uwb_cfar_outputs& o,
+                    void* workspace, uint64_t ws_bytes, uint32_t flags, cudaStream_t s) {
+    const Plan P = make_plan(b, &p, backend == UWB_INTEGRAL ? sat_mode : UWB_SAT_GLOBAL, slab_rows,
+                             static_cast<int64_t>(o.det_capacity));
+    if (P.n_jobs > 65535) return fail(UWB_INVALID_ARGUMENT, "uwb: more than 65535 (map, slab) jobs per call");
+    if (backend == UWB_INTEGRAL && ws_bytes < P.total) return fail(UWB_INVALID_ARGUMENT, "uwb: workspace too small");
+    char* ws = static_cast<char*>(workspace);
+    cudaEvent_t* ev = (flags & 2u) ? g_phase.slot() : nullptr;
+    UWB_CUDA_TRY(cudaMemsetAsync(o.det_counts, 0, sizeof(uint64_t) * b.n_maps, s));
+    if (o.first_bad) UWB_CUDA_TRY(cudaMemsetAsync(o.first_bad, 0xff, sizeof(uint64_t) * 2 * b.n_maps, s));
+    if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[0], s));
+    if (backend == UWB_INTEGRAL) {
+        const SatLaunch SL = sat_launch(P, b, ws, reinterpret_cast<unsigned long long*>(o.first_bad));
+        UWB_CUDA_TRY(run_sat(P, SL, b.dtype, s));
+        if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[1], s));
+        UWB_CUDA_TRY(launch_cfar_integral(cfar_launch(P, b, p, alpha, ws, o), b.dtype, s));
+    } else {
+        if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[1], s));
+        UWB_CUDA_TRY(launch_cfar_naive(cfar_launch(P, b, p, alpha, nullptr, o), b.dtype, s));
+    }
+    if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[2], s));
+    struct Tail {
+        cudaEvent_t* ev;
+        cudaStream_t s;
+        ~Tail() {
+            if (ev) cudaEventRecord(ev[3], s);
+        }
+    } tail{ev, s};
+    if (!(flags & 1u)) {
+        uwb_detection* scratch = (o.det_capacity > 2048 && ws && ws_bytes >= P.total)
+                                     ? reinterpret_cast<uwb_detection*>(ws + P.off_scratch)
+                                     : nullptr;
+        UWB_CUDA_TRY(launch_sort_detections(o.dets, static_cast<int64_t>(o.det_capacity),
+                                            reinterpret_cast<const unsigned long long*>(o.det_counts),
+                                            static_cast<int64_t>(b.n_maps), scratch, s));
+    }
+    return UWB_OK;
+}
+
+void twiddles(int64_t L, std::vector<double>& wr, std::vector<double>& wi) {
+    // identical expression to oracle/fftw_shim/fft_provider.c:uwb_fft_twiddles
+    wr.resize(static_cast<size_t>(L));
+    wi.resize(static_cast<size_t>(L));
+    for (int64_t k = 0; k < L; ++k) {
+        const double angle = (2.0 * M_PI * static_cast<double>(k)) / static_cast<double>(L);
+        wr[static_cast<size_t>(k)] = std::cos(angle);
+        wi[static_cast<size_t>(k)] = -std::sin(angle);
+    }
+}
+
+uint64_t next_pow2(uint64_t n) {
+    uint64_t p = 1;
+    while (p < n) p <<= 1;
+    return p;
+}
+
+} // namespace
+
+uwb_status set_error(uwb_status s, const char* msg, int64_t row, int64_t col) {
+    return fail(s, msg, row, col);
+}
+
+uwb_status set_cuda_error(cudaError_t e, const char* what) {
+    return fail(UWB_CUDA_ERROR, std::string("CUDA error ") + cudaGetErrorString(e) + " in " + what);
+}
+
+} // namespace uwb
+
+using namespace uwb;
+
+// ======================================================================== API
+
+extern "C" {
+
+const char* uwb_last_error(void) { return g_err.message.c_str(); }
+
+void uwb_last_error_cell(int64_t* row, int64_t* col) {
+    if (row) *row = g_err.row;
+    if (col) *col = g_err.col;
+}
+
+int uwb_device_available(void) { return device_ok() ? 1 : 0; }
+
+uwb_status uwb_alpha_factor(uint64_t n_train, double pfa, double* out) {
+    if (n_train == 0) return fail(UWB_PARAMETER_ERROR, "alpha_factor: n_train must be >= 1");
+    if (!(pfa > 0.0) || !(pfa < 1.0))
+        return fail(UWB_PARAMETER_ERROR, "alpha_factor: pfa must lie in (0,1), got " + fmt_double(pfa));
+    *out = alpha_value(n_train, pfa);
+    return ok();
+}
+
+uwb_status uwb_cfar_params_validate(const uwb_cfar_params* p) {
+    if (!p) return fail(UWB_INVALID_ARGUMENT, "uwb: null params");
+    return validate_params(*p);
+}
+
+uint64_t uwb_interior_train_count(const uwb_cfar_params* p) { return p ? interior_count(*p) : 0; }
+
+uwb_status uwb_training_window(const uwb_cfar_params* p, uint64_t row, uint64_t col, uint64_t rows,
+                               uint64_t cols, uint64_t out[9]) {
+    // cfar.cpp:179-198
+    if (uwb_status s = validate_params(*p)) return s;
+    if (row >= rows || col >= cols)
+        return fail(UWB_BOUNDS_ERROR, "training_window: cell (" + S(row) + ", " + S(col) + ") outside " +
+                                          S(rows) + "x" + S(cols) + " map");
+    auto lo = [](uint64_t c, int r) -> uint64_t {
+        const long long v = static_cast<long long>(c) - r;
+        return v < 0 ? 0 : static_cast<uint64_t>(v);
+    };
+    auto hi = [](uint64_t c, int r, uint64_t d) -> uint64_t {
+        const uint64_t v = c + static_cast<uint64_t>(r);
+        return v >= d ? d - 1 : v;
+    };
+    const int hr = p->guard_rows + p->background_rows, hc = p->guard_cols + p->background_cols;
+    out[0] = lo(row, hr); out[1] = hi(row, hr, rows); out[2] = lo(col, hc); out[3] = hi(col, hc, cols);
+    out[4] = lo(row, p->guard_rows); out[5] = hi(row, p->guard_rows, rows);
+    out[6] = lo(col, p->guard_cols); out[7] = hi(col, p->guard_cols, cols);
+    out[8] = (out[1] - out[0] + 1) * (out[3] - out[2] + 1) - (out[5] - out[4] + 1) * (out[7] - out[6] + 1);
+    if (out[8] == 0)
+        return fail(UWB_CONFIGURATION_ERROR, "training_window: " + S(rows) + "x" + S(cols) +
+                                                 " map leaves no training cells at (" + S(row) + ", " +
+                                                 S(col) + ")");
+    return ok();
+}
+
+uwb_status uwb_alpha_table(const uwb_cfar_params* p, double* out, uint64_t len) {
+    if (uwb_status s = validate_params(*p)) return s;
+    const std::vector<double> a = alpha_table_host(*p);
+    if (len < a.size()) return fail(UWB_INVALID_ARGUMENT, "uwb_alpha_table: buffer shorter than interior_train_count+1");
+    std::memcpy(out, a.data(), sizeof(double) * a.size());
+    return ok();
+}
+
+// ------------------------------------------------------------ build_sat ---
+
+uwb_status uwb_build_sat(const double* src, uint64_t rows, uint64_t cols, double* table) {
+    if (rows == 0 || cols == 0)
+        return fail(UWB_DIMENSION_ERROR, "build_sat: source matrix must be at least 1x1, got " + S(rows) + "x" + S(cols));
+    if (uwb_status s = need_device()) return s;
+    cudaStream_t s = host_stream();
+    uwb_map_batch b{};
+    b.dtype = UWB_F64;
+    b.n_maps = 1;
+    b.rows = rows;
+    b.cols = cols;
+    b.ld = cols;
+    b.map_stride = rows * cols;
+    DevBuf d_src, d_ws, d_bad;
+    UWB_CUDA_TRY(d_src.alloc(sizeof(double) * rows * cols, s));
+    UWB_CUDA_TRY(cudaMemcpyAsync(d_src.p, src, sizeof(double) * rows * cols, cudaMemcpyHostToDevice, s));
+    b.maps = d_src.p;
+    const uint64_t wsb = uwb_dev_build_sat_workspace(&b);
+    UWB_CUDA_TRY(d_ws.alloc(wsb, s));
+    UWB_CUDA_TRY(d_bad.alloc(sizeof(uint64_t) * 2, s));
+    const Plan P = make_plan(b, nullptr, UWB_SAT_GLOBAL, 0, 0);
+    double* d_table = reinterpret_cast<double*>(static_cast<char*>(d_ws.p) + P.off_tables);
+    if (uwb_status st = uwb_dev_build_sat(&b, d_table, P.table_ld, P.table_stride, d_bad.as<uint64_t>(),
+                                          d_ws.p, wsb, s))
+        return st;
+    uint64_t bad[2];
+    UWB_CUDA_TRY(cudaMemcpyAsync(bad, d_bad.p, sizeof(bad), cudaMemcpyDeviceToHost, s));
+    UWB_CUDA_TRY(cudaMemcpy2DAsync(table, sizeof(double) * (cols + 1), d_table + 1,
+                                   sizeof(double) * P.table_ld, sizeof(double) * (cols + 1), rows + 1,
+                                   cudaMemcpyDeviceToHost, s));
+    UWB_CUDA_TRY(cudaStreamSynchronize(s));
+    if (bad[0] != ~0ull) {
+        const int64_t r = static_cast<int64_t>(bad[0] / cols), c = static_cast<int64_t>(bad[0] % cols);
+        return fail(UWB_INPUT_ERROR, "build_sat: non-finite entry at (" + S(r) + ", " + S(c) + ")", r, c);
+    }
+    return ok();
+}
+
+uint64_t uwb_dev_build_sat_workspace(const uwb_map_batch* b) {
+    return make_plan(*b, nullptr, UWB_SAT_GLOBAL, 0, 0).total;
+}
+
+uwb_status uwb_dev_build_sat(const uwb_map_batch* b, double* sat, uint64_t sat_ld, uint64_t sat_map_stride,
+                             uint64_t* first_nonfinite, void* workspace, uint64_t ws_bytes, void* stream) {
+    if (uwb_status s = check_batch(b)) return s;
+    if (uwb_status s = need_device()) return s;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Plan P = make_plan(*b, nullptr, UWB_SAT_GLOBAL, 0, 0);
+    if (ws_bytes < P.total) return fail(UWB_INVALID_ARGUMENT, "uwb: workspace too small");
+    if (sat_ld < static_cast<uint64_t>(P.cols + 2) || sat_ld % 2 || reinterpret_cast<uintptr_t>(sat) % 16)
+        return fail(UWB_INVALID_ARGUMENT, "uwb_dev_build_sat: table must be 16-byte aligned with even ld >= cols+2");
+    char* ws = static_cast<char*>(workspace);
+    // first_nonfinite uses the 2-slot-per-map layout internally
+    DevBuf bad;
+    UWB_CUDA_TRY(bad.alloc(sizeof(uint64_t) * 2 * b->n_maps, s));
+    UWB_CUDA_TRY(cudaMemsetAsync(bad.p, 0xff, sizeof(uint64_t) * 2 * b->n_maps, s));
+    SatLaunch L = sat_launch(P, *b, ws, bad.as<unsigned long long>());
+    L.table = sat;
+    L.table_ld = static_cast<int64_t>(sat_ld);
+    L.table_stride = static_cast<int64_t>(sat_map_stride);
+    UWB_CUDA_TRY(run_sat(P, L, b->dtype, s));
+    if (first_nonfinite)
+        UWB_CUDA_TRY(cudaMemcpy2DAsync(first_nonfinite, sizeof(uint64_t), bad.p, 2 * sizeof(uint64_t),
+                                       sizeof(uint64_t), b->n_maps, cudaMemcpyDeviceToDevice, s));
+    return ok();
+}
+
+// ---------------------------------------------------------------- CFAR ---
+
+uint64_t uwb_dev_cfar2d_workspace(const uwb_map_batch* b, const uwb_cfar_params* p, int32_t sat_mode,
+                                  uint64_t slab_rows, uint64_t det_capacity) {
+    return make_plan(*b, p, sat_mode, slab_rows, static_cast<int64_t>(det_capacity)).total;
+}
+
+uwb_status uwb_dev_cfar2d(const uwb_map_batch* b, const uwb_cfar_params* p, const double* alpha_dev,
+                          int32_t sat_mode, uint64_t slab_rows, const uwb_cfar_outputs* out,
+                          void* workspace, uint64_t ws_bytes, uint32_t flags, void* stream) {
+    if (uwb_status s = check_batch(b)) return s;
+    if (uwb_status s = validate_params(*p)) return s;
+    if (b->rows == 0 || b->cols == 0) return fail(UWB_DIMENSION_ERROR, "cfar2d: power map must be at least 1x1");
+    if (degenerate(*p, b->rows, b->cols)) return fail(UWB_CONFIGURATION_ERROR, degenerate_msg(*p, b->rows, b->cols));
+    if (uwb_status s = need_device()) return s;
+    const Plan P = make_plan(*b, p, sat_mode, slab_rows, static_cast<int64_t>(out->det_capacity));
+    if (ws_bytes < P.total) return fail(UWB_INVALID_ARGUMENT, "uwb: workspace too small (need " + S(static_cast<uint64_t>(P.total)) + ")");
+    if (uwb_status s = dev_cfar(*b, *p, alpha_dev, UWB_INTEGRAL, sat_mode, slab_rows, *out, workspace,
+                                ws_bytes, flags, static_cast<cudaStream_t>(stream)))
+        return s;
+    return ok();
+}
+
+uwb_status uwb_cfar2d(uwb_backend backend, const double* map, uint64_t rows, uint64_t cols,
+                      const uwb_cfar_params* p, uint8_t* mask, double* thresholds, uwb_detection* dets,
+                      uint64_t det_capacity, uint64_t* n_det) {
+    *n_det = 0;
+    const uint64_t cells = rows * cols;
+    if (backend == UWB_INTEGRAL && cells == 0) // sat.cpp:13-16 runs first
+        return fail(UWB_DIMENSION_ERROR, "build_sat: source matrix must be at least 1x1, got " + S(rows) + "x" + S(cols));
+    if (backend == UWB_NAIVE) {
+        if (uwb_status s = validate_params(*p)) return s;
+        if (cells == 0) return fail(UWB_DIMENSION_ERROR, "cfar2d: power map must be at least 1x1");
+    }
+    if (uwb_status s = need_device()) return s;
+    cudaStream_t s = host_stream();
+
+    uwb_map_batch b{};
+    b.dtype = UWB_F64;
+    b.n_maps = 1;
+    b.rows = rows;
+    b.cols = cols;
+    b.ld = cols;
+    b.map_stride = cells;
+    // parameters may be invalid at this point for the integral backend (the
+    // reference validates them after building the table); keep the kernels safe
+    uwb_cfar_params q = *p;
+    const bool params_ok = validate_params(q) == UWB_OK;
+    if (!params_ok) q = uwb_cfar_params{0, 0, 1, 1, 0.5};
+    const std::vector<double> alpha = alpha_table_host(q);
+    // first pass with a bounded list; rerun with the exact count on overflow
+    uint64_t cap = std::max<uint64_t>(std::min<uint64_t>(cells, 1u << 16), 1);
+retry:
+    DevBuf d_map, d_alpha, d_mask, d_thr, d_dets, d_cnt, d_bad, d_bits, d_ws;
+    UWB_CUDA_TRY(d_map.alloc(sizeof(double) * cells, s));
+    UWB_CUDA_TRY(cudaMemcpyAsync(d_map.p, map, sizeof(double) * cells, cudaMemcpyHostToDevice, s));
+    b.maps = d_map.p;
+    UWB_CUDA_TRY(d_alpha.alloc(sizeof(double) * alpha.size(), s));
+    UWB_CUDA_TRY(cudaMemcpyAsync(d_alpha.p, alpha.data(), sizeof(double) * alpha.size(), cudaMemcpyHostToDevice, s));
+    UWB_CUDA_TRY(d_mask.alloc(cells, s));
+    UWB_CUDA_TRY(d_thr.alloc(sizeof(double) * cells, s));
+    UWB_CUDA_TRY(d_dets.alloc(sizeof(uwb_detection) * cap, s));
+    UWB_CUDA_TRY(d_cnt.alloc(sizeof(uint64_t), s));
+    UWB_CUDA_TRY(d_bad.alloc(sizeof(uint64_t) * 2, s));
+    const uint64_t words = (cols + 31) / 32;
+    UWB_CUDA_TRY(d_bits.alloc(sizeof(uint32_t) * words * rows, s));
+
+    uwb_cfar_outputs o{};
+    o.mask_bits = d_bits.as<uint32_t>();
+    o.words_per_row = words;
+    o.mask_map_stride = words * rows;
+    o.mask_u8 = d_mask.as<uint8_t>();
+    o.thresholds = d_thr.as<double>();
+    o.dets = d_dets.as<uwb_detection>();
+    o.det_capacity = cap;
+    o.det_counts = d_cnt.as<uint64_t>();
+    o.first_bad = d_bad.as<uint64_t>();
+
+    const Plan P = make_plan(b, &q, UWB_SAT_GLOBAL, 0, static_cast<int64_t>(cap));
+    UWB_CUDA_TRY(d_ws.alloc(P.total, s));
+    if (uwb_status st = dev_cfar(b, q, d_alpha.as<double>(), backend, UWB_SAT_GLOBAL, 0, o, d_ws.p, P.total, 0, s))
+        return st;
+    uint64_t bad[2], cnt = 0;
+    UWB_CUDA_TRY(cudaMemcpyAsync(bad, d_bad.p, sizeof(bad), cudaMemcpyDeviceToHost, s));
+    UWB_CUDA_TRY(cudaMemcpyAsync(&cnt, d_cnt.p, sizeof(cnt), cudaMemcpyDeviceToHost, s));
+    UWB_CUDA_TRY(cudaStreamSynchronize(s));
+
+    auto cell_rc = [&](uint64_t idx, int64_t& r, int64_t& c) {
+        r = static_cast<int64_t>(idx / cols);
+        c = static_cast<int64_t>(idx % cols);
+    };
+    if (backend == UWB_INTEGRAL) {
+        if (bad[0] != ~0ull) { // sat.cpp:28-32
+            int64_t r, c;
+            cell_rc(bad[0], r, c);
+            return fail(UWB_INPUT_ERROR, "build_sat: non-finite entry at (" + S(r) + ", " + S(c) + ")", r, c);
+        }
+        if (!params_ok) return validate_params(*p);
+    }
+    if (bad[1] != ~0ull) { // cfar.cpp:85-92
+        int64_t r, c;
+        cell_rc(bad[1], r, c);
+        return fail(UWB_INPUT_ERROR, "cfar2d: cell (" + S(r) + ", " + S(c) + ") is not a finite non-negative power", r, c);
+    }
+    if (degenerate(*p, rows, cols)) return fail(UWB_CONFIGURATION_ERROR, degenerate_msg(*p, rows, cols));
+    if (cnt > cap) {
+        cap = cnt;
+        goto retry;
+    }
+
+    *n_det = cnt;
+    const uint64_t n_copy = std::min(cnt, det_capacity);
+    if (mask) UWB_CUDA_TRY(cudaMemcpyAsync(mask, d_mask.p, cells, cudaMemcpyDeviceToHost, s));
+    if (thresholds) UWB_CUDA_TRY(cudaMemcpyAsync(thresholds, d_thr.p, sizeof(double) * cells, cudaMemcpyDeviceToHost, s));
+    if (dets && n_copy)
+        UWB_CUDA_TRY(cudaMemcpyAsync(dets, d_dets.p, sizeof(uwb_detection) * n_copy, cudaMemcpyDeviceToHost, s));
+    UWB_CUDA_TRY(cudaStreamSynchronize(s));
+    if (cnt > det_capacity) return fail(UWB_CAPACITY_ERROR, "uwb_cfar2d: detection buffer too small");
+    return ok();
+}
+
+// ----------------------------------------------------------- front-end ---
+
+namespace {
+
+// Runs the requested front-end stages on the device. in_host: m x n doubles.
+// Outputs (host, optional): frame_out m x n, band m x kept, full m x bins.
+uwb_status run_frontend(const double* in_host, uint64_t m, uint64_t n, int stages, uint64_t window,
+                        int mode, double eps, uint64_t L, uint64_t first, uint64_t kept, double* frame_out,
+                        double* band_out, double* full_out, bool check_finite, uint64_t* first_nonfinite) {
+    if (uwb_status s = need_device()) return s;
+    cudaStream_t s = host_stream();
+    if (L > 8192 && (stages & 16)) return fail(UWB_INVALID_ARGUMENT, "uwb: fft_length > 8192 not supported on the device path");
+    DevBuf d_in, d_work, d_band, d_full, d_wr, d_wi, d_bad;
+    UWB_CUDA_TRY(d_in.alloc(sizeof(double) * m * n, s));
+    UWB_CUDA_TRY(cudaMemcpyAsync(d_in.p, in_host, sizeof(double) * m * n, cudaMemcpyHostToDevice, s));
+    UWB_CUDA_TRY(d_work.alloc(sizeof(double) * m * n, s));
+    UWB_CUDA_TRY(d_bad.alloc(sizeof(uint64_t), s));
+    UWB_CUDA_TRY(cudaMemsetAsync(d_bad.p, 0xff, sizeof(uint64_t), s));
+    FrontendLaunch F{};
+    F.frame = d_in.p;
+    F.dtype = UWB_F64;
+    F.m = static_cast<int64_t>(m);
+    F.n = static_cast<int64_t>(n);
+    F.work = d_work.as<double>();
+    F.first_nonfinite = check_finite ? d_bad.as<unsigned long long>() : nullptr;
+    F.window = window;
+    F.mode = mode;
+    F.epsilon = eps;
+    F.L = static_cast<int64_t>(L);
+    F.first_bin = static_cast<int64_t>(first);
+    F.kept = static_cast<int64_t>(kept);
+    std::vector<double> wr, wi;
+    if (stages & 16) {
+        twiddles(F.L, wr, wi);
+        UWB_CUDA_TRY(d_wr.alloc(sizeof(double) * L, s));
+        UWB_CUDA_TRY(d_wi.alloc(sizeof(double) * L, s));
+        UWB_CUDA_TRY(cudaMemcpyAsync(d_wr.p, wr.data(), sizeof(double) * L, cudaMemcpyHostToDevice, s));
+        UWB_CUDA_TRY(cudaMemcpyAsync(d_wi.p, wi.data(), sizeof(double) * L, cudaMemcpyHostToDevice, s));
+        F.wr = d_wr.as<double>();
+        F.wi = d_wi.as<double>();
+        if (band_out) {
+            UWB_CUDA_TRY(d_band.alloc(sizeof(double) * m * kept, s));
+            F.band = d_band.as<double>();
+        }
+        if (full_out) {
+            UWB_CUDA_TRY(d_full.alloc(sizeof(double) * m * (L / 2 + 1), s));
+            F.full_power = d_full.as<double>();
+        }
+    }
+    // columns stage (always runs: it also moves the input into the work buffer)
+    F.stage_mask = stages & 3;
+    UWB_CUDA_TRY(launch_frontend_columns(F, s));
+    if (stages & (4 | 8 | 16)) {
+        F.stage_mask = stages & (4 | 8 | 16);
+        UWB_CUDA_TRY(launch_frontend_rows(F, s));
+    }
+    uint64_t bad = ~0ull;
+    UWB_CUDA_TRY(cudaMemcpyAsync(&bad, d_bad.p, sizeof(bad), cudaMemcpyDeviceToHost, s));
+    if (frame_out) UWB_CUDA_TRY(cudaMemcpyAsync(frame_out, d_work.p, sizeof(double) * m * n, cudaMemcpyDeviceToHost, s));
+    if (band_out && (stages & 16))
+        UWB_CUDA_TRY(cudaMemcpyAsync(band_out, d_band.p, sizeof(double) * m * kept, cudaMemcpyDeviceToHost, s));
+    if (full_out && (stages & 16))
+        UWB_CUDA_TRY(cudaMemcpyAsync(full_out, d_full.p, sizeof(double) * m * (L / 2 + 1), cudaMemcpyDeviceToHost, s));
+    UWB_CUDA_TRY(cudaStreamSynchronize(s));
+    if (first_nonfinite) *first_nonfinite = bad;
+    return UWB_OK;
+}
+
+} // namespace
+
+uwb_status uwb_remove_dc(const double* in, uint64_t m, uint64_t n, double* out) {
+    if (m == 0 || n == 0) return ok();
+    if (uwb_status s = run_frontend(in, m, n, 1, 1, 0, 1.0, 0, 0, 0, out, nullptr, nullptr, false, nullptr)) return s;
+    return ok();
+}
+
+uwb_status uwb_detrend_linear(const double* in, uint64_t m, uint64_t n, double* out) {
+    if (m == 0 || n == 0) return ok();
+    if (uwb_status s = run_frontend(in, m, n, 2, 1, 0, 1.0, 0, 0, 0, out, nullptr, nullptr, false, nullptr)) return s;
+    return ok();
+}
+
+uwb_status uwb_mean_filter_slow(const double* in, uint64_t m, uint64_t n, uint64_t window, double* out) {
+    // pipeline.cpp:101-106
+    if (window == 0 || window % 2 == 0 || window > n)
+        return fail(UWB_PARAMETER_ERROR, "mean_filter_slow: window must be odd and in [1, " + S(n) + "], got " + S(window));
+    if (m == 0) return ok();
+    if (uwb_status s = run_frontend(in, m, n, 4, window, 0, 1.0, 0, 0, 0, out, nullptr, nullptr, false, nullptr)) return s;
+    return ok();
+}
+
+uwb_status uwb_subtract_slow_time_mean(const double* in, uint64_t m, uint64_t n, double* out) {
+    if (m == 0 || n == 0) return ok();
+    if (uwb_status s = run_frontend(in, m, n, 4, 1, 1, 1.0, 0, 0, 0, out, nullptr, nullptr, false, nullptr)) return s;
+    return ok();
+}
+
+uwb_status uwb_normalize_slow(const double* in, uint64_t m, uint64_t n, double epsilon, double* out) {
+    if (!(epsilon > 0.0)) return fail(UWB_PARAMETER_ERROR, "normalize_slow: epsilon must be positive");
+    if (m == 0 || n == 0) return ok();
+    if (uwb_status s = run_frontend(in, m, n, 8, 1, 0, epsilon, 0, 0, 0, out, nullptr, nullptr, false, nullptr)) return s;
+    return ok();
+}
+
+uwb_status uwb_slow_time_spectrum(const double* in, uint64_t m, uint64_t n, double fast_rate, double prf,
+                                  uint64_t fft_length, double* power, double* freq_axis, double* range_axis) {
+    if (fft_length < n)
+        return fail(UWB_PARAMETER_ERROR, "slow_time_spectrum: fft_length " + S(fft_length) + " < trace count " + S(n));
+    const uint64_t bins = fft_length / 2 + 1;
+    // pipeline.cpp:169-175 axes (host scalar arithmetic, as the reference)
+    if (freq_axis)
+        for (uint64_t k = 0; k < bins; ++k)
+            freq_axis[k] = static_cast<double>(k) * prf / static_cast<double>(fft_length);
+    if (range_axis)
+        for (uint64_t r = 0; r < m; ++r)
+            range_axis[r] = static_cast<double>(r) * 299792458.0 / (2.0 * fast_rate);
+    if (m == 0) return ok();
+    if (uwb_status s = run_frontend(in, m, n, 16, 1, 0, 1.0, fft_length, 0, 0, nullptr, nullptr, power, false, nullptr))
+        return s;
+    return ok();
+}
+
+uwb_status uwb_band_select(const double* power, uint64_t m, uint64_t bins, const double* freq_axis,
+                           double low, double high, uint64_t* first_out, uint64_t* kept_out,
+                           double* out_power, double* out_freq) {
+    // pipeline.cpp:192-223
+    uint64_t first = bins, last = 0;
+    for (uint64_t k = 0; k < bins; ++k) {
+        const double f = freq_axis[k];
+        if (f >= low && f <= high) {
+            if (first == bins) first = k;
+            last = k;
+        }
+    }
+    if (first == bins) {
+        const double res = bins > 1 ? freq_axis[1] - freq_axis[0] : freq_axis[0];
+        return fail(UWB_CONFIGURATION_ERROR, "band_select: no FFT bin falls in [" + fmt_double(low) + ", " +
+                                                 fmt_double(high) + "] Hz at bin resolution " + fmt_double(res) + " Hz");
+    }
+    const uint64_t kept = last - first + 1;
+    *first_out = first;
+    *kept_out = kept;
+    if (out_freq) std::memcpy(out_freq, freq_axis + first, sizeof(double) * kept);
+    if (out_power && m) {
+        if (uwb_status s = need_device()) return s;
+        UWB_CUDA_TRY(cudaMemcpy2D(out_power, sizeof(double) * kept, power + first, sizeof(double) * bins,
+                                  sizeof(double) * kept, m, cudaMemcpyHostToHost));
+    }
+    return ok();
+}
+
+uwb_status uwb_detect(const double* frame, uint64_t m, uint64_t n, double fast_rate, double prf,
+                      const uwb_pipeline_config* cfg, uint64_t band_capacity, double* band_power,
+                      double* band_freq, double* range_axis, uint64_t* kept_out, uint8_t* mask,
+                      double* thresholds, uwb_detection* dets, uint64_t det_capacity, uint64_t* n_det) {
+    *n_det = 0;
+    *kept_out = 0;
+    // RadarFrame::validate (pipeline.cpp:27-38)
+    if (m < 2 || n < 2)
+        return fail(UWB_DIMENSION_ERROR, "RadarFrame: need at least 2x2 samples, got " + S(m) + "x" + S(n));
+    if (!(fast_rate > 0.0) || !(prf > 0.0))
+        return fail(UWB_PARAMETER_ERROR, "RadarFrame: fast_rate and prf must be positive");
+    if (uwb_status s = need_device()) return s;
+    cudaStream_t s = host_stream();
+
+    const uwb_pipeline_config& c = *cfg;
+    const uint64_t L = c.fft_length == 0 ? next_pow2(n) : c.fft_length;
+    // configuration checks that do not need data; reported after the
+    // finiteness check below to keep the reference's order
+    std::string cfg_msg;
+    uwb_status cfg_status = UWB_OK;
+    if (c.mean_filter_window == 0 || c.mean_filter_window % 2 == 0) {
+        cfg_status = UWB_PARAMETER_ERROR;
+        cfg_msg = "PipelineConfig: mean_filter_window must be odd and positive, got " + S(c.mean_filter_window);
+    } else if (!(c.band_low_hz > 0.0) || !(c.band_low_hz < c.band_high_hz)) {
+        cfg_status = UWB_PARAMETER_ERROR;
+        cfg_msg = "PipelineConfig: need 0 < band_low_hz < band_high_hz";
+    } else if (!(c.normalization_epsilon > 0.0)) {
+        cfg_status = UWB_PARAMETER_ERROR;
+        cfg_msg = "PipelineConfig: normalization_epsilon must be positive";
+    } else if (validate_params(c.cfar) != UWB_OK) {
+        cfg_status = UWB_PARAMETER_ERROR;
+        cfg_msg = g_err.message;
+    } else if (!(c.band_high_hz < prf / 2.0)) {
+        cfg_status = UWB_PARAMETER_ERROR;
+        cfg_msg = "detect: band_high_hz must be below prf/2 = " + fmt_double(prf / 2.0) + " Hz";
+    }
+    const bool smooth = c.mean_filter_mode == 0;
+    std::string stage_msg;
+    uwb_status stage_status = UWB_OK;
+    if (cfg_status == UWB_OK) {
+        if (smooth && (c.mean_filter_window > n)) {
+            stage_status = UWB_PARAMETER_ERROR;
+            stage_msg = "mean_filter_slow: mean_filter_slow: window must be odd and in [1, " + S(n) + "], got " +
+                        S(c.mean_filter_window);
+        } else if (L < n) {
+            stage_status = UWB_PARAMETER_ERROR;
+            stage_msg = "slow_time_spectrum: slow_time_spectrum: fft_length " + S(L) + " < trace count " + S(n);
+        }
+    }
+    uint64_t first = 0, kept = 0;
+    if (cfg_status == UWB_OK && stage_status == UWB_OK) {
+        const uint64_t bins = L / 2 + 1;
+        uint64_t f = bins, l = 0;
+        for (uint64_t k = 0; k < bins; ++k) {
+            const double fr = static_cast<double>(k) * prf / static_cast<double>(L);
+            if (fr >= c.band_low_hz && fr <= c.band_high_hz) {
+                if (f == bins) f = k;
+                l = k;
+            }
+        }
+        if (f == bins) {
+            const double res = bins > 1 ? (1.0 * prf / static_cast<double>(L)) - (0.0 * prf / static_cast<double>(L))
+                                        : 0.0 * prf / static_cast<double>(L);
+            stage_status = UWB_CONFIGURATION_ERROR;
+            stage_msg = "band_select: band_select: no FFT bin falls in [" + fmt_double(c.band_low_hz) + ", " +
+                        fmt_double(c.band_high_hz) + "] Hz at bin resolution " + fmt_double(res) + " Hz";
+        } else {
+            first = f;
+            kept = l - f + 1;
+        }
+    }
+    const bool run_all = cfg_status == UWB_OK && stage_status == UWB_OK;
+    if (run_all && L > 8192) return fail(UWB_INVALID_ARGUMENT, "uwb: fft_length > 8192 not supported on the device path");
+    if (run_all && kept > band_capacity) return fail(UWB_INVALID_ARGUMENT, "uwb_detect: band_capacity too small");
+
+    // ---- device pipeline
+    DevBuf d_in, d_work, d_band, d_wr, d_wi, d_bad;
+    UWB_CUDA_TRY(d_in.alloc(sizeof(double) * m * n, s));
+    UWB_CUDA_TRY(cudaMemcpyAsync(d_in.p, frame, sizeof(double) * m * n, cudaMemcpyHostToDevice, s));
+    UWB_CUDA_TRY(d_work.alloc(sizeof(double) * m * n, s));
+    UWB_CUDA_TRY(d_bad.alloc(sizeof(uint64_t), s));
+    UWB_CUDA_TRY(cudaMemsetAsync(d_bad.p, 0xff, sizeof(uint64_t), s));
+    FrontendLaunch F{};
+    F.frame = d_in.p;
+    F.dtype = UWB_F64;
+    F.m = static_cast<int64_t>(m);
+    F.n = static_cast<int64_t>(n);
+    F.work = d_work.as<double>();
+    F.first_nonfinite = d_bad.as<unsigned long long>();
+    F.window = c.mean_filter_window;
+    F.mode = smooth ? 0 : 1;
+    F.epsilon = c.normalization_epsilon;
+    F.L = static_cast<int64_t>(L);
+    F.first_bin = static_cast<int64_t>(first);
+    F.kept = static_cast<int64_t>(kept);
+    F.stage_mask = 3;
+    UWB_CUDA_TRY(launch_frontend_columns(F, s));
+    std::vector<double> wr, wi;
+    if (run_all) {
+        twiddles(F.L, wr, wi);
+        UWB_CUDA_TRY(d_wr.alloc(sizeof(double) * L, s));
+        UWB_CUDA_TRY(d_wi.alloc(sizeof(double) * L, s));
+        UWB_CUDA_TRY(cudaMemcpyAsync(d_wr.p, wr.data(), sizeof(double) * L, cudaMemcpyHostToDevice, s));
+        UWB_CUDA_TRY(cudaMemcpyAsync(d_wi.p, wi.data(), sizeof(double) * L, cudaMemcpyHostToDevice, s));
+        UWB_CUDA_TRY(d_band.alloc(sizeof(double) * m * kept, s));
+        F.wr = d_wr.as<double>();
+        F.wi = d_wi.as<double>();
+        F.band = d_band.as<double>();
+        F.stage_mask = 4 | 8 | 16;
+        UWB_CUDA_TRY(launch_frontend_rows(F, s));
+    }
+    uint64_t bad = ~0ull;
+    UWB_CUDA_TRY(cudaMemcpyAsync(&bad, d_bad.p, sizeof(bad), cudaMemcpyDeviceToHost, s));
+    UWB_CUDA_TRY(cudaStreamSynchronize(s));
+    if (bad != ~0ull) return fail(UWB_INPUT_ERROR, "RadarFrame: non-finite sample");
+    if (cfg_status) return fail(cfg_status, cfg_msg);
+    if (stage_status) return fail(stage_status, stage_msg);
+
+    // ---- CFAR stage on the band map ("cfar2d: " prefix, pipeline.cpp:269-273)
+    if (band_freq)
+        for (uint64_t k = 0; k < kept; ++k)
+            band_freq[k] = static_cast<double>(first + k) * prf / static_cast<double>(L);
+    if (range_axis)
+        for (uint64_t r = 0; r < m; ++r) range_axis[r] = static_cast<double>(r) * 299792458.0 / (2.0 * fast_rate);
+    if (band_power)
+        UWB_CUDA_TRY(cudaMemcpyAsync(band_power, d_band.p, sizeof(double) * m * kept, cudaMemcpyDeviceToHost, s));
+    *kept_out = kept;
+    if (degenerate(c.cfar, m, kept))
+        return fail(UWB_CONFIGURATION_ERROR, "cfar2d: " + degenerate_msg(c.cfar, m, kept));
+
+    const uint64_t cells = m * kept;
+    const std::vector<double> alpha = alpha_table_host(c.cfar);
+    DevBuf d_alpha, d_mask, d_thr, d_dets, d_cnt, d_fb, d_bits, d_ws;
+    UWB_CUDA_TRY(d_alpha.alloc(sizeof(double) * alpha.size(), s));
+    UWB_CUDA_TRY(cudaMemcpyAsync(d_alpha.p, alpha.data(), sizeof(double) * alpha.size(), cudaMemcpyHostToDevice, s));
+    UWB_CUDA_TRY(d_mask.alloc(cells, s));
+    UWB_CUDA_TRY(d_thr.alloc(sizeof(double) * cells, s));
+    UWB_CUDA_TRY(d_dets.alloc(sizeof(uwb_detection) * cells, s));
+    UWB_CUDA_TRY(d_cnt.alloc(sizeof(uint64_t), s));
+    UWB_CUDA_TRY(d_fb.alloc(sizeof(uint64_t) * 2, s));
+    const uint64_t words = (kept + 31) / 32;
+    UWB_CUDA_TRY(d_bits.alloc(sizeof(uint32_t) * words * m, s));
+    uwb_map_batch b{};
+    b.maps = d_band.p;
+    b.dtype = UWB_F64;
+    b.n_maps = 1;
+    b.rows = m;
+    b.cols = kept;
+    b.ld = kept;
+    b.map_stride = cells;
+    uwb_cfar_outputs o{};
+    o.mask_bits = d_bits.as<uint32_t>();
+    o.words_per_row = words;
+    o.mask_map_stride = words * m;
+    o.mask_u8 = d_mask.as<uint8_t>();
+    o.thresholds = d_thr.as<double>();
+    o.dets = d_dets.as<uwb_detection>();
+    o.det_capacity = cells;
+    o.det_counts = d_cnt.as<uint64_t>();
+    o.first_bad = d_fb.as<uint64_t>();
+    const Plan P = make_plan(b, &c.cfar, UWB_SAT_GLOBAL, 0, static_cast<int64_t>(cells));
+    UWB_CUDA_TRY(d_ws.alloc(P.total, s));
+    const int backend = c.backend == UWB_NAIVE ? UWB_NAIVE : UWB_INTEGRAL;
+    if (uwb_status st = dev_cfar(b, c.cfar, d_alpha.as<double>(), backend, UWB_SAT_GLOBAL, 0, o, d_ws.p, P.total, 0, s))
+        return st;
+    uint64_t cnt = 0, fb[2];
+    UWB_CUDA_TRY(cudaMemcpyAsync(&cnt, d_cnt.p, sizeof(cnt), cudaMemcpyDeviceToHost, s));
+    UWB_CUDA_TRY(cudaMemcpyAsync(fb, d_fb.p, sizeof(fb), cudaMemcpyDeviceToHost, s));
+    UWB_CUDA_TRY(cudaStreamSynchronize(s));
+    if (backend == UWB_INTEGRAL && fb[0] != ~0ull) {
+        const int64_t r = static_cast<int64_t>(fb[0] / kept), cc = static_cast<int64_t>(fb[0] % kept);
+        return fail(UWB_INPUT_ERROR, "cfar2d: build_sat: non-finite entry at (" + S(r) + ", " + S(cc) + ")", r, cc);
+    }
+    if (fb[1] != ~0ull) {
+        const int64_t r = static_cast<int64_t>(fb[1] / kept), cc = static_cast<int64_t>(fb[1] % kept);
+        return fail(UWB_INPUT_ERROR, "cfar2d: cfar2d: cell (" + S(r) + ", " + S(cc) + ") is not a finite non-negative power", r, cc);
+    }
+    *n_det = cnt;
+    if (mask) UWB_CUDA_TRY(cudaMemcpyAsync(mask, d_mask.p, cells, cudaMemcpyDeviceToHost, s));
+    if (thresholds) UWB_CUDA_TRY(cudaMemcpyAsync(thresholds, d_thr.p, sizeof(double) * cells, cudaMemcpyDeviceToHost, s));
+    const uint64_t n_copy = std::min(cnt, det_capacity);
+    if (dets && n_copy)
+        UWB_CUDA_TRY(cudaMemcpyAsync(dets, d_dets.p, sizeof(uwb_detection) * n_copy, cudaMemcpyDeviceToHost, s));
+    UWB_CUDA_TRY(cudaStreamSynchronize(s));
+    if (cnt > det_capacity) return fail(UWB_CAPACITY_ERROR, "uwb_detect: detection buffer too small");
+    return ok();
+}
+
+// ------------------------------------------------- host-buffer batch (e2e) ---
+
+uwb_status uwb_host_cfar2d_batch(const uwb_map_batch* hb, const uwb_cfar_params* p, int32_t sat_mode,
+                                 uint64_t slab_rows, uint32_t* mask_bits, uwb_detection* dets,
+                                 uint64_t det_capacity, uint64_t* det_counts, uint64_t maps_per_chunk) {
+    if (uwb_status s = check_batch(hb)) return s;
+    if (uwb_status s = validate_params(*p)) return s;
+    if (hb->rows == 0 || hb->cols == 0) return fail(UWB_DIMENSION_ERROR, "cfar2d: power map must be at least 1x1");
+    if (degenerate(*p, hb->rows, hb->cols)) return fail(UWB_CONFIGURATION_ERROR, degenerate_msg(*p, hb->rows, hb->cols));
+    if (uwb_status s = need_device()) return s;
+    if (hb->ld != hb->cols || hb->map_stride != hb->rows * hb->cols)
+        return fail(UWB_INVALID_ARGUMENT, "uwb_host_cfar2d_batch: host maps must be dense");
+    const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(maps_per_chunk ? maps_per_chunk : 64, hb->n_maps));
+    const size_t esz = hb->dtype == UWB_F32 ? 4 : 8;
+    const uint64_t cells = hb->rows * hb->cols;
+    const uint64_t words = (hb->cols + 31) / 32;
+    const uint64_t mask_words = words * hb->rows;
+
+    // two pipelines (double buffering): H2D of chunk k+1 overlaps compute/D2H of chunk k
+    constexpr int kPipes = 2;
+    struct StreamSet {
+        cudaStream_t s[kPipes] = {};
+        ~StreamSet() {
+            for (auto x : s)
+                if (x) { cudaStreamSynchronize(x); cudaStreamDestroy(x); }
+        }
+    } streams;
+    cudaStream_t* st = streams.s;
+    for (int i = 0; i < kPipes; ++i) UWB_CUDA_TRY(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking));
+    struct Pipe {
+        DevBuf in, bits, dets, cnt, bad, ws;
+    } pipes[kPipes];
+    uwb_map_batch cb = *hb;
+    cb.n_maps = chunk;
+    const Plan P = make_plan(cb, p, sat_mode, slab_rows, static_cast<int64_t>(det_capacity));
+    const std::vector<double> alpha = alpha_table_host(*p);
+    DevBuf d_alpha;
+    UWB_CUDA_TRY(d_alpha.alloc(sizeof(double) * alpha.size(), st[0]));
+    UWB_CUDA_TRY(cudaMemcpyAsync(d_alpha.p, alpha.data(), sizeof(double) * alpha.size(), cudaMemcpyHostToDevice, st[0]));
+    UWB_CUDA_TRY(cudaStreamSynchronize(st[0]));
+    for (int i = 0; i < kPipes; ++i) {
+        UWB_CUDA_TRY(pipes[i].in.alloc(esz * cells * chunk, st[i]));
+        UWB_CUDA_TRY(pipes[i].bits.alloc(sizeof(uint32_t) * mask_words * chunk, st[i]));
+        UWB_CUDA_TRY(pipes[i].dets.alloc(sizeof(uwb_detection) * std::max<uint64_t>(det_capacity, 1) * chunk, st[i]));
+        UWB_CUDA_TRY(pipes[i].cnt.alloc(sizeof(uint64_t) * chunk, st[i]));
+        UWB_CUDA_TRY(pipes[i].bad.alloc(sizeof(uint64_t) * 2 * chunk, st[i]));
+        UWB_CUDA_TRY(pipes[i].ws.alloc(P.total, st[i]));
+    }
+    uwb_status result = UWB_OK;
+    for (uint64_t m0 = 0, k = 0; m0 < hb->n_maps; m0 += chunk, ++k) {
+        const int i = static_cast<int>(k % kPipes);
+        const uint64_t nm = std::min(chunk, hb->n_maps - m0);
+        Pipe& pp = pipes[i];
+        const char* src = static_cast<const char*>(hb->maps) + esz * cells * m0;
+        UWB_CUDA_TRY(cudaMemcpyAsync(pp.in.p, src, esz * cells * nm, cudaMemcpyHostToDevice, st[i]));
+        uwb_map_batch db = cb;
+        db.maps = pp.in.p;
+        db.n_maps = nm;
+        uwb_cfar_outputs o{};
+        o.mask_bits = pp.bits.as<uint32_t>();
+        o.words_per_row = words;
+        o.mask_map_stride = mask_words;
+        o.dets = pp.dets.as<uwb_detection>();
+        o.det_capacity = det_capacity;
+        o.det_counts = pp.cnt.as<uint64_t>();
+        o.first_bad = pp.bad.as<uint64_t>();
+        if (uwb_status s2 = dev_cfar(db, *p, d_alpha.as<double>(), UWB_INTEGRAL, sat_mode, slab_rows, o, pp.ws.p,
+                                     P.total, 0, st[i]))
+            return s2;
+        if (mask_bits)
+            UWB_CUDA_TRY(cudaMemcpyAsync(mask_bits + mask_words * m0, pp.bits.p, sizeof(uint32_t) * mask_words * nm,
+                                         cudaMemcpyDeviceToHost, st[i]));
+        if (dets && det_capacity)
+            UWB_CUDA_TRY(cudaMemcpyAsync(dets + det_capacity * m0, pp.dets.p, sizeof(uwb_detection) * det_capacity * nm,
+                                         cudaMemcpyDeviceToHost, st[i]));
+        UWB_CUDA_TRY(cudaMemcpyAsync(det_counts + m0, pp.cnt.p, sizeof(uint64_t) * nm, cudaMemcpyDeviceToHost, st[i]));
+    }
+    for (int i = 0; i < kPipes; ++i) UWB_CUDA_TRY(cudaStreamSynchronize(st[i]));
+    for (uint64_t i = 0; i < hb->n_maps; ++i)
+        if (det_counts[i] > det_capacity) result = fail(UWB_CAPACITY_ERROR, "uwb_host_cfar2d_batch: detection buffer too small");
+    return result ? result : ok();
+}
+
+uint64_t uwb_kernel_launches(void) { return g_kernel_launches.load(); }
+
+int32_t uwb_dev_phase_ms(float* out, int32_t max_calls) {
+    std::lock_guard<std::mutex> lk(g_phase.mu);
+    const int n = std::min<int>(g_phase.used, max_calls);
+    for (int i = 0; i < n; ++i) {
+        cudaEvent_t* e = &g_phase.ev[static_cast<size_t>(i) * 4];
+        cudaEventSynchronize(e[3]);
+        cudaEventElapsedTime(&out[3 * i + 0], e[0], e[1]);
+        cudaEventElapsedTime(&out[3 * i + 1], e[1], e[2]);
+        cudaEventElapsedTime(&out[3 * i + 2], e[2], e[3]);
+    }
+    g_phase.used = 0;
+    return n;
+}
+
+void* uwb_host_alloc(uint64_t bytes) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, bytes, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+    return p;
+}
+
+void uwb_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
+} // extern "C"

@@ -1,0 +1,142 @@
+// Launch descriptors shared between the kernels and the host-side C ABI.
+#pragma once
+
+#include <atomic>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "uwbvital_b200.h"
+
+namespace uwb {
+
+// Kernels launched by this library (uwb_kernel_launches()).
+extern std::atomic<uint64_t> g_kernel_launches;
+
+// A batch is split into jobs: job = (map, slab). GLOBAL mode has one slab per
+// map covering all rows; SLAB mode owns rows [s*slab_rows, (s+1)*slab_rows) and
+// builds its table over the owned rows plus `halo` rows on each side (clipped).
+struct JobGeometry {
+    int64_t rows;       // map rows
+    int64_t slab_rows;  // owned rows per slab (== rows in GLOBAL mode)
+    int64_t n_slabs;
+    int64_t halo;       // g_r + b_r in SLAB mode, 0 in GLOBAL mode
+
+    __host__ __device__ int64_t owned_begin(int64_t s) const { return s * slab_rows; }
+    __host__ __device__ int64_t owned_end(int64_t s) const {
+        const int64_t e = (s + 1) * slab_rows;
+        return e < rows ? e : rows;
+    }
+    __host__ __device__ int64_t table_begin(int64_t s) const {
+        const int64_t b = owned_begin(s) - halo;
+        return b > 0 ? b : 0;
+    }
+    __host__ __device__ int64_t table_end(int64_t s) const {
+        const int64_t e = owned_end(s) + halo;
+        return e < rows ? e : rows;
+    }
+    // rows of the largest table (source rows, excluding the zero row)
+    __host__ __device__ int64_t max_table_rows() const {
+        const int64_t r = slab_rows + 2 * halo;
+        return r < rows ? r : rows;
+    }
+};
+
+struct SatLaunch {
+    const void* maps;
+    int64_t ld;          // source row pitch (elements)
+    int64_t map_stride;  // elements between maps
+    int64_t cols;
+    JobGeometry geo;
+    int64_t n_jobs;      // n_maps * n_slabs
+    double* table;       // padded tables, shifted layout
+    int64_t table_ld;
+    int64_t table_stride; // doubles between job tables
+    int64_t strips;
+    double* gedge;       // strips > 1: (n_jobs * strips) edge columns
+    int64_t edge_stride;
+    unsigned* gprog;     // (n_jobs * strips) row counters, zeroed before launch
+    unsigned* tile_counter;
+    unsigned long long* first_bad; // per map 2 slots; slot 0 = first non-finite
+    bool vec_ok;         // 16-byte vector loads legal
+    int elem_bytes;
+};
+
+struct SatJobView {
+    const void* src;
+    int64_t rows;
+    int64_t row0;        // map row of table source row 0
+    double* table;
+    unsigned long long* nonfinite;
+};
+
+__host__ __device__ inline SatJobView sat_job(const SatLaunch& L, int64_t job) {
+    const int64_t m = job / L.geo.n_slabs;
+    const int64_t s = job % L.geo.n_slabs;
+    const int64_t b = L.geo.table_begin(s);
+    SatJobView v;
+    v.src = static_cast<const char*>(L.maps) + (m * L.map_stride + b * L.ld) * L.elem_bytes;
+    v.rows = L.geo.table_end(s) - b;
+    v.row0 = b;
+    v.table = L.table + job * L.table_stride;
+    v.nonfinite = L.first_bad ? L.first_bad + 2 * m : nullptr;
+    return v;
+}
+
+struct CfarLaunch {
+    const void* maps;
+    int64_t ld;
+    int64_t map_stride;
+    int64_t cols;
+    JobGeometry geo;
+    int64_t n_jobs;
+    const double* table;
+    int64_t table_ld;
+    int64_t table_stride;
+    int gr, gc, hr, hc;  // guard radii and outer half-widths (g + b) per axis
+    const double* alpha; // alpha[n], n = 0..n_int
+    // outputs
+    uint32_t* mask_bits;
+    int64_t words_per_row;
+    int64_t mask_map_stride;
+    uint8_t* mask_u8;
+    double* thresholds;
+    uwb_detection* dets;
+    int64_t det_cap;
+    unsigned long long* det_counts;
+    unsigned long long* first_bad;
+    int64_t row_chunks;  // row chunks per job
+    int64_t col_tiles;
+};
+
+cudaError_t launch_sat(const SatLaunch& L, int dtype, cudaStream_t stream);
+int64_t sat_strips(int64_t cols);
+
+cudaError_t launch_cfar_integral(const CfarLaunch& L, int dtype, cudaStream_t stream);
+cudaError_t launch_cfar_naive(const CfarLaunch& L, int dtype, cudaStream_t stream);
+// Sort each map's detection list: value desc, row asc, col asc (cfar.cpp:170-173).
+cudaError_t launch_sort_detections(uwb_detection* dets, int64_t cap,
+                                   const unsigned long long* counts, int64_t n_maps,
+                                   uwb_detection* scratch, cudaStream_t stream);
+
+// Front-end (pipeline.cpp:58-223)
+struct FrontendLaunch {
+    const void* frame;   // m x n, row pitch n
+    int dtype;
+    int64_t m, n;
+    double* work;        // m x n doubles (detrended frame)
+    unsigned long long* first_nonfinite;
+    uint64_t window;     // mean filter window (odd); 1 = identity
+    int mode;            // 0 smoothing, 1 subtract mean
+    double epsilon;
+    int64_t L;           // fft length
+    const double* wr;    // twiddles, L entries
+    const double* wi;
+    int64_t first_bin, kept;
+    double* band;        // m x kept
+    double* full_power;  // optional m x (L/2+1) (slow_time_spectrum)
+    int stage_mask;      // which stages to run (see frontend.cu)
+};
+cudaError_t launch_frontend_columns(const FrontendLaunch& F, cudaStream_t stream);
+cudaError_t launch_frontend_rows(const FrontendLaunch& F, cudaStream_t stream);
+
+} // namespace uwb

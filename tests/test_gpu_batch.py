@@ -1,0 +1,155 @@
+"""GPU parity of the batched device path (BatchCfar, the path bench.py times)
+against the reference (square windows) and the C restatement (per-axis windows,
+row-slab tables), on inputs from the BASELINE.json config generators."""
+import numpy as np
+import pytest
+import torch
+
+from tests.helpers import assert_bitwise
+
+pytestmark = pytest.mark.gpu
+
+
+def _check_map(batch, i, ref_res, what):
+    mask = batch.mask_u8[i].cpu().numpy()
+    thr = batch.thresholds[i].cpu().numpy()
+    assert np.array_equal(mask, ref_res.mask), f"{what}: mask"
+    assert np.array_equal(batch.mask(i), ref_res.mask), f"{what}: bit-packed mask"
+    assert_bitwise(thr, ref_res.threshold_map, f"{what}: thresholds")
+    d = batch.detections(i)
+    r = ref_res.detections
+    assert len(d) == len(r), f"{what}: {len(d)} vs {len(r)} detections"
+    assert np.array_equal(d["row"], r["row"]) and np.array_equal(d["col"], r["col"]), f"{what}: order"
+    assert_bitwise(d["value"], r["value"], f"{what}: values")
+    assert_bitwise(d["threshold"], r["threshold"], f"{what}: det thresholds")
+
+
+def test_cfg3_maps_bit_identical_to_reference(uwb, ref, cuda):
+    """Config 3 maps (1024x1024 fp32, Exp(1) + 32 targets, g2 b8 pfa 1e-4)."""
+    from paper_2012_11077_b200 import synth
+    from paper_2012_11077_b200.batch import BatchCfar
+    n = 6
+    maps = synth.cfg3_maps(n, seed=3, device=cuda)
+    p = uwb.CfarParams(2, 8, 1e-4)
+    b = BatchCfar(n, 1024, 1024, p, torch.float32, det_capacity=1024, want_mask_u8=True, want_thresholds=True)
+    b(maps)
+    torch.cuda.synchronize()
+    b.check_inputs()
+    host = maps.double().cpu().numpy()
+    for i in range(n):
+        _check_map(b, i, ref.cfar2d(host[i], 2, 8, 1e-4, "integral"), f"cfg3 map {i}")
+    assert (b.detection_counts() >= 20).all()  # most of the 32 targets are found
+
+
+def test_cfg1_map_and_sat(uwb, ref, cuda):
+    """Config 1: one fp64 256x512 map, 5 targets at 15 dB, g2 b8 pfa 1e-4; output mask + SAT."""
+    from paper_2012_11077_b200 import synth
+    m = synth.cfg1_map(seed=1, device=cuda).cpu().numpy()
+    got = uwb.cfar2d_integral(m, uwb.CfarParams(2, 8, 1e-4))
+    exp = ref.cfar2d(m, 2, 8, 1e-4, "integral")
+    assert np.array_equal(got.mask, exp.mask)
+    assert_bitwise(got.threshold_map, exp.threshold_map, "cfg1 thresholds")
+    assert_bitwise(uwb.build_sat(m).table(), ref.build_sat(m), "cfg1 SAT")
+    assert len(got.detections) >= 5
+
+
+@pytest.mark.parametrize("win", [((1, 3), (4, 16)), ((3, 1), (16, 4))])
+@pytest.mark.parametrize("pfa", [1e-3, 1e-5])
+def test_cfg5_per_axis_windows_vs_restatement(uwb, oracle, cuda, win, pfa):
+    """Config 5 (K-clutter, non-square windows), scaled to 3 maps of 1024x512."""
+    from paper_2012_11077_b200 import synth
+    from paper_2012_11077_b200.batch import BatchCfar
+    (gr, gc), (br, bc) = win
+    maps = synth.cfg5_maps(3, seed=5, device=cuda, rows=1024, cols=512)
+    p = uwb.CfarParams(guard_radius=gr, background_radius=br, pfa=pfa, guard_cols=gc, background_cols=bc)
+    b = BatchCfar(3, 1024, 512, p, torch.float32, det_capacity=4096, want_mask_u8=True, want_thresholds=True)
+    b(maps)
+    torch.cuda.synchronize()
+    host = maps.double().cpu().numpy()
+    for i in range(3):
+        _check_map(b, i, oracle.cfar(host[i], gr, gc, br, bc, pfa), f"cfg5 map {i}")
+
+
+def test_slab_mode_vs_restatement_and_reference(uwb, ref, oracle, cuda):
+    """Config 4 decomposition (row slabs, slab-local tables, global clamps) on a
+    2048x1024 map with g4 b32 pfa 1e-5: bit-identical to the restatement with the
+    same slabs; vs the reference's global table: masks equal outside a 1e-6 tie
+    band and thresholds within 1e-9 relative."""
+    from paper_2012_11077_b200 import synth
+    from paper_2012_11077_b200.batch import BatchCfar
+    m = synth.cfg4_map(seed=4, device=cuda, rows=2048, cols=1024)
+    p = uwb.CfarParams(4, 32, 1e-5)
+    slab = 512
+    b = BatchCfar(1, 2048, 1024, p, torch.float32, sat_mode="slab", slab_rows=slab, det_capacity=8192,
+                  want_mask_u8=True, want_thresholds=True)
+    b(m.unsqueeze(0).contiguous())
+    torch.cuda.synchronize()
+    host = m.double().cpu().numpy()
+    thr = b.thresholds[0].cpu().numpy()
+    mask = b.mask_u8[0].cpu().numpy()
+    exp_thr = np.zeros_like(host)
+    exp_mask = np.zeros(host.shape, np.uint8)
+    for s0 in range(0, 2048, slab):
+        r = oracle.cfar(host, 4, 4, 32, 32, 1e-5, row_begin=s0, row_end=s0 + slab, slab_local=True)
+        exp_thr[s0:s0 + slab] = r.threshold_map[s0:s0 + slab]
+        exp_mask[s0:s0 + slab] = r.mask[s0:s0 + slab]
+    assert_bitwise(thr, exp_thr, "slab thresholds vs restatement")
+    assert np.array_equal(mask, exp_mask)
+    g = ref.cfar2d(host, 4, 32, 1e-5, "integral")
+    rel = np.abs(thr - g.threshold_map) / np.maximum(g.threshold_map, 1e-300)
+    assert rel.max() < 1e-9
+    tie = np.abs(host - g.threshold_map) <= 1e-6 * g.threshold_map
+    assert np.array_equal(mask[~tie], g.mask[~tie])
+
+
+def test_wide_map_strip_chain_and_big_lists(uwb, ref, cuda):
+    """Maps wider than one 1024-column strip chain their SAT strips; lists longer
+    than one shared-memory sort run use the merge path."""
+    from paper_2012_11077_b200.batch import BatchCfar
+    g = torch.Generator(device="cuda").manual_seed(17)
+    maps = torch.empty((2, 700, 3100), device="cuda", dtype=torch.float32).exponential_(1.0, generator=g)
+    p = uwb.CfarParams(1, 3, 0.05)
+    b = BatchCfar(2, 700, 3100, p, torch.float32, det_capacity=1 << 17, want_mask_u8=True,
+                  want_thresholds=True)
+    b(maps)
+    torch.cuda.synchronize()
+    host = maps.double().cpu().numpy()
+    for i in range(2):
+        _check_map(b, i, ref.cfar2d(host[i], 1, 3, 0.05, "integral"), f"wide map {i}")
+    assert (b.detection_counts() > 2048).all()
+
+
+def test_batch_reports_bad_cells(uwb, cuda):
+    from paper_2012_11077_b200.batch import BatchCfar
+    maps = torch.ones((3, 64, 64), device="cuda")
+    maps[1, 5, 7] = float("nan")
+    maps[2, 9, 1] = -1.0
+    b = BatchCfar(3, 64, 64, uwb.CfarParams(1, 2, 1e-3), torch.float32)
+    b(maps)
+    torch.cuda.synchronize()
+    fb = b.first_bad.cpu().numpy().astype(np.uint64)
+    assert fb[1, 0] == 5 * 64 + 7 and fb[2, 1] == 9 * 64 + 1
+    with pytest.raises(uwb.InputError) as e:
+        b.check_inputs()
+    assert str(e.value) == "build_sat: non-finite entry at (5, 7)"
+
+
+def test_host_batch_e2e_matches_device_batch(uwb, cuda):
+    from paper_2012_11077_b200 import synth
+    from paper_2012_11077_b200.batch import BatchCfar, host_cfar2d_batch
+    n = 10
+    maps = synth.cfg3_maps(n, seed=33, device=cuda)
+    p = uwb.CfarParams(2, 8, 1e-4)
+    b = BatchCfar(n, 1024, 1024, p, torch.float32, det_capacity=512)
+    b(maps)
+    torch.cuda.synchronize()
+    host_in = maps.cpu().pin_memory()
+    bits = torch.zeros((n, 1024, 32), dtype=torch.int32).pin_memory()
+    dets = torch.zeros((n, 512, 32), dtype=torch.uint8).pin_memory()
+    counts = torch.zeros(n, dtype=torch.int64).pin_memory()
+    host_cfar2d_batch(host_in, p, bits, dets, counts, 512, maps_per_chunk=3)
+    assert torch.equal(bits, b.mask_bits.cpu())
+    assert torch.equal(counts, b.counts.cpu())
+    for i in range(n):
+        k = int(counts[i])
+        assert torch.equal(dets[i, :k], b.dets[i, :k].cpu())
