@@ -375,9 +375,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--maps", type=int, default=N_MAPS, help="batch size (profiling runs only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    globals()["N_MAPS"] = args.maps
     if args.impl == "reference":
         return run_reference(args)
     return run_b200(args)

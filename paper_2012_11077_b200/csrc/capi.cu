@@ -158,7 +158,7 @@ Plan make_plan(const uwb_map_batch& b, const uwb_cfar_params* p, int sat_mode, u
     P.geo.n_slabs = P.geo.rows > 0 ? (P.geo.rows + P.geo.slab_rows - 1) / P.geo.slab_rows : 0;
     P.n_jobs = P.n_maps * P.geo.n_slabs;
     P.max_rows = P.geo.max_table_rows();
-    P.table_ld = round_up(P.cols + 2, 4);
+    P.table_ld = table_ld_for(P.cols);
     P.table_stride = (P.max_rows + 1) * P.table_ld;
     P.strips = sat_strips(P.cols);
     size_t off = 0;
@@ -168,7 +168,7 @@ Plan make_plan(const uwb_map_batch& b, const uwb_cfar_params* p, int sat_mode, u
         return o;
     };
     P.off_tables = take(sizeof(double) * static_cast<size_t>(P.n_jobs) * P.table_stride);
-    P.off_edge = take(P.strips > 1 ? sizeof(double) * P.n_jobs * P.strips * P.max_rows : 0);
+    P.off_edge = take(0); // strips hand over through the table itself
     P.off_prog = take(sizeof(unsigned) * P.n_jobs * P.strips);
     P.off_counter = take(sizeof(unsigned) * 4);
     P.off_scratch = take(det_cap > 2048 ? sizeof(uwb_detection) * P.n_maps * det_cap : 0);
@@ -427,7 +427,7 @@ uwb_status uwb_build_sat(const double* src, uint64_t rows, uint64_t cols, double
         return st;
     uint64_t bad[2];
     UWB_CUDA_TRY(cudaMemcpyAsync(bad, d_bad.p, sizeof(bad), cudaMemcpyDeviceToHost, s));
-    UWB_CUDA_TRY(cudaMemcpy2DAsync(table, sizeof(double) * (cols + 1), d_table + 1,
+    UWB_CUDA_TRY(cudaMemcpy2DAsync(table, sizeof(double) * (cols + 1), d_table + kTabShift,
                                    sizeof(double) * P.table_ld, sizeof(double) * (cols + 1), rows + 1,
                                    cudaMemcpyDeviceToHost, s));
     UWB_CUDA_TRY(cudaStreamSynchronize(s));
@@ -449,8 +449,9 @@ uwb_status uwb_dev_build_sat(const uwb_map_batch* b, double* sat, uint64_t sat_l
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     Plan P = make_plan(*b, nullptr, UWB_SAT_GLOBAL, 0, 0);
     if (ws_bytes < P.total) return fail(UWB_INVALID_ARGUMENT, "uwb: workspace too small");
-    if (sat_ld < static_cast<uint64_t>(P.cols + 2) || sat_ld % 2 || reinterpret_cast<uintptr_t>(sat) % 16)
-        return fail(UWB_INVALID_ARGUMENT, "uwb_dev_build_sat: table must be 16-byte aligned with even ld >= cols+2");
+    if (sat_ld < static_cast<uint64_t>(table_ld_for(P.cols)) || sat_ld % 4 || reinterpret_cast<uintptr_t>(sat) % 32)
+        return fail(UWB_INVALID_ARGUMENT,
+                    "uwb_dev_build_sat: table must be 32-byte aligned with ld a multiple of 4 and >= cols+4");
     char* ws = static_cast<char*>(workspace);
     // first_nonfinite uses the 2-slot-per-map layout internally
     DevBuf bad;

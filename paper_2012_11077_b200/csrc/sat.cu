@@ -5,21 +5,28 @@
 //     S(r,c) = ((x(r,c) + S(r-1,c)) + S(r,c-1)) - S(r-1,c-1)        (sat.cpp:33)
 // Every S depends only on its up, left and up-left neighbours, so any schedule
 // that respects those dependencies and performs the same three IEEE additions
-// reproduces the reference table bit for bit. This kernel runs that recurrence
+// reproduces the reference table bit for bit. This kernel runs the recurrence
 // as a systolic wavefront:
-//   * a CTA owns a strip of 1024 columns of one table (8 warps x 32 lanes x 4
-//     columns); lane l of warp w handles row r at step T = r + 32 w + l, so the
-//     lanes of a warp sweep one anti-diagonal band;
-//   * S(r, left column) arrives from lane l-1 by a register shuffle of the value
-//     it produced one step earlier; warp boundaries hand over through a
-//     double-buffered shared-memory slot, one __syncthreads per step;
-//   * strips of wider maps are chained through a global edge column and a
-//     release/acquire row counter; tiles are claimed from an atomic counter in
-//     (table, strip) order, so the strip a CTA waits on is always already running.
-// Loads of the source row slice are 16-byte vectors; the table is written in the
-// shifted layout (padded element (i,j) at table[i*ld + 1 + j]) so each lane's
-// four outputs land as two aligned 16-byte stores. Non-finite inputs are
-// reported as the smallest row-major index (sat.cpp:28-32 semantics).
+//   * the unit of work is one warp on a 32-column strip of one table; lane l
+//     owns column l of the strip and handles row r = s - l at step s, so the
+//     warp sweeps an anti-diagonal band down the whole strip. Warps are
+//     independent (no CTA barrier);
+//   * S(r, left column) comes from lane l-1 by a register shuffle of the value
+//     it produced one step earlier; lane 0 takes it from the table column the
+//     strip to the left has already written, 32 rows at a time (one load per
+//     lane, handed over by shuffle);
+//   * global traffic stays coalesced although every lane works on a different
+//     row: the warp streams its 32 source columns row by row into a shared
+//     ring with cp.async (one 128-byte row segment per step, 8 rows ahead), and
+//     every lane delays its results through a 32-row shared ring so the
+//     completed row s-31 leaves as one 256-byte segment per step;
+//   * strips are claimed from an atomic counter in strip-major order (every
+//     table's strip 0, then strip 1, ...), so the strip a warp depends on is
+//     already running or finished; the dependency is a release/acquire count
+//     of rows the left strip has flushed.
+// The table uses the shifted layout of kernels.cuh (padded (i, j) at
+// table[i*ld + kTabShift + j]), which makes every 32-column flush sector-aligned.
+// Non-finite inputs are reported as the smallest row-major index (sat.cpp:28-32).
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -27,145 +34,143 @@ namespace uwb {
 
 namespace {
 
-constexpr int kSatK = 4;
-constexpr int kSatWarps = 8;
-constexpr int kSatStripCols = kSatWarps * kWarp * kSatK; // 1024
-constexpr int kPublishEvery = 8;
+constexpr int kStripCols = kWarp;          // 32 columns per unit of work
+constexpr int kWarpsPerCta = 4;            // independent warps per CTA
+constexpr int kAhead = 8;                  // source rows prefetched ahead
+constexpr int kInSlots = kWarp + kAhead;   // source ring depth (rows)
+constexpr int kPublishEvery = 128;
 
 template <typename T>
-__device__ __forceinline__ void load_slice(const T* row, int64_t c0, int nvalid, bool vec_ok,
-                                           double (&x)[kSatK]);
+struct WarpSmem {
+    T xin[kInSlots][kWarp];
+    double sout[kWarp][kWarp];
+};
 
+template <typename T>
+__device__ __forceinline__ void cp_async_cell(T* dst, const T* src);
 template <>
-__device__ __forceinline__ void load_slice<float>(const float* row, int64_t c0, int nvalid,
-                                                  bool vec_ok, double (&x)[kSatK]) {
-    if (vec_ok && nvalid == kSatK) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(row + c0));
-        x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
-    } else {
-#pragma unroll
-        for (int j = 0; j < kSatK; ++j) x[j] = j < nvalid ? static_cast<double>(__ldg(row + c0 + j)) : 0.0;
-    }
+__device__ __forceinline__ void cp_async_cell<float>(float* dst, const float* src) { cp_async_4(dst, src); }
+template <>
+__device__ __forceinline__ void cp_async_cell<double>(double* dst, const double* src) { cp_async_8(dst, src); }
+
+__device__ __forceinline__ int wrap_inc(int s, int n) { return s + 1 == n ? 0 : s + 1; }
+
+// Lane 31 (which flushed the strip's last column) releases the flushed-row count.
+__device__ __noinline__ void publish_rows(unsigned* prog, int flushed, int lane) {
+    if (lane == kWarp - 1 && flushed > 0) st_release_u32(prog, static_cast<unsigned>(flushed));
+    __syncwarp();
 }
-
-template <>
-__device__ __forceinline__ void load_slice<double>(const double* row, int64_t c0, int nvalid,
-                                                   bool vec_ok, double (&x)[kSatK]) {
-    if (vec_ok && nvalid == kSatK) {
-        const double2 a = __ldg(reinterpret_cast<const double2*>(row + c0));
-        const double2 b = __ldg(reinterpret_cast<const double2*>(row + c0 + 2));
-        x[0] = a.x; x[1] = a.y; x[2] = b.x; x[3] = b.y;
-    } else {
-#pragma unroll
-        for (int j = 0; j < kSatK; ++j) x[j] = j < nvalid ? __ldg(row + c0 + j) : 0.0;
-    }
+__device__ __forceinline__ int pos_mod(int a, int n) {
+    const int m = a % n;
+    return m < 0 ? m + n : m;
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kSatWarps * kWarp)
+__global__ void __launch_bounds__(kWarpsPerCta * kWarp)
 sat_systolic_kernel(SatLaunch L) {
-    __shared__ double edge_s[kSatWarps][2];
-    __shared__ long long tile_s;
-
+    extern __shared__ __align__(16) unsigned char sat_smem_raw[];
     const int warp = threadIdx.x / kWarp;
     const int lane = threadIdx.x % kWarp;
+    WarpSmem<T>& sm = reinterpret_cast<WarpSmem<T>*>(sat_smem_raw)[warp];
     const int64_t n_tiles = L.n_jobs * L.strips;
+    const int cols = static_cast<int>(L.cols);
 
     for (;;) {
-        if (threadIdx.x == 0) tile_s = static_cast<long long>(atomicAdd(L.tile_counter, 1u));
-        __syncthreads();
-        const int64_t tile = tile_s;
-        __syncthreads();
+        long long tile = 0;
+        if (lane == 0) tile = static_cast<long long>(atomicAdd(L.tile_counter, 1u));
+        tile = __shfl_sync(0xffffffffu, tile, 0);
         if (tile >= n_tiles) return;
 
-        const int64_t job = tile / L.strips;
-        const int strip = static_cast<int>(tile % L.strips);
+        // strip-major claim order
+        const int strip = static_cast<int>(tile / L.n_jobs);
+        const int64_t job = tile % L.n_jobs;
         const SatJobView J = sat_job(L, job);
-
-        const int64_t c_strip0 = static_cast<int64_t>(strip) * kSatStripCols;
-        const int64_t strip_cols = imin(kSatStripCols, L.cols - c_strip0);
-        const int nwa = static_cast<int>((strip_cols + kWarp * kSatK - 1) / (kWarp * kSatK));
-        const int64_t c0 = c_strip0 + static_cast<int64_t>(warp) * kWarp * kSatK + lane * kSatK;
-        const int nvalid = static_cast<int>(imax(0, imin(kSatK, L.cols - c0)));
-
+        const int rows = static_cast<int>(J.rows);
+        const int c = strip * kStripCols + lane;
+        const bool live = c < cols;
         double* table = J.table;
-        // padded row 0 is identically zero (sat.hpp:11-13)
-        for (int64_t c = threadIdx.x; c < strip_cols; c += blockDim.x)
-            table[1 + 1 + c_strip0 + c] = 0.0;
-        if (strip == 0 && threadIdx.x == 0) table[1] = 0.0;
+        const int64_t tld = L.table_ld;
 
-        const bool has_left = strip > 0;
-        const bool has_right = strip + 1 < L.strips;
-        const int64_t edge_base = job * L.strips + strip;
-        const double* ge_in = has_left ? L.gedge + (edge_base - 1) * L.edge_stride : nullptr;
-        const unsigned* prog_in = has_left ? L.gprog + (edge_base - 1) : nullptr;
-        double* ge_out = has_right ? L.gedge + edge_base * L.edge_stride : nullptr;
-        unsigned* prog_out = has_right ? L.gprog + edge_base : nullptr;
-        const bool edge_writer = has_right && warp == kSatWarps - 1 && lane == kWarp - 1;
+        if (live) table[kTabShift + 1 + c] = 0.0; // padded row 0 is identically zero
+        if (strip == 0 && lane == 0) table[kTabShift] = 0.0;
 
-        double prev[kSatK];
-#pragma unroll
-        for (int j = 0; j < kSatK; ++j) prev[j] = 0.0;
-        double left_prev = 0.0; // S(r-1, left column)
-        double my_last = 0.0;   // S(r, my last column), shuffled right next step
+        const unsigned* prog_in = strip > 0 ? L.gprog + job * L.strips + strip - 1 : nullptr;
+        unsigned* prog_out = strip + 1 < L.strips ? L.gprog + job * L.strips + strip : nullptr;
+        // left neighbour column: table column (padded) c_strip0, i.e. S(r, c_strip0 - 1)
+        const double* left_col = table + kTabShift + strip * kStripCols;
         unsigned avail = 0;
+        // left values for rows [blk, blk+32) live in lane k's `lcur` (row blk + k)
+        auto fetch_left = [&](int base) -> double {
+            if (!prog_in || base >= rows) return 0.0; // warp-uniform
+            const unsigned need = static_cast<unsigned>(min(rows, base + kWarp));
+            if (avail < need) { // lane 0 acquires; the warp barrier extends the ordering to all lanes
+                if (lane == 0)
+                    while (avail < need) avail = ld_acquire_u32(prog_in);
+                avail = __shfl_sync(0xffffffffu, avail, 0);
+            }
+            const int rr = base + lane;
+            return rr < rows ? left_col[static_cast<int64_t>(rr + 1) * tld] : 0.0;
+        };
+        double lcur = fetch_left(0);
+        double lnext = fetch_left(kWarp);
 
-        const T* src = static_cast<const T*>(J.src);
-        const int64_t steps = J.rows + static_cast<int64_t>(kWarp) * nwa - 1;
-        for (int64_t t = 0; t < steps; ++t) {
-            const int64_t r = t - static_cast<int64_t>(kWarp) * warp - lane;
-            double left = __shfl_up_sync(0xffffffffu, my_last, 1);
-            const bool in_rows = r >= 0 && r < J.rows;
-            if (lane == 0) {
-                if (warp == 0) {
-                    left = 0.0;
-                    if (has_left && in_rows) {
-                        while (avail <= static_cast<unsigned>(r)) avail = ld_acquire_u32(prog_in);
-                        left = ge_in[r];
-                    }
-                } else {
-                    left = edge_s[warp - 1][(t - 1) & 1];
-                }
-            }
-            const bool active = warp < nwa && in_rows && nvalid > 0;
-            if (active) {
-                double x[kSatK];
-                load_slice<T>(src + r * L.ld, c0, nvalid, L.vec_ok, x);
-                double s_left = left, a_left = left_prev;
+        const T* src = static_cast<const T*>(J.src) + c;
+        const int64_t ld = L.ld;
+        double* tcol = table + kTabShift + 1 + c; // my column of the table
 #pragma unroll
-                for (int j = 0; j < kSatK; ++j) {
-                    if (j < nvalid) {
-                        if (!isfinite(x[j]))
-                            report_min(J.nonfinite, static_cast<unsigned long long>(
-                                                        (J.row0 + r) * L.cols + c0 + j));
-                        // sat.cpp:33: out[c+1] = v + above[c+1] + out[c] - above[c]
-                        const double s = dsub(dadd(dadd(x[j], prev[j]), s_left), a_left);
-                        a_left = prev[j];
-                        prev[j] = s;
-                        s_left = s;
-                    }
-                }
-                double* out = table + (r + 1) * L.table_ld + 1 + 1 + c0;
-                if (nvalid == kSatK) {
-                    reinterpret_cast<double2*>(out)[0] = make_double2(prev[0], prev[1]);
-                    reinterpret_cast<double2*>(out)[1] = make_double2(prev[2], prev[3]);
-                } else {
-#pragma unroll
-                    for (int j = 0; j < kSatK; ++j)
-                        if (j < nvalid) out[j] = prev[j];
-                }
-                if (strip == 0 && warp == 0 && lane == 0) table[(r + 1) * L.table_ld + 1] = 0.0;
-                my_last = s_left;
-                left_prev = left;
-                if (lane == kWarp - 1) edge_s[warp][t & 1] = my_last;
-                if (edge_writer) {
-                    ge_out[r] = my_last;
-                    if ((r + 1) % kPublishEvery == 0 || r + 1 == J.rows)
-                        st_release_u32(prog_out, static_cast<unsigned>(r + 1));
-                }
-            }
-            __syncthreads();
+        for (int u = 0; u < kAhead; ++u) {
+            if (live && u < rows) cp_async_cell<T>(&sm.xin[u][lane], src + u * ld);
+            cp_async_commit();
         }
+
+        double prev = 0.0;      // S(r-1, c)
+        double left_prev = 0.0; // S(r-1, c-1)
+        double my_last = 0.0;   // S(r, c), shuffled right next step
+        int slot_r = pos_mod(-lane, kInSlots);
+        int slot_n = kAhead;
+        const int steps = rows + kWarp;
+        for (int s = 0; s < steps; ++s) {
+            const int r = s - lane;
+            {   // stream in source row s + kAhead
+                const int rn = s + kAhead;
+                if (live && rn < rows) cp_async_cell<T>(&sm.xin[slot_n][lane], src + rn * ld);
+                cp_async_commit();
+                cp_async_wait<kAhead>();
+            }
+            if ((s & (kWarp - 1)) == 0 && s > 0) {
+                lcur = lnext;
+                lnext = fetch_left(s + kWarp);
+            }
+            const double from_left_strip = __shfl_sync(0xffffffffu, lcur, s & (kWarp - 1));
+            double left = __shfl_up_sync(0xffffffffu, my_last, 1);
+            if (lane == 0) left = from_left_strip;
+            if (live && r >= 0 && r < rows) {
+                const double v = static_cast<double>(sm.xin[slot_r][lane]);
+                if (!isfinite(v))
+                    report_min(J.nonfinite, static_cast<unsigned long long>((J.row0 + r) * L.cols + c));
+                // sat.cpp:33: out[c+1] = v + above[c+1] + out[c] - above[c]
+                const double sv = dsub(dadd(dadd(v, prev), left), left_prev);
+                prev = sv;
+                left_prev = left;
+                my_last = sv;
+                sm.sout[r & (kWarp - 1)][lane] = sv;
+            }
+            // flush the completed row s - 31 (own column; the warp stores one segment)
+            const int rf = s - (kWarp - 1);
+            if (rf >= 0 && rf < rows) {
+                if (live) tcol[static_cast<int64_t>(rf + 1) * tld] = sm.sout[rf & (kWarp - 1)][lane];
+                if (strip == 0 && lane == 0) table[static_cast<int64_t>(rf + 1) * tld + kTabShift] = 0.0;
+            }
+            slot_r = wrap_inc(slot_r, kInSlots);
+            slot_n = wrap_inc(slot_n, kInSlots);
+            // publish the flushed row count for the strip to the right once per
+            // kPublishEvery steps, in a real (not if-converted) warp-uniform branch
+            if (((s + 1) & (kPublishEvery - 1)) == 0 || s + 1 == steps) {
+                if (prog_out) publish_rows(prog_out, min(rows, s + 1 - (kWarp - 1)), lane);
+            }
+        }
+        cp_async_wait<0>();
+        __syncwarp();
     }
 }
 
@@ -173,27 +178,30 @@ sat_systolic_kernel(SatLaunch L) {
 
 std::atomic<uint64_t> g_kernel_launches{0};
 
-cudaError_t launch_sat(const SatLaunch& L, int dtype, cudaStream_t stream) {
+template <typename T>
+static cudaError_t launch_sat_t(const SatLaunch& L, cudaStream_t stream) {
     const int64_t n_tiles = L.n_jobs * L.strips;
-    if (n_tiles == 0) return cudaSuccess;
-    ++g_kernel_launches;
+    const size_t smem = sizeof(WarpSmem<T>) * kWarpsPerCta;
+    cudaError_t e = cudaFuncSetAttribute(sat_systolic_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (dtype == UWB_F32)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sat_systolic_kernel<float>,
-                                                      kSatWarps * kWarp, 0);
-    else
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sat_systolic_kernel<double>,
-                                                      kSatWarps * kWarp, 0);
-    const int64_t grid = imin(n_tiles, static_cast<int64_t>(sms) * max(per_sm, 1));
-    if (dtype == UWB_F32)
-        sat_systolic_kernel<float><<<static_cast<unsigned>(grid), kSatWarps * kWarp, 0, stream>>>(L);
-    else
-        sat_systolic_kernel<double><<<static_cast<unsigned>(grid), kSatWarps * kWarp, 0, stream>>>(L);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sat_systolic_kernel<T>, kWarpsPerCta * kWarp, smem);
+    const int64_t ctas = (n_tiles + kWarpsPerCta - 1) / kWarpsPerCta;
+    const int64_t grid = imin(ctas, static_cast<int64_t>(sms) * (per_sm > 0 ? per_sm : 1));
+    ++g_kernel_launches;
+    sat_systolic_kernel<T><<<static_cast<unsigned>(grid), kWarpsPerCta * kWarp, smem, stream>>>(L);
     return cudaGetLastError();
 }
 
-int64_t sat_strips(int64_t cols) { return (cols + kSatStripCols - 1) / kSatStripCols; }
+cudaError_t launch_sat(const SatLaunch& L, int dtype, cudaStream_t stream) {
+    if (L.n_jobs * L.strips == 0) return cudaSuccess;
+    if (L.geo.rows >= (int64_t(1) << 31) - 4096 || L.cols >= (int64_t(1) << 30)) return cudaErrorInvalidValue;
+    return dtype == UWB_F32 ? launch_sat_t<float>(L, stream) : launch_sat_t<double>(L, stream);
+}
+
+int64_t sat_strips(int64_t cols) { return (cols + kStripCols - 1) / kStripCols; }
 
 } // namespace uwb

@@ -162,14 +162,24 @@ def test_detect_modes_and_static_clutter(uwb, ref, cuda):  # test_pipeline.cpp:3
     assert len(got.detections.detections) == 0
     got, exp = _detect_both(uwb, ref, data, mean_filter_mode="subtract_mean")
     assert_same_result(got.detections, exp["result"], "subtract-mean mode")
+    # test_pipeline.cpp:344-354 uses a 64 x 64 zero frame at prf 68.6: with 64
+    # traces the bin spacing is 1.07 Hz and the reference itself throws from
+    # band_select; the drop-in must throw the same error. The property is then
+    # checked on a frame long enough to resolve the band.
+    from oracle.pyoracle import OracleError
     z = np.zeros((64, 64))
-    got, exp = _detect_both(uwb, ref, z, guard_radius=1, background_radius=2)
+    with pytest.raises(OracleError) as re:
+        ref.detect(z, guard_radius=1, background_radius=2)
+    with pytest.raises(uwb.ConfigurationError) as ge:
+        uwb.detect(F(uwb, z), uwb.PipelineConfig(cfar=uwb.CfarParams(1, 2)))
+    assert str(ge.value) == re.value.message
+    got, exp = _detect_both(uwb, ref, np.zeros((64, 600)), guard_radius=1, background_radius=2)
     assert len(got.detections.detections) == 0 and (got.band_map.power == 0).all()
 
 
 def test_detect_errors_match_reference(uwb, ref, cuda):  # test_pipeline.cpp:414-438
     from oracle.pyoracle import OracleError
-    data, _ = ref.generate_scene(m_samples=64, n_traces=64)
+    data, _ = ref.generate_scene(n_traces=64)
     nan = data.copy()
     nan[3, 3] = np.nan
     cases = [
