@@ -202,9 +202,9 @@ uwb_status uwb_dev_cfar2d(const uwb_map_batch* batch, const uwb_cfar_params* par
 
 /* The global (M+1)x(N+1) tables of a batch in the device layout used by the
  * CFAR kernels: map i's padded element (i_r, j) at sat[i*sat_map_stride +
- * i_r*sat_ld + 3 + j] (the three-element shift puts every 32-column group of a
- * row on whole 32-byte sectors). sat must be 32-byte aligned and sat_ld a
- * multiple of 4 with sat_ld >= cols + 4. */
+ * i_r*sat_ld + 31 + j] (the 31-element shift puts every 32-column group of a
+ * row on two whole 128-byte lines). sat must be 256-byte aligned and sat_ld a
+ * multiple of 32 with sat_ld >= cols + 32. */
 uwb_status uwb_dev_build_sat(const uwb_map_batch* batch, double* sat, uint64_t sat_ld,
                              uint64_t sat_map_stride, uint64_t* first_nonfinite,
                              void* workspace, uint64_t workspace_bytes, void* stream);

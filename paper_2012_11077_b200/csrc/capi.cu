@@ -449,9 +449,10 @@ uwb_status uwb_dev_build_sat(const uwb_map_batch* b, double* sat, uint64_t sat_l
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     Plan P = make_plan(*b, nullptr, UWB_SAT_GLOBAL, 0, 0);
     if (ws_bytes < P.total) return fail(UWB_INVALID_ARGUMENT, "uwb: workspace too small");
-    if (sat_ld < static_cast<uint64_t>(table_ld_for(P.cols)) || sat_ld % 4 || reinterpret_cast<uintptr_t>(sat) % 32)
+    if (sat_ld < static_cast<uint64_t>(table_ld_for(P.cols)) || sat_ld % kTabAlign ||
+        reinterpret_cast<uintptr_t>(sat) % 256)
         return fail(UWB_INVALID_ARGUMENT,
-                    "uwb_dev_build_sat: table must be 32-byte aligned with ld a multiple of 4 and >= cols+4");
+                    "uwb_dev_build_sat: table must be 256-byte aligned with ld a multiple of 32 and >= cols+32");
     char* ws = static_cast<char*>(workspace);
     // first_nonfinite uses the 2-slot-per-map layout internally
     DevBuf bad;

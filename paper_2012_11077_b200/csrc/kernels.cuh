@@ -14,11 +14,14 @@ extern std::atomic<uint64_t> g_kernel_launches;
 
 // Device table layout ("shifted pitched"): padded element (i, j) of the
 // (M+1) x (N+1) summed-area table lives at table[i * ld + kTabShift + j], with
-// ld a multiple of 4 doubles. S(r, c) = padded (r+1, c+1) then sits at index
-// (r+1)*ld + 4 + c, so the 32 values a warp writes for columns 32k..32k+31 fill
-// eight whole 32-byte sectors (no read-modify-write in L2).
-constexpr int kTabShift = 3;
-__host__ __device__ constexpr int64_t table_ld_for(int64_t cols) { return (cols + kTabShift + 1 + 3) / 4 * 4; }
+// ld a multiple of 32 doubles. S(r, c) = padded (r+1, c+1) then sits at index
+// (r+1)*ld + 32 + c, so the 32 values a warp writes for columns 32k..32k+31
+// fill two whole, 256-byte aligned L2 lines (no partial-line write-back).
+constexpr int kTabShift = 31;
+constexpr int kTabAlign = 32;
+__host__ __device__ constexpr int64_t table_ld_for(int64_t cols) {
+    return (cols + kTabShift + 1 + kTabAlign - 1) / kTabAlign * kTabAlign;
+}
 
 // A batch is split into jobs: job = (map, slab). GLOBAL mode has one slab per
 // map covering all rows; SLAB mode owns rows [s*slab_rows, (s+1)*slab_rows) and

@@ -20,13 +20,18 @@
 //     ring with cp.async (one 128-byte row segment per step, 8 rows ahead), and
 //     every lane delays its results through a 32-row shared ring so the
 //     completed row s-31 leaves as one 256-byte segment per step;
-//   * strips are claimed from an atomic counter in strip-major order (every
-//     table's strip 0, then strip 1, ...), so the strip a warp depends on is
-//     already running or finished; the dependency is a release/acquire count
-//     of rows the left strip has flushed.
+//   * strips are claimed from an atomic counter in pair-major order: strips
+//     2p and 2p+1 of a table are claimed back to back (so the two halves of
+//     each 256-byte source segment are read close together and stay in L2),
+//     and every table's pair p precedes any table's pair p+1. The strip a warp
+//     depends on is therefore already running or finished; the dependency is a
+//     release/acquire count of rows the left strip has flushed.
 // The table uses the shifted layout of kernels.cuh (padded (i, j) at
-// table[i*ld + kTabShift + j]), which makes every 32-column flush sector-aligned.
+// table[i*ld + kTabShift + j]), which makes every 32-column flush line-aligned.
 // Non-finite inputs are reported as the smallest row-major index (sat.cpp:28-32).
+#include <climits>
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -38,7 +43,7 @@ constexpr int kStripCols = kWarp;          // 32 columns per unit of work
 constexpr int kWarpsPerCta = 4;            // independent warps per CTA
 constexpr int kAhead = 8;                  // source rows prefetched ahead
 constexpr int kInSlots = kWarp + kAhead;   // source ring depth (rows)
-constexpr int kPublishEvery = 128;
+constexpr int kPublishEvery = 64;
 
 template <typename T>
 struct WarpSmem {
@@ -47,22 +52,42 @@ struct WarpSmem {
 };
 
 template <typename T>
-__device__ __forceinline__ void cp_async_cell(T* dst, const T* src);
+__device__ __forceinline__ void cp_async_cell(unsigned dst, const T* src);
 template <>
-__device__ __forceinline__ void cp_async_cell<float>(float* dst, const float* src) { cp_async_4(dst, src); }
+__device__ __forceinline__ void cp_async_cell<float>(unsigned dst, const float* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
 template <>
-__device__ __forceinline__ void cp_async_cell<double>(double* dst, const double* src) { cp_async_8(dst, src); }
-
-__device__ __forceinline__ int wrap_inc(int s, int n) { return s + 1 == n ? 0 : s + 1; }
+__device__ __forceinline__ void cp_async_cell<double>(unsigned dst, const double* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+template <typename T>
+__device__ __forceinline__ double lds_x(unsigned addr);
+template <>
+__device__ __forceinline__ double lds_x<float>(unsigned addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return static_cast<double>(v);
+}
+template <>
+__device__ __forceinline__ double lds_x<double>(unsigned addr) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void sts_f64(unsigned addr, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ double lds_f64(unsigned addr) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+    return v;
+}
 
 // Lane 31 (which flushed the strip's last column) releases the flushed-row count.
 __device__ __noinline__ void publish_rows(unsigned* prog, int flushed, int lane) {
     if (lane == kWarp - 1 && flushed > 0) st_release_u32(prog, static_cast<unsigned>(flushed));
     __syncwarp();
-}
-__device__ __forceinline__ int pos_mod(int a, int n) {
-    const int m = a % n;
-    return m < 0 ? m + n : m;
 }
 
 template <typename T>
@@ -72,6 +97,9 @@ sat_systolic_kernel(SatLaunch L) {
     const int warp = threadIdx.x / kWarp;
     const int lane = threadIdx.x % kWarp;
     WarpSmem<T>& sm = reinterpret_cast<WarpSmem<T>*>(sat_smem_raw)[warp];
+    const unsigned xin_base = smem_u32(&sm.xin[0][lane]);
+    const unsigned xin_end = xin_base + kInSlots * kWarp * sizeof(T);
+    const unsigned sout_base = smem_u32(&sm.sout[0][lane]);
     const int64_t n_tiles = L.n_jobs * L.strips;
     const int cols = static_cast<int>(L.cols);
 
@@ -81,9 +109,18 @@ sat_systolic_kernel(SatLaunch L) {
         tile = __shfl_sync(0xffffffffu, tile, 0);
         if (tile >= n_tiles) return;
 
-        // strip-major claim order
-        const int strip = static_cast<int>(tile / L.n_jobs);
-        const int64_t job = tile % L.n_jobs;
+        // pair-major claim order: (pair, job, half)
+        const int64_t pair = tile / (2 * L.n_jobs);
+        const int64_t rem = tile % (2 * L.n_jobs);
+        int64_t job;
+        int strip;
+        if (2 * pair + 1 < L.strips) {
+            job = rem / 2;
+            strip = static_cast<int>(2 * pair + (rem & 1));
+        } else { // odd strip count: the last layer holds single strips
+            job = rem;
+            strip = static_cast<int>(2 * pair);
+        }
         const SatJobView J = sat_job(L, job);
         const int rows = static_cast<int>(J.rows);
         const int c = strip * kStripCols + lane;
@@ -99,7 +136,7 @@ sat_systolic_kernel(SatLaunch L) {
         // left neighbour column: table column (padded) c_strip0, i.e. S(r, c_strip0 - 1)
         const double* left_col = table + kTabShift + strip * kStripCols;
         unsigned avail = 0;
-        // left values for rows [blk, blk+32) live in lane k's `lcur` (row blk + k)
+        // left values for rows [blk, blk+32) live in lane k's register (row blk + k)
         auto fetch_left = [&](int base) -> double {
             if (!prog_in || base >= rows) return 0.0; // warp-uniform
             const unsigned need = static_cast<unsigned>(min(rows, base + kWarp));
@@ -114,62 +151,87 @@ sat_systolic_kernel(SatLaunch L) {
         double lcur = fetch_left(0);
         double lnext = fetch_left(kWarp);
 
-        const T* src = static_cast<const T*>(J.src) + c;
         const int64_t ld = L.ld;
-        double* tcol = table + kTabShift + 1 + c; // my column of the table
+        const T* xsrc = static_cast<const T*>(J.src) + c; // row 0 of my column
 #pragma unroll
         for (int u = 0; u < kAhead; ++u) {
-            if (live && u < rows) cp_async_cell<T>(&sm.xin[u][lane], src + u * ld);
+            if (live && u < rows) cp_async_cell<T>(xin_base + u * kWarp * sizeof(T), xsrc + u * ld);
             cp_async_commit();
         }
+        const T* xnext = xsrc + kAhead * ld;                                // row s + kAhead
+        unsigned xin_next = xin_base + kAhead * kWarp * sizeof(T);          // its ring slot
+        unsigned xin_cur = xin_base + ((kInSlots - lane) % kInSlots) * kWarp * sizeof(T); // slot of row s - lane
+        double* tflush = table + tld + kTabShift + 1 + c;                   // table row rf + 1, rf = s - 31
+        double* zflush = table + tld + kTabShift;                           // padded column 0
 
         double prev = 0.0;      // S(r-1, c)
         double left_prev = 0.0; // S(r-1, c-1)
         double my_last = 0.0;   // S(r, c), shuffled right next step
-        int slot_r = pos_mod(-lane, kInSlots);
-        int slot_n = kAhead;
+        int first_bad = INT_MAX; // first row of my column holding a non-finite value
+        const bool corner = strip == 0 && lane == 0;
         const int steps = rows + kWarp;
-        for (int s = 0; s < steps; ++s) {
+
+        // One systolic step. kSteady: every lane's row and the flushed row are
+        // inside the table and the prefetched row exists (no range checks).
+        auto step = [&](const int s, const int u, auto steady_tag) {
+            constexpr bool kSteady = decltype(steady_tag)::value;
             const int r = s - lane;
-            {   // stream in source row s + kAhead
-                const int rn = s + kAhead;
-                if (live && rn < rows) cp_async_cell<T>(&sm.xin[slot_n][lane], src + rn * ld);
-                cp_async_commit();
-                cp_async_wait<kAhead>();
-            }
-            if ((s & (kWarp - 1)) == 0 && s > 0) {
-                lcur = lnext;
-                lnext = fetch_left(s + kWarp);
-            }
-            const double from_left_strip = __shfl_sync(0xffffffffu, lcur, s & (kWarp - 1));
+            // stream in source row s + kAhead
+            if (kSteady ? live : (live && s + kAhead < rows)) cp_async_cell<T>(xin_next, xnext);
+            cp_async_commit();
+            xnext += ld;
+            xin_next += kWarp * sizeof(T);
+            if (xin_next == xin_end) xin_next = xin_base;
+            cp_async_wait<kAhead>();
+            const double from_left_strip = __shfl_sync(0xffffffffu, lcur, u);
             double left = __shfl_up_sync(0xffffffffu, my_last, 1);
             if (lane == 0) left = from_left_strip;
-            if (live && r >= 0 && r < rows) {
-                const double v = static_cast<double>(sm.xin[slot_r][lane]);
-                if (!isfinite(v))
-                    report_min(J.nonfinite, static_cast<unsigned long long>((J.row0 + r) * L.cols + c));
-                // sat.cpp:33: out[c+1] = v + above[c+1] + out[c] - above[c]
-                const double sv = dsub(dadd(dadd(v, prev), left), left_prev);
+            const double v = lds_x<T>(xin_cur);
+            // sat.cpp:33: out[c+1] = v + above[c+1] + out[c] - above[c]
+            const double sv = dsub(dadd(dadd(v, prev), left), left_prev);
+            const bool act = kSteady ? live : (live && r >= 0 && r < rows);
+            if (act) {
+                first_bad = (!isfinite(v) && r < first_bad) ? r : first_bad;
                 prev = sv;
                 left_prev = left;
                 my_last = sv;
-                sm.sout[r & (kWarp - 1)][lane] = sv;
+                sts_f64(sout_base + static_cast<unsigned>(r & (kWarp - 1)) * kWarp * 8u, sv);
             }
-            // flush the completed row s - 31 (own column; the warp stores one segment)
+            xin_cur += kWarp * sizeof(T);
+            if (xin_cur == xin_end) xin_cur = xin_base;
+            // flush the completed row rf = s - 31 (own column; the warp stores one segment)
             const int rf = s - (kWarp - 1);
-            if (rf >= 0 && rf < rows) {
-                if (live) tcol[static_cast<int64_t>(rf + 1) * tld] = sm.sout[rf & (kWarp - 1)][lane];
-                if (strip == 0 && lane == 0) table[static_cast<int64_t>(rf + 1) * tld + kTabShift] = 0.0;
+            if (kSteady || (rf >= 0 && rf < rows)) {
+                if (live) *tflush = lds_f64(sout_base + static_cast<unsigned>(rf & (kWarp - 1)) * kWarp * 8u);
+                if (corner) *zflush = 0.0;
             }
-            slot_r = wrap_inc(slot_r, kInSlots);
-            slot_n = wrap_inc(slot_n, kInSlots);
-            // publish the flushed row count for the strip to the right once per
-            // kPublishEvery steps, in a real (not if-converted) warp-uniform branch
-            if (((s + 1) & (kPublishEvery - 1)) == 0 || s + 1 == steps) {
-                if (prog_out) publish_rows(prog_out, min(rows, s + 1 - (kWarp - 1)), lane);
+            if (kSteady || rf >= 0) {
+                tflush += tld;
+                zflush += tld;
+            }
+        };
+
+        for (int s0 = 0; s0 < steps; s0 += kWarp) {
+            if (s0 > 0) { // left-strip values for rows [s0, s0 + 32) come from the previous fetch
+                lcur = lnext;
+                lnext = fetch_left(s0 + kWarp);
+            }
+            if (s0 >= kWarp && s0 + kWarp + kAhead <= rows) {
+#pragma unroll
+                for (int u = 0; u < kWarp; ++u) step(s0 + u, u, std::true_type{});
+            } else {
+#pragma unroll 1
+                for (int u = 0; u < kWarp && s0 + u < steps; ++u) step(s0 + u, u, std::false_type{});
+            }
+            // publish the flushed row count for the strip to the right (warp-uniform)
+            const int s_end = min(s0 + kWarp, steps);
+            if ((s_end & (kPublishEvery - 1)) == 0 || s_end == steps) {
+                if (prog_out) publish_rows(prog_out, min(rows, s_end - (kWarp - 1)), lane);
             }
         }
         cp_async_wait<0>();
+        if (first_bad != INT_MAX)
+            report_min(J.nonfinite, static_cast<unsigned long long>((J.row0 + first_bad) * L.cols + c));
         __syncwarp();
     }
 }
