@@ -293,7 +293,7 @@ def run_b200(args):
     cells_local = n_local * ROWS * COLS
     kernels = {
         "sat_systolic_kernel": (sat_ms, SAT_BYTES_PER_CELL * cells_local),
-        "cfar_integral_kernel": (cfar_ms, CFAR_BYTES_PER_CELL * cells_local),
+        "cfar_ws_kernel": (cfar_ms, CFAR_BYTES_PER_CELL * cells_local),
     }
     dom = max(kernels, key=lambda k: kernels[k][0])
     dom_ms, dom_bytes = kernels[dom]

@@ -138,7 +138,7 @@ std::string degenerate_msg(const uwb_cfar_params& p, uint64_t rows, uint64_t col
 
 struct Plan {
     JobGeometry geo;
-    int64_t n_maps, cols, n_jobs, table_ld, table_stride, strips, max_rows;
+    int64_t n_maps, cols, n_jobs, table_ld, table_stride, strips, max_rows, edge_stride;
     size_t off_tables, off_edge, off_prog, off_counter, off_scratch, total;
 };
 
@@ -168,7 +168,9 @@ Plan make_plan(const uwb_map_batch& b, const uwb_cfar_params* p, int sat_mode, u
         return o;
     };
     P.off_tables = take(sizeof(double) * static_cast<size_t>(P.n_jobs) * P.table_stride);
-    P.off_edge = take(0); // strips hand over through the table itself
+    P.edge_stride = round_up(P.max_rows, 32);
+    // S(r, strip's last column) handed from each strip to the next, contiguous per strip
+    P.off_edge = take(P.strips > 1 ? sizeof(double) * static_cast<size_t>(P.n_jobs) * P.strips * P.edge_stride : 0);
     P.off_prog = take(sizeof(unsigned) * P.n_jobs * P.strips);
     P.off_counter = take(sizeof(unsigned) * 4);
     P.off_scratch = take(det_cap > 2048 ? sizeof(uwb_detection) * P.n_maps * det_cap : 0);
@@ -189,7 +191,7 @@ SatLaunch sat_launch(const Plan& P, const uwb_map_batch& b, char* ws, unsigned l
     L.table_stride = P.table_stride;
     L.strips = P.strips;
     L.gedge = reinterpret_cast<double*>(ws + P.off_edge);
-    L.edge_stride = P.max_rows;
+    L.edge_stride = P.edge_stride;
     L.gprog = reinterpret_cast<unsigned*>(ws + P.off_prog);
     L.tile_counter = reinterpret_cast<unsigned*>(ws + P.off_counter);
     L.first_bad = first_bad;

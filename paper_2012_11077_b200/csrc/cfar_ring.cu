@@ -32,8 +32,7 @@ namespace {
 
 constexpr int kRingRows = 256;   // output rows per CTA
 constexpr int kG = 4;            // rows per group (output step, copy group)
-constexpr int kAheadGroups = 3;  // groups of look-ahead
-constexpr int kNcg = 1 + kAheadGroups; // CUT groups in the ring
+constexpr int kDefaultAhead = 2; // groups of look-ahead (UWB_RING_AHEAD overrides: 1..4)
 constexpr int kColsPerThread = 2;
 
 struct RingGeom {
@@ -42,21 +41,22 @@ struct RingGeom {
     int stride; // doubles per table slot
 };
 
-__host__ __device__ inline RingGeom ring_geom(int w, int hr, int hc) {
+__host__ __device__ inline RingGeom ring_geom(int w, int hr, int hc, int ahead) {
     RingGeom g;
     // output rows r..r+3 read table rows r-hr .. r+4+hr: 2hr+5 rows, spread over
     // at most ceil((2hr+5)/4)+1 groups
-    g.ng = (2 * hr + 5 + kG - 1) / kG + 1 + kAheadGroups;
+    g.ng = (2 * hr + 5 + kG - 1) / kG + 1 + ahead;
     g.nr = g.ng * kG;
     g.stride = w + 2 * hc + 4;
     return g;
 }
 
 template <typename T>
-inline size_t ring_smem_bytes(int w, int hr, int hc) {
-    const RingGeom g = ring_geom(w, hr, hc);
-    return sizeof(double) * static_cast<size_t>(g.nr) * g.stride + sizeof(T) * static_cast<size_t>(kNcg) * kG * w +
-           2 * sizeof(uint64_t) * (g.ng + kNcg);
+inline size_t ring_smem_bytes(int w, int hr, int hc, int ahead) {
+    const RingGeom g = ring_geom(w, hr, hc, ahead);
+    const int ncg = 1 + ahead;
+    return sizeof(double) * static_cast<size_t>(g.nr) * g.stride + sizeof(T) * static_cast<size_t>(ncg) * kG * w +
+           2 * sizeof(uint64_t) * (g.ng + ncg + 1) + (sizeof(uint4) + sizeof(int2)) * kRingRows;
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -108,12 +108,13 @@ __device__ __forceinline__ double train_sum(const ColConst& k, unsigned rA, unsi
     return dsub(rs_o, rs_g);
 }
 
-template <typename T, int NCW>
+template <typename T, int NCW, int AHEAD>
 __global__ void __launch_bounds__((NCW + 1) * kWarp)
 cfar_ws_kernel(CfarLaunch L) {
     constexpr int W = NCW * kWarp * kColsPerThread;
+    constexpr int kNcg = 1 + AHEAD; // CUT groups in the ring
     extern __shared__ __align__(16) unsigned char ring_smem[];
-    const RingGeom G = ring_geom(W, L.hr, L.hc);
+    const RingGeom G = ring_geom(W, L.hr, L.hc, AHEAD);
     double* slots = reinterpret_cast<double*>(ring_smem);
     T* cuts = reinterpret_cast<T*>(slots + static_cast<size_t>(G.nr) * G.stride);
     uint64_t* full_t = reinterpret_cast<uint64_t*>(cuts + static_cast<size_t>(kNcg) * kG * W);
@@ -151,6 +152,23 @@ cfar_ws_kernel(CfarLaunch L) {
     const int i_hi = min(rows, rb + hr);
     const int n_steps = (rb - ra + kG - 1) / kG;
 
+    // Per output row of the tile: the ring addresses of its four tap rows and
+    // its clamped outer / guard heights, computed once (cfar.cpp:117-120).
+    // (the ring, CUT and 2 * (ng + kNcg) barrier regions keep 16-byte alignment)
+    uint4* tap_rows = reinterpret_cast<uint4*>(empty_c + kNcg);
+    int2* heights = reinterpret_cast<int2*>(tap_rows + kRingRows);
+    {
+        const unsigned ring_base = smem_u32(slots);
+        const unsigned row_bytes = static_cast<unsigned>(G.stride) * 8u;
+        auto ring_addr = [&](int i) { return ring_base + static_cast<unsigned>((i - i_lo) % G.nr) * row_bytes; };
+        for (int lr = threadIdx.x; lr < rb - ra; lr += blockDim.x) {
+            const int r = ra + lr;
+            const int iA = clamp_lo32(r, hr), iB = clamp_hi32(r, hr, rows) + 1;
+            const int iC = clamp_lo32(r, gr), iD = clamp_hi32(r, gr, rows) + 1;
+            tap_rows[lr] = make_uint4(ring_addr(iA), ring_addr(iB), ring_addr(iC), ring_addr(iD));
+            heights[lr] = make_int2(iB - iA, iD - iC);
+        }
+    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < G.ng + kNcg; ++s) {
             mbar_init(&full_t[s], 1);
@@ -195,10 +213,9 @@ cfar_ws_kernel(CfarLaunch L) {
     }
 
     // ============================ consumer warps ============================
-    const unsigned ring_base = smem_u32(slots);
     const unsigned cut_smem = smem_u32(cuts);
-    const unsigned row_bytes = static_cast<unsigned>(G.stride) * 8u;
-    const unsigned ring_end = ring_base + static_cast<unsigned>(G.nr) * row_bytes;
+    const unsigned tap_smem = smem_u32(tap_rows);
+    const unsigned ht_smem = smem_u32(heights);
     const int tc = warp * kWarp * kColsPerThread + lane; // my first column within the tile
     const ColConst K0 = col_const(c0 + tc, cols, hc, gc, e_lo);
     const ColConst K1 = col_const(c0 + tc + kWarp, cols, hc, gc, e_lo);
@@ -207,19 +224,6 @@ cfar_ws_kernel(CfarLaunch L) {
     int waited = -1, wslot = 0, wphase = 0; // full_t groups known resident
     int released = -1, rslot = 0;            // table groups handed back
     int cslot = 0, cphase = 0;
-    // tap rows and ring row addresses, initialised for row ra - 1 so that every
-    // row (ra included) advances them the same way
-    int iA = clamp_lo32(ra - 1, hr), iB = clamp_hi32(ra - 1, hr, rows) + 1;
-    int iC = clamp_lo32(ra - 1, gr), iD = clamp_hi32(ra - 1, gr, rows) + 1;
-    auto ring_addr = [&](int i) {
-        const int m = ((i - i_lo) % G.nr + G.nr) % G.nr;
-        return ring_base + static_cast<unsigned>(m) * row_bytes;
-    };
-    unsigned rA = ring_addr(iA), rB = ring_addr(iB), rC = ring_addr(iC), rD = ring_addr(iD);
-    auto adv = [&](unsigned& a) {
-        a += row_bytes;
-        if (a == ring_end) a = ring_base;
-    };
     // per-column alpha cache: n is constant over interior rows
     int n0c = -1, n1c = -1;
     double k0 = 0.0, k1 = 0.0;
@@ -237,30 +241,21 @@ cfar_ws_kernel(CfarLaunch L) {
         }
         mbar_wait(&full_c[cslot], static_cast<unsigned>(cphase));
         const unsigned cut_grp = cut_smem + static_cast<unsigned>(cslot * kG * W) * sizeof(T);
-        // away from the top and bottom borders every tap row moves down by one per row
-        const bool interior = r0 - 1 - hr >= 0 && r_last + hr + 1 <= rows;
-        // phase 1: ring rows and clamped heights of the step's rows (warp-uniform)
+        // phase 1: ring rows and clamped heights of the step's rows (table lookups)
         unsigned RA[kG], RB[kG], RC[kG], RD[kG];
         int HR[kG], HG[kG];
 #pragma unroll
         for (int k = 0; k < kG; ++k) {
-            const int r = r0 + k;
-            if (r <= r_last) {
-                if (interior) {
-                    adv(rA); adv(rB); adv(rC); adv(rD);
-                    ++iA; ++iB; ++iC; ++iD;
-                } else {
-                    const int nA = clamp_lo32(r, hr), nB = clamp_hi32(r, hr, rows) + 1;
-                    const int nC = clamp_lo32(r, gr), nD = clamp_hi32(r, gr, rows) + 1;
-                    if (nA != iA) { iA = nA; adv(rA); }
-                    if (nB != iB) { iB = nB; adv(rB); }
-                    if (nC != iC) { iC = nC; adv(rC); }
-                    if (nD != iD) { iD = nD; adv(rD); }
-                }
-            }
-            RA[k] = rA; RB[k] = rB; RC[k] = rC; RD[k] = rD;
-            HR[k] = iB - iA;
-            HG[k] = iD - iC;
+            const int lr = min(r0 + k, r_last) - ra;
+            uint4 t;
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(t.x), "=r"(t.y), "=r"(t.z), "=r"(t.w)
+                         : "r"(tap_smem + 16u * static_cast<unsigned>(lr)));
+            int2 h;
+            asm volatile("ld.shared.v2.s32 {%0,%1}, [%2];" : "=r"(h.x), "=r"(h.y) : "r"(ht_smem + 8u * static_cast<unsigned>(lr)));
+            RA[k] = t.x; RB[k] = t.y; RC[k] = t.z; RD[k] = t.w;
+            HR[k] = h.x;
+            HG[k] = h.y;
         }
         // phase 2: every cell of the step (loads first, decisions after)
         double v[kG][2], sum[kG][2], approx[kG][2];
@@ -396,19 +391,37 @@ cfar_ws_kernel(CfarLaunch L) {
     }
 }
 
-template <typename T, int NCW>
+template <typename T, int NCW, int AHEAD>
 cudaError_t go(const CfarLaunch& L0, size_t smem, cudaStream_t stream) {
     constexpr int W = NCW * kWarp * kColsPerThread;
     CfarLaunch L = L0;
     L.col_tiles = (L.cols + W - 1) / W;
     L.row_chunks = (L.geo.slab_rows + kRingRows - 1) / kRingRows;
     const dim3 grid(static_cast<unsigned>(L.col_tiles * L.row_chunks), static_cast<unsigned>(L.n_jobs), 1);
-    cudaError_t e = cudaFuncSetAttribute(cfar_ws_kernel<T, NCW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+    cudaError_t e = cudaFuncSetAttribute(cfar_ws_kernel<T, NCW, AHEAD>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     ++g_kernel_launches;
-    cfar_ws_kernel<T, NCW><<<grid, (NCW + 1) * kWarp, smem, stream>>>(L);
+    cfar_ws_kernel<T, NCW, AHEAD><<<grid, (NCW + 1) * kWarp, smem, stream>>>(L);
     return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t go_cfg(const CfarLaunch& L, int ncw, int ahead, size_t smem, cudaStream_t stream) {
+    if (ncw == 4) {
+        switch (ahead) {
+            case 1: return go<T, 4, 1>(L, smem, stream);
+            case 3: return go<T, 4, 3>(L, smem, stream);
+            case 4: return go<T, 4, 4>(L, smem, stream);
+            default: return go<T, 4, 2>(L, smem, stream);
+        }
+    }
+    switch (ahead) {
+        case 1: return go<T, 2, 1>(L, smem, stream);
+        case 3: return go<T, 2, 3>(L, smem, stream);
+        case 4: return go<T, 2, 4>(L, smem, stream);
+        default: return go<T, 2, 2>(L, smem, stream);
+    }
 }
 
 } // namespace
@@ -426,12 +439,18 @@ cudaError_t launch_cfar_ring(const CfarLaunch& L, int dtype, cudaStream_t stream
     if ((reinterpret_cast<uintptr_t>(L.maps) % 16) || ((L.ld * esz) % 16) || ((L.map_stride * esz) % 16))
         return cudaErrorNotSupported;
     if (((L.cols * esz) % 16) && L.ld * esz < ((L.cols * esz + 15) / 16) * 16) return cudaErrorNotSupported;
-    const size_t s4 = f32 ? ring_smem_bytes<float>(256, L.hr, L.hc) : ring_smem_bytes<double>(256, L.hr, L.hc);
-    const size_t s2 = f32 ? ring_smem_bytes<float>(128, L.hr, L.hc) : ring_smem_bytes<double>(128, L.hr, L.hc);
-    if (s4 <= 113 * 1024 && L.cols > 128)
-        return f32 ? go<float, 4>(L, s4, stream) : go<double, 4>(L, s4, stream);
+    int ahead = kDefaultAhead;
+    if (const char* a = getenv("UWB_RING_AHEAD")) ahead = min(4, max(1, atoi(a)));
+    int ncw_pref = 4;
+    if (const char* a = getenv("UWB_RING_NCW")) ncw_pref = atoi(a) == 2 ? 2 : 4;
+    auto bytes = [&](int w) {
+        return f32 ? ring_smem_bytes<float>(w, L.hr, L.hc, ahead) : ring_smem_bytes<double>(w, L.hr, L.hc, ahead);
+    };
+    const size_t s4 = bytes(256), s2 = bytes(128);
+    if (ncw_pref == 4 && s4 <= 113 * 1024 && L.cols > 128)
+        return f32 ? go_cfg<float>(L, 4, ahead, s4, stream) : go_cfg<double>(L, 4, ahead, s4, stream);
     if (s2 <= 200 * 1024)
-        return f32 ? go<float, 2>(L, s2, stream) : go<double, 2>(L, s2, stream);
+        return f32 ? go_cfg<float>(L, 2, ahead, s2, stream) : go_cfg<double>(L, 2, ahead, s2, stream);
     return cudaErrorNotSupported;
 }
 

@@ -133,8 +133,10 @@ sat_systolic_kernel(SatLaunch L) {
 
         const unsigned* prog_in = strip > 0 ? L.gprog + job * L.strips + strip - 1 : nullptr;
         unsigned* prog_out = strip + 1 < L.strips ? L.gprog + job * L.strips + strip : nullptr;
-        // left neighbour column: table column (padded) c_strip0, i.e. S(r, c_strip0 - 1)
-        const double* left_col = table + kTabShift + strip * kStripCols;
+        // S(r, last column) of the strip to the left / of this strip, one double
+        // per row (contiguous, so 32 rows are fetched as one 256-byte segment)
+        const double* ge_in = prog_in ? L.gedge + (job * L.strips + strip - 1) * L.edge_stride : nullptr;
+        double* ge_out = prog_out ? L.gedge + (job * L.strips + strip) * L.edge_stride : nullptr;
         unsigned avail = 0;
         // left values for rows [blk, blk+32) live in lane k's register (row blk + k)
         auto fetch_left = [&](int base) -> double {
@@ -146,16 +148,32 @@ sat_systolic_kernel(SatLaunch L) {
                 avail = __shfl_sync(0xffffffffu, avail, 0);
             }
             const int rr = base + lane;
-            return rr < rows ? left_col[static_cast<int64_t>(rr + 1) * tld] : 0.0;
+            return rr < rows ? ge_in[rr] : 0.0;
         };
         double lcur = fetch_left(0);
         double lnext = fetch_left(kWarp);
 
         const int64_t ld = L.ld;
         const T* xsrc = static_cast<const T*>(J.src) + c; // row 0 of my column
+        // full strips with 16-byte aligned rows stage each row segment with
+        // 16-byte copies by the first 32*sizeof(T)/16 lanes
+        constexpr int kVecLanes = kWarp * static_cast<int>(sizeof(T)) / 16;
+        constexpr int kElemsPerVec = 16 / static_cast<int>(sizeof(T));
+        const bool vec = (strip + 1) * kStripCols <= cols && (ld * sizeof(T)) % 16 == 0 &&
+                         (reinterpret_cast<uintptr_t>(J.src) % 16) == 0;
+        const bool vec_lane = lane < kVecLanes;
+        const unsigned vdst_off = (16u - static_cast<unsigned>(sizeof(T))) * static_cast<unsigned>(lane);
+        const int vsrc_off = lane * (kElemsPerVec - 1);
+        auto stage = [&](unsigned dst, const T* src) { // source row segment -> ring slot
+            if (vec) {
+                if (vec_lane) cp_async_16(dst + vdst_off, src + vsrc_off);
+            } else if (live) {
+                cp_async_cell<T>(dst, src);
+            }
+        };
 #pragma unroll
         for (int u = 0; u < kAhead; ++u) {
-            if (live && u < rows) cp_async_cell<T>(xin_base + u * kWarp * sizeof(T), xsrc + u * ld);
+            if (u < rows) stage(xin_base + u * kWarp * sizeof(T), xsrc + u * ld);
             cp_async_commit();
         }
         const T* xnext = xsrc + kAhead * ld;                                // row s + kAhead
@@ -177,12 +195,13 @@ sat_systolic_kernel(SatLaunch L) {
             constexpr bool kSteady = decltype(steady_tag)::value;
             const int r = s - lane;
             // stream in source row s + kAhead
-            if (kSteady ? live : (live && s + kAhead < rows)) cp_async_cell<T>(xin_next, xnext);
+            if (kSteady || s + kAhead < rows) stage(xin_next, xnext);
             cp_async_commit();
             xnext += ld;
             xin_next += kWarp * sizeof(T);
             if (xin_next == xin_end) xin_next = xin_base;
             cp_async_wait<kAhead>();
+            __syncwarp(); // rows staged by other lanes' 16-byte copies
             const double from_left_strip = __shfl_sync(0xffffffffu, lcur, u);
             double left = __shfl_up_sync(0xffffffffu, my_last, 1);
             if (lane == 0) left = from_left_strip;
@@ -196,6 +215,7 @@ sat_systolic_kernel(SatLaunch L) {
                 left_prev = left;
                 my_last = sv;
                 sts_f64(sout_base + static_cast<unsigned>(r & (kWarp - 1)) * kWarp * 8u, sv);
+                if (lane == kWarp - 1 && ge_out) ge_out[r] = sv;
             }
             xin_cur += kWarp * sizeof(T);
             if (xin_cur == xin_end) xin_cur = xin_base;
