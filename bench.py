@@ -310,12 +310,12 @@ def run_b200(args):
         bits = torch.zeros((n_local, ROWS, (COLS + 31) // 32), dtype=torch.int32, pin_memory=True)
         dets = torch.zeros((n_local, det_cap, 32), dtype=torch.uint8, pin_memory=True)
         counts = torch.zeros(n_local, dtype=torch.int64, pin_memory=True)
-        host_cfar2d_batch(host_maps, params, bits, dets, counts, det_cap, maps_per_chunk=128)
+        host_cfar2d_batch(host_maps, params, bits, dets, counts, det_cap, maps_per_chunk=args.e2e_chunk)
         e_steps = max(2, min(args.steps, args.e2e_steps))
         barrier()
         t0 = time.perf_counter()
         for _ in range(e_steps):
-            host_cfar2d_batch(host_maps, params, bits, dets, counts, det_cap, maps_per_chunk=128)
+            host_cfar2d_batch(host_maps, params, bits, dets, counts, det_cap, maps_per_chunk=args.e2e_chunk)
         t1 = time.perf_counter()
         barrier()
         e_ms = torch.tensor([(t1 - t0) * 1e3 / e_steps], dtype=torch.float64, device=dev)
@@ -326,7 +326,8 @@ def run_b200(args):
         e2e = {"value": cells_total / (e_ms_v / 1e3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": int(host_maps.numel() * 4) * world,
                "d2h_bytes_per_step": int(bits.numel() * 4 + dets.numel() + counts.numel() * 8) * world,
-               "ms_per_step": e_ms_v, "steps": e_steps, "timer": "host wall clock around the synchronous call",
+               "ms_per_step": e_ms_v, "steps": e_steps, "maps_per_chunk": args.e2e_chunk,
+               "timer": "host wall clock around the synchronous call",
                "matches_device_path": same}
         del host_maps
 
@@ -375,6 +376,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-chunk", type=int, default=64, help="maps per H2D chunk in the end-to-end call")
     ap.add_argument("--maps", type=int, default=N_MAPS, help="batch size (profiling runs only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

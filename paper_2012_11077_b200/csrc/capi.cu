@@ -85,6 +85,17 @@ bool device_ok() {
 
 uwb_status need_device() {
     if (!device_ok()) return fail(UWB_CUDA_ERROR, "uwbvital_b200: no CUDA device available (no CPU fallback)");
+    // stream-ordered scratch is returned to the device's default pool, not to the
+    // driver, so repeated calls do not re-map their workspaces
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    });
     return UWB_OK;
 }
 
@@ -949,66 +960,96 @@ uwb_status uwb_host_cfar2d_batch(const uwb_map_batch* hb, const uwb_cfar_params*
     const uint64_t words = (hb->cols + 31) / 32;
     const uint64_t mask_words = words * hb->rows;
 
-    // two pipelines (double buffering): H2D of chunk k+1 overlaps compute/D2H of chunk k
-    constexpr int kPipes = 2;
-    struct StreamSet {
-        cudaStream_t s[kPipes] = {};
-        ~StreamSet() {
-            for (auto x : s)
-                if (x) { cudaStreamSynchronize(x); cudaStreamDestroy(x); }
+    // Three engines, three streams: the copy-in stream streams chunks back to
+    // back (the PCIe H2D link is the bound of this call), the compute stream runs
+    // SAT+CFAR+sort per chunk in one workspace, the copy-out stream drains
+    // results. kSlots input/output slots rotate; events order reuse.
+    constexpr int kSlots = 3;
+    struct Streams {
+        cudaStream_t in = nullptr, comp = nullptr, out = nullptr;
+        cudaEvent_t loaded[kSlots] = {}, done[kSlots] = {}, drained[kSlots] = {};
+        ~Streams() {
+            for (cudaStream_t x : {in, comp, out})
+                if (x) cudaStreamSynchronize(x);
+            for (int i = 0; i < kSlots; ++i)
+                for (cudaEvent_t e : {loaded[i], done[i], drained[i]})
+                    if (e) cudaEventDestroy(e);
+            for (cudaStream_t x : {in, comp, out})
+                if (x) cudaStreamDestroy(x);
         }
-    } streams;
-    cudaStream_t* st = streams.s;
-    for (int i = 0; i < kPipes; ++i) UWB_CUDA_TRY(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking));
-    struct Pipe {
-        DevBuf in, bits, dets, cnt, bad, ws;
-    } pipes[kPipes];
+    } S;
+    UWB_CUDA_TRY(cudaStreamCreateWithFlags(&S.in, cudaStreamNonBlocking));
+    UWB_CUDA_TRY(cudaStreamCreateWithFlags(&S.comp, cudaStreamNonBlocking));
+    UWB_CUDA_TRY(cudaStreamCreateWithFlags(&S.out, cudaStreamNonBlocking));
+    for (int i = 0; i < kSlots; ++i) {
+        UWB_CUDA_TRY(cudaEventCreateWithFlags(&S.loaded[i], cudaEventDisableTiming));
+        UWB_CUDA_TRY(cudaEventCreateWithFlags(&S.done[i], cudaEventDisableTiming));
+        UWB_CUDA_TRY(cudaEventCreateWithFlags(&S.drained[i], cudaEventDisableTiming));
+    }
+    struct Slot {
+        DevBuf in, bits, dets, cnt, bad;
+    } slots[kSlots];
     uwb_map_batch cb = *hb;
     cb.n_maps = chunk;
     const Plan P = make_plan(cb, p, sat_mode, slab_rows, static_cast<int64_t>(det_capacity));
     const std::vector<double> alpha = alpha_table_host(*p);
-    DevBuf d_alpha;
-    UWB_CUDA_TRY(d_alpha.alloc(sizeof(double) * alpha.size(), st[0]));
-    UWB_CUDA_TRY(cudaMemcpyAsync(d_alpha.p, alpha.data(), sizeof(double) * alpha.size(), cudaMemcpyHostToDevice, st[0]));
-    UWB_CUDA_TRY(cudaStreamSynchronize(st[0]));
-    for (int i = 0; i < kPipes; ++i) {
-        UWB_CUDA_TRY(pipes[i].in.alloc(esz * cells * chunk, st[i]));
-        UWB_CUDA_TRY(pipes[i].bits.alloc(sizeof(uint32_t) * mask_words * chunk, st[i]));
-        UWB_CUDA_TRY(pipes[i].dets.alloc(sizeof(uwb_detection) * std::max<uint64_t>(det_capacity, 1) * chunk, st[i]));
-        UWB_CUDA_TRY(pipes[i].cnt.alloc(sizeof(uint64_t) * chunk, st[i]));
-        UWB_CUDA_TRY(pipes[i].bad.alloc(sizeof(uint64_t) * 2 * chunk, st[i]));
-        UWB_CUDA_TRY(pipes[i].ws.alloc(P.total, st[i]));
+    DevBuf d_alpha, ws;
+    struct Drain { // on every exit: copies finish before the buffers are freed on the compute stream
+        const Streams& s;
+        ~Drain() {
+            cudaStreamSynchronize(s.in);
+            cudaStreamSynchronize(s.out);
+        }
+    } drain{S};
+    UWB_CUDA_TRY(d_alpha.alloc(sizeof(double) * alpha.size(), S.comp));
+    UWB_CUDA_TRY(cudaMemcpyAsync(d_alpha.p, alpha.data(), sizeof(double) * alpha.size(), cudaMemcpyHostToDevice, S.comp));
+    UWB_CUDA_TRY(ws.alloc(P.total, S.comp));
+    for (auto& sl : slots) {
+        UWB_CUDA_TRY(sl.in.alloc(esz * cells * chunk, S.comp));
+        UWB_CUDA_TRY(sl.bits.alloc(sizeof(uint32_t) * mask_words * chunk, S.comp));
+        UWB_CUDA_TRY(sl.dets.alloc(sizeof(uwb_detection) * std::max<uint64_t>(det_capacity, 1) * chunk, S.comp));
+        UWB_CUDA_TRY(sl.cnt.alloc(sizeof(uint64_t) * chunk, S.comp));
+        UWB_CUDA_TRY(sl.bad.alloc(sizeof(uint64_t) * 2 * chunk, S.comp));
     }
+    UWB_CUDA_TRY(cudaStreamSynchronize(S.comp)); // allocations visible to the other streams
     uwb_status result = UWB_OK;
     for (uint64_t m0 = 0, k = 0; m0 < hb->n_maps; m0 += chunk, ++k) {
-        const int i = static_cast<int>(k % kPipes);
+        const int i = static_cast<int>(k % kSlots);
         const uint64_t nm = std::min(chunk, hb->n_maps - m0);
-        Pipe& pp = pipes[i];
+        Slot& sl = slots[i];
         const char* src = static_cast<const char*>(hb->maps) + esz * cells * m0;
-        UWB_CUDA_TRY(cudaMemcpyAsync(pp.in.p, src, esz * cells * nm, cudaMemcpyHostToDevice, st[i]));
+        if (k >= kSlots) UWB_CUDA_TRY(cudaStreamWaitEvent(S.in, S.done[i], 0)); // input slot consumed
+        UWB_CUDA_TRY(cudaMemcpyAsync(sl.in.p, src, esz * cells * nm, cudaMemcpyHostToDevice, S.in));
+        UWB_CUDA_TRY(cudaEventRecord(S.loaded[i], S.in));
+        UWB_CUDA_TRY(cudaStreamWaitEvent(S.comp, S.loaded[i], 0));
+        if (k >= kSlots) UWB_CUDA_TRY(cudaStreamWaitEvent(S.comp, S.drained[i], 0)); // output slot drained
         uwb_map_batch db = cb;
-        db.maps = pp.in.p;
+        db.maps = sl.in.p;
         db.n_maps = nm;
         uwb_cfar_outputs o{};
-        o.mask_bits = pp.bits.as<uint32_t>();
+        o.mask_bits = sl.bits.as<uint32_t>();
         o.words_per_row = words;
         o.mask_map_stride = mask_words;
-        o.dets = pp.dets.as<uwb_detection>();
+        o.dets = sl.dets.as<uwb_detection>();
         o.det_capacity = det_capacity;
-        o.det_counts = pp.cnt.as<uint64_t>();
-        o.first_bad = pp.bad.as<uint64_t>();
-        if (uwb_status s2 = dev_cfar(db, *p, d_alpha.as<double>(), UWB_INTEGRAL, sat_mode, slab_rows, o, pp.ws.p,
-                                     P.total, 0, st[i]))
+        o.det_counts = sl.cnt.as<uint64_t>();
+        o.first_bad = sl.bad.as<uint64_t>();
+        if (uwb_status s2 = dev_cfar(db, *p, d_alpha.as<double>(), UWB_INTEGRAL, sat_mode, slab_rows, o, ws.p,
+                                     P.total, 0, S.comp))
             return s2;
+        UWB_CUDA_TRY(cudaEventRecord(S.done[i], S.comp));
+        UWB_CUDA_TRY(cudaStreamWaitEvent(S.out, S.done[i], 0));
         if (mask_bits)
-            UWB_CUDA_TRY(cudaMemcpyAsync(mask_bits + mask_words * m0, pp.bits.p, sizeof(uint32_t) * mask_words * nm,
-                                         cudaMemcpyDeviceToHost, st[i]));
+            UWB_CUDA_TRY(cudaMemcpyAsync(mask_bits + mask_words * m0, sl.bits.p, sizeof(uint32_t) * mask_words * nm,
+                                         cudaMemcpyDeviceToHost, S.out));
         if (dets && det_capacity)
-            UWB_CUDA_TRY(cudaMemcpyAsync(dets + det_capacity * m0, pp.dets.p, sizeof(uwb_detection) * det_capacity * nm,
-                                         cudaMemcpyDeviceToHost, st[i]));
-        UWB_CUDA_TRY(cudaMemcpyAsync(det_counts + m0, pp.cnt.p, sizeof(uint64_t) * nm, cudaMemcpyDeviceToHost, st[i]));
+            UWB_CUDA_TRY(cudaMemcpyAsync(dets + det_capacity * m0, sl.dets.p, sizeof(uwb_detection) * det_capacity * nm,
+                                         cudaMemcpyDeviceToHost, S.out));
+        UWB_CUDA_TRY(cudaMemcpyAsync(det_counts + m0, sl.cnt.p, sizeof(uint64_t) * nm, cudaMemcpyDeviceToHost, S.out));
+        UWB_CUDA_TRY(cudaEventRecord(S.drained[i], S.out));
     }
-    for (int i = 0; i < kPipes; ++i) UWB_CUDA_TRY(cudaStreamSynchronize(st[i]));
+    UWB_CUDA_TRY(cudaStreamSynchronize(S.out));
+    UWB_CUDA_TRY(cudaStreamSynchronize(S.comp));
     for (uint64_t i = 0; i < hb->n_maps; ++i)
         if (det_counts[i] > det_capacity) result = fail(UWB_CAPACITY_ERROR, "uwb_host_cfar2d_batch: detection buffer too small");
     return result ? result : ok();
