@@ -1,28 +1,36 @@
 // Kernel (d), production path: warp-specialised CA-CFAR over shared-memory rings
-// of table rows.
+// of table rows, fed by tensor TMA.
 //
 // Replaces cfar_rows / run_cfar of /root/reference/proj/src/cfar.cpp:109-175 for
 // the integral-image backend (cfar2d_integral, cfar.cpp:218-227).
 //
-// A CTA owns a W-column x 256-row tile of one job (W = 64 x consumer warps).
-// One producer warp streams every table row the tile's windows touch into a
-// shared-memory ring with the TMA engine (cp.async.bulk global->shared, one
-// 16-byte-aligned row segment per copy), and the CUT row segments into a second
-// ring; rows move in groups of 4 that complete on one "full" mbarrier. The
-// consumer warps (two output columns per thread, c and c+32) wait on "full",
-// evaluate 4 output rows, and hand slots back through "empty" mbarriers, so the
-// two sides never meet at a CTA barrier. The eight taps of a cell are
-// shared-memory reads:
+// A CTA owns a 128-column x 256-row tile of one job. One producer thread moves
+// every table row the tile's windows touch into a shared-memory ring with 3-D
+// tensor TMA (cp.async.bulk.tensor: one box = 4 table rows x (128 + pad)
+// columns of one job's table), and the CUT rows into a second ring (one box = 4
+// map rows x 128 columns); each box completes on one "full" mbarrier. Ring
+// slots are handed back through "empty" mbarriers, so producer and consumers
+// never meet at a CTA barrier, and the producer checks both rings without
+// blocking so neither stream waits for the other. Both streams are also
+// prefetched into L2 kPfGroups boxes ahead. The consumer warps evaluate 4 output
+// rows per step; the eight taps of a cell are shared-memory reads
 //     RS = (t[r0][c0] + t[r1+1][c1+1]) - (t[r0][c1+1] + t[r1+1][c0])   (sat.hpp:32-33)
 // sum = RS(outer) - RS(guard), T = alpha[n] * (sum / n), mask = cut > T
 // (cfar.cpp:115-127).
 //
-// Threshold decision: the IEEE division is skipped on the common path, which
-// compares cut with sum * (alpha[n] / n) (within a few ulp of T); a warp takes
-// the exact path (the reference expression alpha[n] * (sum / n)) when any lane
-// has cut within 1e-13 relative of it, a detection (whose record carries T), or
-// when the threshold map is an output. Decisions equal the reference's `cut > T`.
+// Interior fast path (all 4 rows and all of the warp's columns have unclamped
+// windows): the 4 tap rows of the step are consecutive ring slots (the first
+// group is mirrored past the ring's end), so every tap is one shared load at a
+// compile-time offset from one of 8 row pointers, and n = n_int. The IEEE
+// division is skipped: a cell with 0 <= cut < sum * (alpha/n) * (1 - 1e-13) is
+// certainly below T; any other cell in the warp sends the warp through the
+// reference expression alpha[n] * (sum / n). Decisions, thresholds and
+// detection records are exactly the reference's.
+#include <climits>
 #include <cstdlib>
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <mutex>
 
 #include "cfar_common.cuh"
 
@@ -30,54 +38,94 @@ namespace uwb {
 
 namespace {
 
-constexpr int kRingRows = 256;   // output rows per CTA
-constexpr int kG = 4;            // rows per group (output step, copy group)
-constexpr int kDefaultAhead = 2; // groups of look-ahead (UWB_RING_AHEAD overrides: 1..4)
-constexpr int kColsPerThread = 2;
+constexpr int kRingRows = 256;  // output rows per CTA
+constexpr int kG = 4;           // rows per group (output step, TMA box height)
+constexpr int kW = 128;         // output columns per CTA
+constexpr int kTableAhead = 1;  // table groups of look-ahead beyond the window
+constexpr int kCutGroups = 4;   // CUT ring depth (groups)
+constexpr int kPfGroups = 6;    // L2 prefetch distance of both streams (groups)
+constexpr int kCtasPerSm = 4;   // occupancy target at 4-row steps (registers and shared memory)
 
 struct RingGeom {
     int ng;     // table row groups in the ring
-    int nr;     // table row slots (ng * kG)
-    int stride; // doubles per table slot
+    int nr;     // table row slots (ng * kG); sg mirror groups follow in memory
 };
 
-__host__ __device__ inline RingGeom ring_geom(int w, int hr, int hc, int ahead) {
+// sg = groups per consumer step (rows per step rs = 4 sg)
+__host__ __device__ inline RingGeom ring_geom(int hr, int sg) {
     RingGeom g;
-    // output rows r..r+3 read table rows r-hr .. r+4+hr: 2hr+5 rows, spread over
-    // at most ceil((2hr+5)/4)+1 groups
-    g.ng = (2 * hr + 5 + kG - 1) / kG + 1 + ahead;
+    // output rows r..r+rs-1 read table rows r-hr .. r+rs+hr: 2hr+rs+1 rows,
+    // spread over at most ceil((2hr+rs+1)/4)+1 groups
+    g.ng = (2 * hr + kG * sg + 1 + kG - 1) / kG + 1 + kTableAhead;
     g.nr = g.ng * kG;
-    g.stride = w + 2 * hc + 4;
     return g;
 }
 
 template <typename T>
-inline size_t ring_smem_bytes(int w, int hr, int hc, int ahead) {
-    const RingGeom g = ring_geom(w, hr, hc, ahead);
-    const int ncg = 1 + ahead;
-    return sizeof(double) * static_cast<size_t>(g.nr) * g.stride + sizeof(T) * static_cast<size_t>(ncg) * kG * w +
-           2 * sizeof(uint64_t) * (g.ng + ncg + 1) + (sizeof(uint4) + sizeof(int2)) * kRingRows;
+inline size_t ring_smem_bytes(int hr, int boxc, int sg) {
+    const RingGeom g = ring_geom(hr, sg);
+    return 128 /* alignment slack */ + sizeof(double) * static_cast<size_t>(g.nr + kG * sg) * boxc +
+           sizeof(T) * static_cast<size_t>(kCutGroups) * kG * kW + 2 * sizeof(uint64_t) * (g.ng + kCutGroups);
 }
 
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// Blocking wait that suspends the thread in the barrier unit (up to hint_ns per
+// try) instead of spinning through issue slots the other warps need.
+__device__ __forceinline__ void mbar_wait_susp(uint64_t* bar, unsigned parity, unsigned hint_ns) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "UWB_WAITS_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra UWB_WAITS_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(hint_ns)
+        : "memory");
+}
+// One suspended try (returns whether the phase completed).
+__device__ __forceinline__ bool mbar_try_susp(uint64_t* bar, unsigned parity, unsigned hint_ns) {
+    unsigned ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(hint_ns)
+        : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ double lds_f64(unsigned addr) {
-    double v;
-    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
-    return v;
+// 3-D tensor box -> L2 (no shared memory, no completion tracking).
+__device__ __forceinline__ void tma_prefetch3(const CUtensorMap* map, int x, int y, int z) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(x), "r"(y), "r"(z)
+                 : "memory");
 }
-__device__ __forceinline__ float lds_f32(unsigned addr) {
-    float v;
-    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
-    return v;
+// 3-D tensor TMA box -> shared memory, completing on `bar`.
+__device__ __forceinline__ void tma_box3(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
 }
-template <typename T>
-__device__ __forceinline__ double lds_cut(unsigned addr);
-template <>
-__device__ __forceinline__ double lds_cut<float>(unsigned addr) { return static_cast<double>(lds_f32(addr)); }
-template <>
-__device__ __forceinline__ double lds_cut<double>(unsigned addr) { return lds_f64(addr); }
 
 // Per-column constants of one output column.
 struct ColConst {
@@ -101,25 +149,103 @@ __device__ __forceinline__ ColConst col_const(int c, int cols, int hc, int gc, i
     return k;
 }
 
+__device__ __forceinline__ double tap(const char* row, unsigned off) {
+    return *reinterpret_cast<const double*>(row + off);
+}
 // Four-tap sums of one cell: sat.hpp:32-33 for outer and guard, then outer - guard.
-__device__ __forceinline__ double train_sum(const ColConst& k, unsigned rA, unsigned rB, unsigned rC, unsigned rD) {
-    const double rs_o = dsub(dadd(lds_f64(rA + k.xa), lds_f64(rB + k.xb)), dadd(lds_f64(rA + k.xb), lds_f64(rB + k.xa)));
-    const double rs_g = dsub(dadd(lds_f64(rC + k.ya), lds_f64(rD + k.yb)), dadd(lds_f64(rC + k.yb), lds_f64(rD + k.ya)));
+__device__ __forceinline__ double train_sum(const ColConst& k, const char* rA, const char* rB, const char* rC,
+                                            const char* rD) {
+    const double rs_o = dsub(dadd(tap(rA, k.xa), tap(rB, k.xb)), dadd(tap(rA, k.xb), tap(rB, k.xa)));
+    const double rs_g = dsub(dadd(tap(rC, k.ya), tap(rD, k.yb)), dadd(tap(rC, k.yb), tap(rD, k.ya)));
     return dsub(rs_o, rs_g);
 }
 
-template <typename T, int NCW, int AHEAD>
-__global__ void __launch_bounds__((NCW + 1) * kWarp)
-cfar_ws_kernel(CfarLaunch L) {
-    constexpr int W = NCW * kWarp * kColsPerThread;
-    constexpr int kNcg = 1 + AHEAD; // CUT groups in the ring
-    extern __shared__ __align__(16) unsigned char ring_smem[];
-    const RingGeom G = ring_geom(W, L.hr, L.hc, AHEAD);
+// Mask words, optional per-cell outputs and detections of one thread's block
+// (rows r0..r0+RS-1, columns c_first + 32 j); lane k*CPT+j stores word (k, j).
+template <int RS, int CPT>
+__device__ __forceinline__ void emit_block(const CfarLaunch& L, int64_t map, int r0, int r_last, int c_word0,
+                                           int c_first, const bool (&okc)[CPT], const bool (&hit)[RS][CPT],
+                                           const double (&v)[RS][CPT], const double (&thr)[RS][CPT],
+                                           bool per_cell) {
+    const int lane = threadIdx.x % kWarp;
+    const int cols = static_cast<int>(L.cols);
+    unsigned my_word = 0, any_bits = 0;
+#pragma unroll
+    for (int k = 0; k < RS; ++k) {
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) {
+            const unsigned b = __ballot_sync(0xffffffffu, hit[k][j]);
+            any_bits |= b;
+            if (lane == k * CPT + j) my_word = b;
+        }
+    }
+    const int wk = lane / CPT, wj = lane % CPT;
+    const int wc = c_word0 + wj * kWarp; // first column of the word
+    if (lane < CPT * RS && r0 + wk <= r_last && wc < cols && L.mask_bits)
+        L.mask_bits[map * L.mask_map_stride + static_cast<int64_t>(r0 + wk) * L.words_per_row + (wc >> 5)] = my_word;
+    if (per_cell) { // parity runs only
+#pragma unroll
+        for (int k = 0; k < RS; ++k) {
+#pragma unroll
+            for (int j = 0; j < CPT; ++j) {
+                if (okc[j] && r0 + k <= r_last) {
+                    const int64_t cell =
+                        map * L.geo.rows * L.cols + static_cast<int64_t>(r0 + k) * cols + c_first + j * kWarp;
+                    if (L.mask_u8) L.mask_u8[cell] = hit[k][j] ? 1 : 0;
+                    if (L.thresholds) L.thresholds[cell] = thr[k][j];
+                }
+            }
+        }
+    }
+    if (any_bits) { // detections (about pfa of the cells plus targets)
+#pragma unroll
+        for (int k = 0; k < RS; ++k) {
+#pragma unroll
+            for (int j = 0; j < CPT; ++j) {
+                const unsigned b = __ballot_sync(0xffffffffu, hit[k][j]);
+                if (b) {
+                    unsigned long long base = 0;
+                    if (lane == 0) base = atomicAdd(L.det_counts + map, static_cast<unsigned long long>(__popc(b)));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    if (hit[k][j]) {
+                        const unsigned long long slot = base + __popc(b & ((1u << lane) - 1u));
+                        if (slot < static_cast<unsigned long long>(L.det_cap)) {
+                            uwb_detection d;
+                            d.row = static_cast<uint64_t>(r0 + k);
+                            d.col = static_cast<uint64_t>(c_first + j * kWarp);
+                            d.value = v[k][j];
+                            d.threshold = thr[k][j];
+                            L.dets[map * L.det_cap + slot] = d;
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
+// NCW consumer warps x CPT columns per thread = kW columns; BOXC = ring row
+// width in doubles (the table box width, >= kW + 2 hc + 4, multiple of 4).
+template <typename T, int NCW, int CPT, int BOXC, int SG>
+__global__ void __launch_bounds__((NCW + 1) * kWarp, SG == 1 ? kCtasPerSm : kCtasPerSm - 1)
+cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUtensorMap tmap_tab,
+               const __grid_constant__ CUtensorMap tmap_cut) {
+    static_assert(NCW * CPT * kWarp == kW, "tile width");
+    static_assert(kCutGroups % SG == 0, "CUT ring depth");
+    constexpr int RS = kG * SG; // output rows per consumer step
+    constexpr unsigned kRowBytes = 8u * BOXC;
+    constexpr unsigned kTabBox = kG * kRowBytes;
+    constexpr unsigned kCutBox = kG * kW * sizeof(T);
+    extern __shared__ unsigned char ring_raw[];
+    unsigned char* ring_smem =
+        ring_raw + ((128u - (static_cast<unsigned>(__cvta_generic_to_shared(ring_raw)) & 127u)) & 127u);
+    const RingGeom G = ring_geom(L.hr, SG);
     double* slots = reinterpret_cast<double*>(ring_smem);
-    T* cuts = reinterpret_cast<T*>(slots + static_cast<size_t>(G.nr) * G.stride);
-    uint64_t* full_t = reinterpret_cast<uint64_t*>(cuts + static_cast<size_t>(kNcg) * kG * W);
+    const char* ring = reinterpret_cast<const char*>(ring_smem);
+    T* cuts = reinterpret_cast<T*>(slots + static_cast<size_t>(G.nr + RS) * BOXC);
+    uint64_t* full_t = reinterpret_cast<uint64_t*>(cuts + static_cast<size_t>(kCutGroups) * kG * kW);
     uint64_t* full_c = full_t + G.ng;
-    uint64_t* empty_t = full_c + kNcg;
+    uint64_t* empty_t = full_c + kCutGroups;
     uint64_t* empty_c = empty_t + G.ng;
 
     const int64_t job = blockIdx.y;
@@ -129,48 +255,24 @@ cfar_ws_kernel(CfarLaunch L) {
     const int chunk = static_cast<int>(blockIdx.x / L.col_tiles);
     const int rows = static_cast<int>(L.geo.rows), cols = static_cast<int>(L.cols);
     const int hr = L.hr, hc = L.hc, gr = L.gr, gc = L.gc;
-    const int c0 = col_tile * W;
+    const int c0 = col_tile * kW;
     const int ra = static_cast<int>(L.geo.owned_begin(slab)) + chunk * kRingRows;
     const int rb = min(ra + kRingRows, static_cast<int>(L.geo.owned_end(slab)));
     if (ra >= rb) return;
     const int trow0 = static_cast<int>(L.geo.table_begin(slab));
-    const double* tab = L.table + job * L.table_stride;
-    const int64_t ld = L.table_ld;
-    const T* cut_base = static_cast<const T*>(L.maps) + map * L.map_stride;
 
-    // table columns the strip touches, as a 16-byte aligned storage span
-    const int jlo = max(0, c0 - hc);
-    const int jhi = min(cols, c0 + W + hc);
-    const int e_lo = (kTabShift + jlo) & ~1;
-    const int e_hi = kTabShift + jhi;
-    const unsigned copy_bytes = static_cast<unsigned>(((e_hi - e_lo) / 2 + 1) * 16);
-    const int strip_w = min(W, cols - c0);
-    const unsigned cut_bytes = static_cast<unsigned>(((strip_w * static_cast<int>(sizeof(T)) + 15) / 16) * 16);
-
+    // table storage columns of the ring rows: [e_lo, e_lo + BOXC), 16-byte aligned
+    const int e_lo = (kTabShift + max(0, c0 - hc)) & ~1;
     // padded table rows needed by output rows [ra, rb), in groups of kG from i_lo
     const int i_lo = max(0, ra - hr);
     const int i_hi = min(rows, rb + hr);
-    const int n_steps = (rb - ra + kG - 1) / kG;
+    const int n_steps = (rb - ra + RS - 1) / RS;
+    const int n_cg = (rb - ra + kG - 1) / kG; // CUT groups
 
-    // Per output row of the tile: the ring addresses of its four tap rows and
-    // its clamped outer / guard heights, computed once (cfar.cpp:117-120).
-    // (the ring, CUT and 2 * (ng + kNcg) barrier regions keep 16-byte alignment)
-    uint4* tap_rows = reinterpret_cast<uint4*>(empty_c + kNcg);
-    int2* heights = reinterpret_cast<int2*>(tap_rows + kRingRows);
-    {
-        const unsigned ring_base = smem_u32(slots);
-        const unsigned row_bytes = static_cast<unsigned>(G.stride) * 8u;
-        auto ring_addr = [&](int i) { return ring_base + static_cast<unsigned>((i - i_lo) % G.nr) * row_bytes; };
-        for (int lr = threadIdx.x; lr < rb - ra; lr += blockDim.x) {
-            const int r = ra + lr;
-            const int iA = clamp_lo32(r, hr), iB = clamp_hi32(r, hr, rows) + 1;
-            const int iC = clamp_lo32(r, gr), iD = clamp_hi32(r, gr, rows) + 1;
-            tap_rows[lr] = make_uint4(ring_addr(iA), ring_addr(iB), ring_addr(iC), ring_addr(iD));
-            heights[lr] = make_int2(iB - iA, iD - iC);
-        }
-    }
+    // ring byte offset of padded table row i (i_lo <= i <= i_hi)
+    auto ring_off = [&](int i) { return static_cast<unsigned>((i - i_lo) % G.nr) * kRowBytes; };
     if (threadIdx.x == 0) {
-        for (int s = 0; s < G.ng + kNcg; ++s) {
+        for (int s = 0; s < G.ng + kCutGroups; ++s) {
             mbar_init(&full_t[s], 1);
             mbar_init(&empty_t[s], NCW);
         }
@@ -182,201 +284,240 @@ cfar_ws_kernel(CfarLaunch L) {
     const int lane = threadIdx.x % kWarp;
 
     if (warp == NCW) {
-        // =========================== producer warp ===========================
+        // =========================== producer thread ===========================
         if (lane != 0) return;
         const int last_grp = (i_hi - i_lo) / kG;
-        int grp = 0, gslot = 0, gphase = 0; // next table group, its slot and empty-phase
-        int cslot = 0, cphase = 0;
-        for (int step = 0; step < n_steps; ++step) {
-            const int r_last = min(ra + step * kG + kG, rb) - 1;
-            const int need = min((clamp_hi32(r_last, hr, rows) + 1 - i_lo) / kG, last_grp);
-            for (; grp <= need; ++grp) {
-                if (grp >= G.ng) mbar_wait(&empty_t[gslot], static_cast<unsigned>(gphase ^ 1));
+        for (int g = 0; g <= min(last_grp, kPfGroups - 1); ++g)
+            tma_prefetch3(&tmap_tab, e_lo, i_lo + g * kG - trow0, static_cast<int>(job));
+        for (int g = 0; g < min(n_cg, kPfGroups); ++g)
+            tma_prefetch3(&tmap_cut, c0, ra + g * kG, static_cast<int>(map));
+        int grp = 0, gslot = 0, gphase = 0;   // next table group, its slot and empty-phase
+        int cstep = 0, cslot = 0, cphase = 0; // next CUT group
+        while (grp <= last_grp || cstep < n_cg) {
+            bool progress = false;
+            if (grp <= last_grp && (grp < G.ng || mbar_test(&empty_t[gslot], static_cast<unsigned>(gphase ^ 1)))) {
                 const int first = i_lo + grp * kG;
-                const int cnt = min(kG, i_hi + 1 - first);
-                mbar_expect_tx(&full_t[gslot], copy_bytes * cnt);
-                for (int k = 0; k < cnt; ++k)
-                    bulk_g2s(slots + static_cast<size_t>(gslot * kG + k) * G.stride,
-                             tab + static_cast<int64_t>(first + k - trow0) * ld + e_lo, copy_bytes, &full_t[gslot]);
+                // the first SG groups are mirrored after the last slot, so RS
+                // consecutive ring rows are always contiguous in memory
+                mbar_expect_tx(&full_t[gslot], gslot < SG ? 2 * kTabBox : kTabBox);
+                tma_box3(slots + static_cast<size_t>(gslot * kG) * BOXC, &tmap_tab, e_lo, first - trow0,
+                         static_cast<int>(job), &full_t[gslot]);
+                if (gslot < SG)
+                    tma_box3(slots + static_cast<size_t>(G.nr + gslot * kG) * BOXC, &tmap_tab, e_lo, first - trow0,
+                             static_cast<int>(job), &full_t[gslot]);
+                if (grp + kPfGroups <= last_grp)
+                    tma_prefetch3(&tmap_tab, e_lo, first + kPfGroups * kG - trow0, static_cast<int>(job));
                 if (++gslot == G.ng) { gslot = 0; gphase ^= 1; }
+                ++grp;
+                progress = true;
             }
-            if (step >= kNcg) mbar_wait(&empty_c[cslot], static_cast<unsigned>(cphase ^ 1));
-            const int first = ra + step * kG;
-            const int cnt = min(kG, rb - first);
-            mbar_expect_tx(&full_c[cslot], cut_bytes * cnt);
-            for (int k = 0; k < cnt; ++k)
-                bulk_g2s(cuts + static_cast<size_t>(cslot * kG + k) * W,
-                         cut_base + static_cast<int64_t>(first + k) * L.ld + c0, cut_bytes, &full_c[cslot]);
-            if (++cslot == kNcg) { cslot = 0; cphase ^= 1; }
+            if (cstep < n_cg &&
+                (cstep < kCutGroups || mbar_test(&empty_c[cslot], static_cast<unsigned>(cphase ^ 1)))) {
+                const int first = ra + cstep * kG;
+                mbar_expect_tx(&full_c[cslot], kCutBox);
+                tma_box3(cuts + static_cast<size_t>(cslot) * kG * kW, &tmap_cut, c0, first, static_cast<int>(map),
+                         &full_c[cslot]);
+                if (cstep + kPfGroups < n_cg)
+                    tma_prefetch3(&tmap_cut, c0, first + kPfGroups * kG, static_cast<int>(map));
+                if (++cslot == kCutGroups) { cslot = 0; cphase ^= 1; }
+                ++cstep;
+                progress = true;
+            }
+            if (!progress) {
+                // both rings full: sleep on the slot the consumers free first
+                // (CUT slot of cstep frees after step cstep - kCutGroups; table
+                // group grp's slot after the step whose window leaves group grp - ng)
+                const int s_cut = cstep < n_cg ? (cstep - kCutGroups) / SG : INT_MAX;
+                const int s_tab = grp <= last_grp ? ((grp - G.ng + 1) + (hr + i_lo - ra) / kG) / SG : INT_MAX;
+                if (s_tab <= s_cut)
+                    mbar_try_susp(&empty_t[gslot], static_cast<unsigned>(gphase ^ 1), L.sleep_ns);
+                else
+                    mbar_try_susp(&empty_c[cslot], static_cast<unsigned>(cphase ^ 1), L.sleep_ns);
+            }
         }
         return;
     }
 
     // ============================ consumer warps ============================
-    const unsigned cut_smem = smem_u32(cuts);
-    const unsigned tap_smem = smem_u32(tap_rows);
-    const unsigned ht_smem = smem_u32(heights);
-    const int tc = warp * kWarp * kColsPerThread + lane; // my first column within the tile
-    const ColConst K0 = col_const(c0 + tc, cols, hc, gc, e_lo);
-    const ColConst K1 = col_const(c0 + tc + kWarp, cols, hc, gc, e_lo);
-    const bool exact_always = L.thresholds != nullptr;
+    const int wc0 = c0 + warp * kWarp * CPT; // first column of my warp
+    const int tc = warp * kWarp * CPT + lane; // my first column within the tile
+    ColConst K[CPT];
+    bool okc[CPT];
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+        K[j] = col_const(c0 + tc + j * kWarp, cols, hc, gc, e_lo);
+        okc[j] = K[j].ok;
+    }
+    const bool per_cell = L.thresholds != nullptr || L.mask_u8 != nullptr;
+    // Interior fast path: the warp's columns have unclamped windows, so column
+    // j's taps sit exactly 32 j doubles after column 0's, and n = n_int
+    // (cfar.cpp:28-32).
+    const bool warp_cols_interior = !per_cell && wc0 - hc >= 0 && wc0 + kWarp * CPT - 1 + hc <= cols - 1;
+    const int n_int = (2 * hr + 1) * (2 * hc + 1) - (2 * gr + 1) * (2 * gc + 1);
+    const double alpha_int = n_int > 0 ? __ldg(L.alpha + n_int) : 0.0;
+    // 0 <= cut < sum * fast_k  implies  cut < alpha * (sum / n) (relative margin 1e-13)
+    const double fast_k = n_int > 0 ? dmul(ddiv(alpha_int, static_cast<double>(n_int)), 1.0 - 1e-13) : 0.0;
 
+    // ring slots of the (unclamped) tap rows of output row r0, advanced 4 rows per step
+    auto slot0 = [&](int i) { return ((i - i_lo) % G.nr + G.nr) % G.nr; };
+    int sA = slot0(ra - hr), sB = slot0(ra + hr + 1), sC = slot0(ra - gr), sD = slot0(ra + gr + 1);
     int waited = -1, wslot = 0, wphase = 0; // full_t groups known resident
     int released = -1, rslot = 0;            // table groups handed back
     int cslot = 0, cphase = 0;
-    // per-column alpha cache: n is constant over interior rows
-    int n0c = -1, n1c = -1;
-    double k0 = 0.0, k1 = 0.0;
+    // per-column alpha cache for the general path
+    int ncache[CPT];
+    double kcache[CPT];
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+        ncache[j] = -1;
+        kcache[j] = 0.0;
+    }
 
     for (int step = 0; step < n_steps; ++step) {
-        const int r0 = ra + step * kG;
-        const int r_last = min(r0 + kG, rb) - 1;
+        const int r0 = ra + step * RS;
+        const int r_last = min(r0 + RS, rb) - 1;
         {
             const int need = (clamp_hi32(r_last, hr, rows) + 1 - i_lo) / kG;
             while (waited < need) {
-                mbar_wait(&full_t[wslot], static_cast<unsigned>(wphase));
+                mbar_wait_susp(&full_t[wslot], static_cast<unsigned>(wphase), L.sleep_ns);
                 ++waited;
                 if (++wslot == G.ng) { wslot = 0; wphase ^= 1; }
             }
         }
-        mbar_wait(&full_c[cslot], static_cast<unsigned>(cphase));
-        const unsigned cut_grp = cut_smem + static_cast<unsigned>(cslot * kG * W) * sizeof(T);
-        // phase 1: ring rows and clamped heights of the step's rows (table lookups)
-        unsigned RA[kG], RB[kG], RC[kG], RD[kG];
-        int HR[kG], HG[kG];
 #pragma unroll
-        for (int k = 0; k < kG; ++k) {
-            const int lr = min(r0 + k, r_last) - ra;
-            uint4 t;
-            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                         : "=r"(t.x), "=r"(t.y), "=r"(t.z), "=r"(t.w)
-                         : "r"(tap_smem + 16u * static_cast<unsigned>(lr)));
-            int2 h;
-            asm volatile("ld.shared.v2.s32 {%0,%1}, [%2];" : "=r"(h.x), "=r"(h.y) : "r"(ht_smem + 8u * static_cast<unsigned>(lr)));
-            RA[k] = t.x; RB[k] = t.y; RC[k] = t.z; RD[k] = t.w;
-            HR[k] = h.x;
-            HG[k] = h.y;
-        }
-        // phase 2: every cell of the step (loads first, decisions after)
-        double v[kG][2], sum[kG][2], approx[kG][2];
-        int n[kG][2];
-        bool need_exact[kG][2], hit[kG][2];
-        bool any_slow = false;
+        for (int q = 0; q < SG; ++q)
+            if (q == 0 || r0 + q * kG <= r_last)
+                mbar_wait_susp(&full_c[cslot + q], static_cast<unsigned>(cphase), L.sleep_ns);
+        const T* cut_grp = cuts + static_cast<size_t>(cslot) * kG * kW;
+        double v[RS][CPT], thr[RS][CPT];
+        bool hit[RS][CPT];
+        if (L.debug & 1u) goto release; // data-movement probe
+        {
+            const bool fast = warp_cols_interior && r0 - hr >= 0 && r0 + RS - 1 == r_last && r_last + hr <= rows - 1;
+            if (fast) {
+                // ---- interior step: 8 row pointers, compile-time tap offsets ----
+                const char* pA = ring + static_cast<unsigned>(sA) * kRowBytes;
+                const char* pB = ring + static_cast<unsigned>(sB) * kRowBytes;
+                const char* pC = ring + static_cast<unsigned>(sC) * kRowBytes;
+                const char* pD = ring + static_cast<unsigned>(sD) * kRowBytes;
+                double sum[RS][CPT];
+                bool need = false;
 #pragma unroll
-        for (int k = 0; k < kG; ++k) {
-            const unsigned cut_row = cut_grp + static_cast<unsigned>(k * W) * sizeof(T);
+                for (int k = 0; k < RS; ++k) {
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                const ColConst& K = j ? K1 : K0;
-                v[k][j] = lds_cut<T>(cut_row + static_cast<unsigned>(tc + j * kWarp) * sizeof(T));
-                sum[k][j] = train_sum(K, RA[k], RB[k], RC[k], RD[k]);
-                n[k][j] = HR[k] * K.ow - HG[k] * K.gw;
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < kG; ++k) {
-            const bool row_ok = r0 + k <= r_last;
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                const ColConst& K = j ? K1 : K0;
-                int& nc = j ? n1c : n0c;
-                double& kc = j ? k1 : k0;
-                if (n[k][j] != nc && row_ok) {
-                    nc = n[k][j];
-                    kc = ddiv(__ldg(L.alpha + n[k][j]), static_cast<double>(n[k][j]));
-                }
-                approx[k][j] = dmul(sum[k][j], kc);
-                const bool ok = K.ok && row_ok;
-                hit[k][j] = ok && v[k][j] > approx[k][j];
-                need_exact[k][j] = ok && (exact_always || hit[k][j] || v[k][j] < 0.0 ||
-                                          !(fabs(dsub(v[k][j], approx[k][j])) > 1e-13 * fabs(approx[k][j])));
-                any_slow |= need_exact[k][j];
-            }
-        }
-        // phase 3: the reference expression where it is needed (rare, warp-uniform branch)
-        double thr[kG][2];
-#pragma unroll
-        for (int k = 0; k < kG; ++k) thr[k][0] = thr[k][1] = 0.0;
-        if (__any_sync(0xffffffffu, any_slow)) {
-#pragma unroll
-            for (int k = 0; k < kG; ++k) {
-#pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    if (need_exact[k][j]) {
-                        thr[k][j] = dmul(__ldg(L.alpha + n[k][j]), ddiv(sum[k][j], static_cast<double>(n[k][j])));
-                        hit[k][j] = v[k][j] > thr[k][j];
-                        if (v[k][j] < 0.0)
-                            report_min(L.first_bad + 2 * map + 1,
-                                       static_cast<unsigned long long>(static_cast<int64_t>(r0 + k) * cols + c0 + tc +
-                                                                       j * kWarp));
+                    for (int j = 0; j < CPT; ++j) {
+                        const unsigned o = k * kRowBytes + j * kWarp * 8u;
+                        const double rs_o = dsub(dadd(tap(pA, K[0].xa + o), tap(pB, K[0].xb + o)),
+                                                 dadd(tap(pA, K[0].xb + o), tap(pB, K[0].xa + o)));
+                        const double rs_g = dsub(dadd(tap(pC, K[0].ya + o), tap(pD, K[0].yb + o)),
+                                                 dadd(tap(pC, K[0].yb + o), tap(pD, K[0].ya + o)));
+                        sum[k][j] = dsub(rs_o, rs_g);
+                        v[k][j] = static_cast<double>(cut_grp[k * kW + tc + j * kWarp]);
+                        need |= !(v[k][j] < dmul(sum[k][j], fast_k)) || v[k][j] < 0.0;
                     }
                 }
-            }
-        }
-        // phase 4: mask words (lane w stores word w of the 4x2 block), optional
-        // per-cell outputs, detections
-        {
-            unsigned my_word = 0, any_bits = 0;
+                if (__any_sync(0xffffffffu, need)) {
 #pragma unroll
-            for (int k = 0; k < kG; ++k) {
+                    for (int k = 0; k < RS; ++k) {
 #pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    const unsigned b = __ballot_sync(0xffffffffu, hit[k][j]);
-                    any_bits |= b;
-                    if (lane == k * 2 + j) my_word = b;
-                }
-            }
-            const int wk = lane >> 1, wj = lane & 1;
-            const int wc = c0 + warp * kWarp * kColsPerThread + wj * kWarp; // first column of the word
-            if (lane < 2 * kG && r0 + wk <= r_last && wc < cols && L.mask_bits)
-                L.mask_bits[map * L.mask_map_stride + static_cast<int64_t>(r0 + wk) * L.words_per_row + (wc >> 5)] =
-                    my_word;
-            if (exact_always || L.mask_u8) { // parity runs only
-#pragma unroll
-                for (int k = 0; k < kG; ++k) {
-#pragma unroll
-                    for (int j = 0; j < 2; ++j) {
-                        const ColConst& K = j ? K1 : K0;
-                        if (K.ok && r0 + k <= r_last) {
-                            const int64_t cell = map * L.geo.rows * L.cols + static_cast<int64_t>(r0 + k) * cols +
-                                                 c0 + tc + j * kWarp;
-                            if (L.mask_u8) L.mask_u8[cell] = hit[k][j] ? 1 : 0;
-                            if (L.thresholds) L.thresholds[cell] = thr[k][j];
+                        for (int j = 0; j < CPT; ++j) {
+                            thr[k][j] = 0.0;
+                            hit[k][j] = false;
+                            if (!(v[k][j] < dmul(sum[k][j], fast_k)) || v[k][j] < 0.0) {
+                                thr[k][j] = dmul(alpha_int, ddiv(sum[k][j], static_cast<double>(n_int)));
+                                hit[k][j] = v[k][j] > thr[k][j];
+                                if (v[k][j] < 0.0)
+                                    report_min(L.first_bad + 2 * map + 1,
+                                               static_cast<unsigned long long>(static_cast<int64_t>(r0 + k) * cols +
+                                                                               c0 + tc + j * kWarp));
+                            }
                         }
                     }
+                    emit_block<RS, CPT>(L, map, r0, r_last, wc0, c0 + tc, okc, hit, v, thr, false);
+                } else if (lane < CPT * RS && L.mask_bits) { // no hit in the block: zero mask words
+                    const int wk = lane / CPT, wc = wc0 + (lane % CPT) * kWarp;
+                    L.mask_bits[map * L.mask_map_stride + static_cast<int64_t>(r0 + wk) * L.words_per_row +
+                                (wc >> 5)] = 0u;
                 }
-            }
-            if (any_bits) { // detections (about pfa of the cells plus targets)
+            } else {
+                // ---- general step: clamped windows, per-cell n ----
+                const char* RA[RS];
+                const char* RB[RS];
+                const char* RC[RS];
+                const char* RD[RS];
+                int HR[RS], HG[RS];
 #pragma unroll
-                for (int k = 0; k < kG; ++k) {
+                for (int k = 0; k < RS; ++k) {
+                    // clamped window rows and heights (cfar.cpp:117-120)
+                    const int r = min(r0 + k, r_last);
+                    const int iA = clamp_lo32(r, hr), iB = clamp_hi32(r, hr, rows) + 1;
+                    const int iC = clamp_lo32(r, gr), iD = clamp_hi32(r, gr, rows) + 1;
+                    RA[k] = ring + ring_off(iA);
+                    RB[k] = ring + ring_off(iB);
+                    RC[k] = ring + ring_off(iC);
+                    RD[k] = ring + ring_off(iD);
+                    HR[k] = iB - iA;
+                    HG[k] = iD - iC;
+                }
+                double sum[RS][CPT], approx[RS][CPT];
+                int n[RS][CPT];
+                bool need_exact[RS][CPT];
+                bool any_slow = false;
 #pragma unroll
-                    for (int j = 0; j < 2; ++j) {
-                        const unsigned b = __ballot_sync(0xffffffffu, hit[k][j]);
-                        if (b) {
-                            unsigned long long base = 0;
-                            if (lane == 0)
-                                base = atomicAdd(L.det_counts + map, static_cast<unsigned long long>(__popc(b)));
-                            base = __shfl_sync(0xffffffffu, base, 0);
-                            if (hit[k][j]) {
-                                const unsigned long long slot = base + __popc(b & ((1u << lane) - 1u));
-                                if (slot < static_cast<unsigned long long>(L.det_cap)) {
-                                    uwb_detection d;
-                                    d.row = static_cast<uint64_t>(r0 + k);
-                                    d.col = static_cast<uint64_t>(c0 + tc + j * kWarp);
-                                    d.value = v[k][j];
-                                    d.threshold = thr[k][j];
-                                    L.dets[map * L.det_cap + slot] = d;
-                                }
+                for (int k = 0; k < RS; ++k) {
+#pragma unroll
+                    for (int j = 0; j < CPT; ++j) {
+                        v[k][j] = static_cast<double>(cut_grp[k * kW + tc + j * kWarp]);
+                        sum[k][j] = train_sum(K[j], RA[k], RB[k], RC[k], RD[k]);
+                        n[k][j] = HR[k] * K[j].ow - HG[k] * K[j].gw;
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < RS; ++k) {
+                    const bool row_ok = r0 + k <= r_last;
+#pragma unroll
+                    for (int j = 0; j < CPT; ++j) {
+                        if (n[k][j] != ncache[j] && row_ok) {
+                            ncache[j] = n[k][j];
+                            kcache[j] = ddiv(__ldg(L.alpha + n[k][j]), static_cast<double>(n[k][j]));
+                        }
+                        approx[k][j] = dmul(sum[k][j], kcache[j]);
+                        const bool ok = K[j].ok && row_ok;
+                        hit[k][j] = ok && v[k][j] > approx[k][j];
+                        need_exact[k][j] = ok && (per_cell || hit[k][j] || v[k][j] < 0.0 ||
+                                                  !(fabs(dsub(v[k][j], approx[k][j])) > 1e-13 * fabs(approx[k][j])));
+                        any_slow |= need_exact[k][j];
+                        thr[k][j] = 0.0;
+                    }
+                }
+                // the reference expression where it is needed (rare, warp-uniform branch)
+                if (__any_sync(0xffffffffu, any_slow)) {
+#pragma unroll
+                    for (int k = 0; k < RS; ++k) {
+#pragma unroll
+                        for (int j = 0; j < CPT; ++j) {
+                            if (need_exact[k][j]) {
+                                thr[k][j] =
+                                    dmul(__ldg(L.alpha + n[k][j]), ddiv(sum[k][j], static_cast<double>(n[k][j])));
+                                hit[k][j] = v[k][j] > thr[k][j];
+                                if (v[k][j] < 0.0)
+                                    report_min(L.first_bad + 2 * map + 1,
+                                               static_cast<unsigned long long>(static_cast<int64_t>(r0 + k) * cols +
+                                                                               c0 + tc + j * kWarp));
                             }
                         }
                     }
                 }
+                emit_block<RS, CPT>(L, map, r0, r_last, wc0, c0 + tc, okc, hit, v, thr, per_cell);
             }
         }
+    release:
         // hand back this step's CUT group and the table groups no later step reads
         __syncwarp();
         if (lane == 0) {
-            mbar_arrive(&empty_c[cslot]);
+#pragma unroll
+            for (int q = 0; q < SG; ++q)
+                if (q == 0 || r0 + q * kG <= r_last) mbar_arrive(&empty_c[cslot + q]);
             if (step + 1 < n_steps) {
                 const int keep_row = max(0, r_last + 1 - hr);
                 const int done = (keep_row - i_lo) / kG - 1; // groups entirely below keep_row
@@ -387,71 +528,112 @@ cfar_ws_kernel(CfarLaunch L) {
                 }
             }
         }
-        if (++cslot == kNcg) { cslot = 0; cphase ^= 1; }
+        cslot += SG;
+        if (cslot == kCutGroups) { cslot = 0; cphase ^= 1; }
+        sA += RS; if (sA >= G.nr) sA -= G.nr;
+        sB += RS; if (sB >= G.nr) sB -= G.nr;
+        sC += RS; if (sC >= G.nr) sC -= G.nr;
+        sD += RS; if (sD >= G.nr) sD -= G.nr;
     }
 }
 
-template <typename T, int NCW, int AHEAD>
-cudaError_t go(const CfarLaunch& L0, size_t smem, cudaStream_t stream) {
-    constexpr int W = NCW * kWarp * kColsPerThread;
+// ---- host side: tensor maps ----
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+bool encode3(CUtensorMap* m, CUtensorMapDataType dt, size_t esz, const void* base, uint64_t d0, uint64_t d1,
+             uint64_t d2, uint64_t s1, uint64_t s2, unsigned b0, unsigned b1) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t dims[3] = {d0, d1, d2};
+    const cuuint64_t strides[2] = {s1 * esz, s2 * esz};
+    const cuuint32_t box[3] = {b0, b1, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return fn(m, dt, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <typename T, int NCW, int CPT, int BOXC, int SG>
+cudaError_t go(const CfarLaunch& L0, cudaStream_t stream) {
     CfarLaunch L = L0;
-    L.col_tiles = (L.cols + W - 1) / W;
+    L.sleep_ns = 20000;
+    if (const char* e = getenv("UWB_RING_SLEEP_NS")) L.sleep_ns = static_cast<unsigned>(atoi(e));
+    L.debug = 0;
+    if (const char* e = getenv("UWB_RING_DEBUG")) L.debug = static_cast<unsigned>(atoi(e));
+    L.col_tiles = (L.cols + kW - 1) / kW;
     L.row_chunks = (L.geo.slab_rows + kRingRows - 1) / kRingRows;
+    const int64_t n_maps = L.n_jobs / L.geo.n_slabs;
+    CUtensorMap tmap_tab, tmap_cut;
+    const uint64_t tab_rows = static_cast<uint64_t>(L.table_stride / L.table_ld);
+    if (!encode3(&tmap_tab, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, L.table, L.table_ld, tab_rows, L.n_jobs, L.table_ld,
+                 L.table_stride, BOXC, kG))
+        return cudaErrorNotSupported;
+    // a single map's stride is never used; give the encoder a valid one
+    const int64_t mstride = n_maps > 1 ? L.map_stride : (L.ld * L.geo.rows + 1) / 2 * 2;
+    if (!encode3(&tmap_cut, sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                 sizeof(T), L.maps, L.cols, L.geo.rows, n_maps, L.ld, mstride, kW, kG))
+        return cudaErrorNotSupported;
+    const size_t smem = ring_smem_bytes<T>(L.hr, BOXC, SG);
+    if (smem > 227 * 1024) return cudaErrorNotSupported;
     const dim3 grid(static_cast<unsigned>(L.col_tiles * L.row_chunks), static_cast<unsigned>(L.n_jobs), 1);
-    cudaError_t e = cudaFuncSetAttribute(cfar_ws_kernel<T, NCW, AHEAD>,
+    cudaError_t e = cudaFuncSetAttribute(cfar_ws_kernel<T, NCW, CPT, BOXC, SG>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     ++g_kernel_launches;
-    cfar_ws_kernel<T, NCW, AHEAD><<<grid, (NCW + 1) * kWarp, smem, stream>>>(L);
+    cfar_ws_kernel<T, NCW, CPT, BOXC, SG><<<grid, (NCW + 1) * kWarp, smem, stream>>>(L, tmap_tab, tmap_cut);
     return cudaGetLastError();
 }
 
+template <typename T, int BOXC>
+cudaError_t go_ncw(const CfarLaunch& L, int ncw, cudaStream_t stream) {
+    int sg = 1;
+    if (const char* a = getenv("UWB_RING_SG")) sg = atoi(a) == 2 ? 2 : 1;
+    if (ncw == 2) return go<T, 2, 2, BOXC, 1>(L, stream);
+    return sg == 1 ? go<T, 4, 1, BOXC, 1>(L, stream) : go<T, 4, 1, BOXC, 2>(L, stream);
+}
+
 template <typename T>
-cudaError_t go_cfg(const CfarLaunch& L, int ncw, int ahead, size_t smem, cudaStream_t stream) {
-    if (ncw == 4) {
-        switch (ahead) {
-            case 1: return go<T, 4, 1>(L, smem, stream);
-            case 3: return go<T, 4, 3>(L, smem, stream);
-            case 4: return go<T, 4, 4>(L, smem, stream);
-            default: return go<T, 4, 2>(L, smem, stream);
-        }
-    }
-    switch (ahead) {
-        case 1: return go<T, 2, 1>(L, smem, stream);
-        case 3: return go<T, 2, 3>(L, smem, stream);
-        case 4: return go<T, 2, 4>(L, smem, stream);
-        default: return go<T, 2, 2>(L, smem, stream);
+cudaError_t go_cfg(const CfarLaunch& L, int ncw, int boxc, cudaStream_t stream) {
+    switch (boxc) {
+        case 152: return go_ncw<T, 152>(L, ncw, stream);
+        case 160: return go_ncw<T, 160>(L, ncw, stream);
+        case 204: return go_ncw<T, 204>(L, ncw, stream);
+        default: return go_ncw<T, 256>(L, ncw, stream);
     }
 }
 
 } // namespace
 
 // Returns cudaErrorNotSupported when the rings do not fit or the layout does
-// not allow 16-byte bulk copies of the CUT rows (caller falls back).
+// not allow tensor copies (caller falls back to the simple kernel).
 cudaError_t launch_cfar_ring(const CfarLaunch& L, int dtype, cudaStream_t stream) {
     if (getenv("UWB_CFAR_SIMPLE")) return cudaErrorNotSupported;
     if (L.geo.rows >= (int64_t(1) << 31) || L.cols >= (int64_t(1) << 30)) return cudaErrorNotSupported;
     const bool f32 = dtype == UWB_F32;
     const size_t esz = f32 ? 4 : 8;
-    // CUT rows are bulk-copied in 16-byte units: rows must start 16-byte aligned
-    // and the row pitch must keep them so; a partial last strip may read up to
-    // 12 bytes past its last cell, which must stay inside the row pitch.
-    if ((reinterpret_cast<uintptr_t>(L.maps) % 16) || ((L.ld * esz) % 16) || ((L.map_stride * esz) % 16))
+    // tensor maps: 16-byte aligned base and row / map pitches
+    if ((reinterpret_cast<uintptr_t>(L.maps) % 16) || ((L.ld * esz) % 16) ||
+        (L.n_jobs / L.geo.n_slabs > 1 && (L.map_stride * esz) % 16))
         return cudaErrorNotSupported;
-    if (((L.cols * esz) % 16) && L.ld * esz < ((L.cols * esz + 15) / 16) * 16) return cudaErrorNotSupported;
-    int ahead = kDefaultAhead;
-    if (const char* a = getenv("UWB_RING_AHEAD")) ahead = min(4, max(1, atoi(a)));
-    int ncw_pref = 4;
-    if (const char* a = getenv("UWB_RING_NCW")) ncw_pref = atoi(a) == 2 ? 2 : 4;
-    auto bytes = [&](int w) {
-        return f32 ? ring_smem_bytes<float>(w, L.hr, L.hc, ahead) : ring_smem_bytes<double>(w, L.hr, L.hc, ahead);
-    };
-    const size_t s4 = bytes(256), s2 = bytes(128);
-    if (ncw_pref == 4 && s4 <= 113 * 1024 && L.cols > 128)
-        return f32 ? go_cfg<float>(L, 4, ahead, s4, stream) : go_cfg<double>(L, 4, ahead, s4, stream);
-    if (s2 <= 200 * 1024)
-        return f32 ? go_cfg<float>(L, 2, ahead, s2, stream) : go_cfg<double>(L, 2, ahead, s2, stream);
-    return cudaErrorNotSupported;
+    // ring row width: kW + 2 hc + 4 doubles at most (16-byte aligned span)
+    const int need = kW + 2 * L.hc + 4;
+    const int boxc = need <= 152 ? 152 : need <= 160 ? 160 : need <= 204 ? 204 : need <= 256 ? 256 : 0;
+    if (!boxc) return cudaErrorNotSupported;
+    int ncw = 4;
+    if (const char* a = getenv("UWB_RING_NCW")) ncw = atoi(a) == 2 ? 2 : 4;
+    return f32 ? go_cfg<float>(L, ncw, boxc, stream) : go_cfg<double>(L, ncw, boxc, stream);
 }
 
 } // namespace uwb

@@ -116,6 +116,8 @@ struct CfarLaunch {
     unsigned long long* det_counts;
     unsigned long long* first_bad;
     int64_t row_chunks;  // row chunks per job
+    unsigned sleep_ns;   // barrier-wait suspend hint of the CFAR ring kernel (ns)
+    unsigned debug;      // bit 0: consumers skip the cell arithmetic (data-movement probe)
     int64_t col_tiles;
 };
 
