@@ -7,29 +7,35 @@
 // that respects those dependencies and performs the same three IEEE additions
 // reproduces the reference table bit for bit. This kernel runs the recurrence
 // as a systolic wavefront:
-//   * the unit of work is one warp on a 32-column strip of one table; lane l
-//     owns column l of the strip and handles row r = s - l at step s, so the
+//   * the unit of work is one warp on a 64-column strip of one table; lane l
+//     owns columns 2l and 2l+1 and handles row r = s - l at step s, so the
 //     warp sweeps an anti-diagonal band down the whole strip. Warps are
-//     independent (no CTA barrier);
-//   * S(r, left column) comes from lane l-1 by a register shuffle of the value
-//     it produced one step earlier; lane 0 takes it from the table column the
-//     strip to the left has already written, 32 rows at a time (one load per
-//     lane, handed over by shuffle);
-//   * global traffic stays coalesced although every lane works on a different
-//     row: the warp streams its 32 source columns row by row into a shared
-//     ring with cp.async (one 128-byte row segment per step, 8 rows ahead), and
-//     every lane delays its results through a 32-row shared ring so the
-//     completed row s-31 leaves as one 256-byte segment per step;
-//   * strips are claimed from an atomic counter in pair-major order: strips
-//     2p and 2p+1 of a table are claimed back to back (so the two halves of
-//     each 256-byte source segment are read close together and stay in L2),
-//     and every table's pair p precedes any table's pair p+1. The strip a warp
-//     depends on is therefore already running or finished; the dependency is a
-//     release/acquire count of rows the left strip has flushed.
+//     independent (no CTA barrier). Per step a lane does 6 dependent-pair
+//     additions; S(r, 2l-1) comes from lane l-1 by a register shuffle of the
+//     value it produced one step earlier, and lane 0 takes it from the edge
+//     column of the strip to the left, fetched 32 rows at a time;
+//   * lanes form 4 groups of 8. Group g stages, with 8-byte cp.async per lane,
+//     the row its lanes need kAhead..kAhead+7 steps later (one 64-byte
+//     segment per group and step) into lane-private slots of a 32-step ring
+//     (slot = copy step mod 32), so no lane ever reads data another lane
+//     copied; lane 0 also prefetches the strip's row kPrefetch steps ahead
+//     into L2 so the staging copies hit L2. Results go through a
+//     lane-private 8-row delay ring; group g writes back row s - 8g - 7, so each
+//     group stores one whole 128-byte line of the table per step;
+//   * all ring slots used inside the 32-step unrolled block are compile-time
+//     offsets or one ADD/AND away from a per-lane base;
+//   * strips are claimed from an atomic counter in strip-major order, so the
+//     strip a warp depends on was claimed earlier and is running or finished;
+//     the dependency is a release/acquire count of rows the left strip has
+//     handed over through the edge buffer.
 // The table uses the shifted layout of kernels.cuh (padded (i, j) at
-// table[i*ld + kTabShift + j]), which makes every 32-column flush line-aligned.
-// Non-finite inputs are reported as the smallest row-major index (sat.cpp:28-32).
+// table[i*ld + kTabShift + j]), which makes every group's flush line-aligned.
+// Non-finite inputs are reported as the smallest row-major index (sat.cpp:28-32):
+// a non-finite input makes every later S of its column non-finite, so each lane
+// checks its last S once per block and, the first time it is not finite,
+// rescans its own columns for the first offending row.
 #include <climits>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -39,67 +45,87 @@ namespace uwb {
 
 namespace {
 
-constexpr int kStripCols = kWarp;          // 32 columns per unit of work
-constexpr int kWarpsPerCta = 4;            // independent warps per CTA
-constexpr int kAhead = 8;                  // source rows prefetched ahead
-constexpr int kInSlots = kWarp + kAhead;   // source ring depth (rows)
-constexpr int kPublishEvery = 64;
+constexpr int kStripCols = 2 * kWarp;   // 64 columns per unit of work
+constexpr int kWarpsPerCta = 4;         // independent warps per CTA
+constexpr int kAhead = 24;              // staging distance in steps (<= kXSlots - 8)
+constexpr int kXSlots = 32;             // lane-private source ring (copy steps)
+constexpr int kPrefetch = 64;           // L2 prefetch distance (rows)
+constexpr int kOSlots = 8;              // lane-private result delay ring (rows)
+constexpr int kPublishEvery = 64;       // steps between edge hand-overs
 
+// Shared memory per CTA: the warps' source rings, the result rings and the
+// edge staging.
 template <typename T>
-struct WarpSmem {
-    T xin[kInSlots][kWarp];
-    double sout[kWarp][kWarp];
+struct SatSmem {
+    static constexpr unsigned kXSlotBytes = kWarp * 2 * sizeof(T);
+    static constexpr unsigned kXRing = kXSlots * kXSlotBytes;        // 8 KB (f32) / 16 KB (f64)
+    static constexpr unsigned kOSlotBytes = kWarp * 2 * sizeof(double);
+    static constexpr unsigned kORing = kOSlots * kOSlotBytes;        // 4 KB
+    static constexpr size_t bytes() {
+        return 16 /* alignment slack */ + kWarpsPerCta * (kXRing + kORing + kWarp * sizeof(double));
+    }
 };
 
-template <typename T>
-__device__ __forceinline__ void cp_async_cell(unsigned dst, const T* src);
-template <>
-__device__ __forceinline__ void cp_async_cell<float>(unsigned dst, const float* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
-}
-template <>
-__device__ __forceinline__ void cp_async_cell<double>(unsigned dst, const double* src) {
+__device__ __forceinline__ void cp_async_pair(unsigned dst, const float* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
 }
-template <typename T>
-__device__ __forceinline__ double lds_x(unsigned addr);
-template <>
-__device__ __forceinline__ double lds_x<float>(unsigned addr) {
-    float v;
-    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
-    return static_cast<double>(v);
+__device__ __forceinline__ void cp_async_pair(unsigned dst, const double* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
-template <>
-__device__ __forceinline__ double lds_x<double>(unsigned addr) {
-    double v;
-    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
-    return v;
+__device__ __forceinline__ void cp_async_one(unsigned dst, const float* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
 }
-__device__ __forceinline__ void sts_f64(unsigned addr, double v) {
-    asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+__device__ __forceinline__ void cp_async_one(unsigned dst, const double* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
 }
-__device__ __forceinline__ double lds_f64(unsigned addr) {
+__device__ __forceinline__ void lds_pair(unsigned addr, float& a, float& b) {
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(a), "=f"(b) : "r"(addr));
+}
+__device__ __forceinline__ void lds_pair(unsigned addr, double& a, double& b) {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "r"(addr));
+}
+__device__ __forceinline__ void sts_pair(unsigned addr, double a, double b) {
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(a), "d"(b) : "memory");
+}
+__device__ __forceinline__ void lds_dpair(unsigned addr, double& a, double& b) {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "r"(addr) : "memory");
+}
+__device__ __forceinline__ double lds_d(unsigned addr) {
     double v;
     asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
     return v;
 }
 
-// Lane 31 (which flushed the strip's last column) releases the flushed-row count.
-__device__ __noinline__ void publish_rows(unsigned* prog, int flushed, int lane) {
-    if (lane == kWarp - 1 && flushed > 0) st_release_u32(prog, static_cast<unsigned>(flushed));
+// Lane 31 (which produced the strip's edge column) releases the row count.
+__device__ __noinline__ void publish_rows(unsigned* prog, int rows_done, int lane) {
+    if (lane == kWarp - 1 && rows_done > 0) st_release_u32(prog, static_cast<unsigned>(rows_done));
     __syncwarp();
+}
+
+// First non-finite row of columns [c, c + n) in source rows [0, rows_end).
+template <typename T>
+__device__ __noinline__ int first_nonfinite_row(const T* src, int64_t ld, int c, int n, int rows_end) {
+    for (int r = 0; r < rows_end; ++r)
+        for (int k = 0; k < n; ++k)
+            if (!isfinite(widen(src[static_cast<int64_t>(r) * ld + c + k]))) return r;
+    return INT_MAX;
 }
 
 template <typename T>
 __global__ void __launch_bounds__(kWarpsPerCta * kWarp)
 sat_systolic_kernel(SatLaunch L) {
     extern __shared__ __align__(16) unsigned char sat_smem_raw[];
+    using SM = SatSmem<T>;
+    constexpr unsigned kXSlotBytes = SM::kXSlotBytes;
+    constexpr unsigned kOSlotBytes = SM::kOSlotBytes;
     const int warp = threadIdx.x / kWarp;
     const int lane = threadIdx.x % kWarp;
-    WarpSmem<T>& sm = reinterpret_cast<WarpSmem<T>*>(sat_smem_raw)[warp];
-    const unsigned xin_base = smem_u32(&sm.xin[0][lane]);
-    const unsigned xin_end = xin_base + kInSlots * kWarp * sizeof(T);
-    const unsigned sout_base = smem_u32(&sm.sout[0][lane]);
+    const int grp = lane >> 3; // lane group: stages and flushes together
+    const unsigned raw = smem_u32(sat_smem_raw);
+    const unsigned base = (raw + 15u) & ~15u;
+    const unsigned x_lane = base + warp * SM::kXRing + lane * 2 * sizeof(T); // slot 0, my pair
+    const unsigned o_lane = base + kWarpsPerCta * SM::kXRing + warp * SM::kORing + lane * 2 * sizeof(double);
+    const unsigned edge_smem = base + kWarpsPerCta * (SM::kXRing + SM::kORing) + warp * kWarp * sizeof(double);
     const int64_t n_tiles = L.n_jobs * L.strips;
     const int cols = static_cast<int>(L.cols);
 
@@ -109,26 +135,20 @@ sat_systolic_kernel(SatLaunch L) {
         tile = __shfl_sync(0xffffffffu, tile, 0);
         if (tile >= n_tiles) return;
 
-        // pair-major claim order: (pair, job, half)
-        const int64_t pair = tile / (2 * L.n_jobs);
-        const int64_t rem = tile % (2 * L.n_jobs);
-        int64_t job;
-        int strip;
-        if (2 * pair + 1 < L.strips) {
-            job = rem / 2;
-            strip = static_cast<int>(2 * pair + (rem & 1));
-        } else { // odd strip count: the last layer holds single strips
-            job = rem;
-            strip = static_cast<int>(2 * pair);
-        }
+        // strip-major claim order: every job's strip k precedes any job's strip k+1
+        const int strip = static_cast<int>(tile / L.n_jobs);
+        const int64_t job = tile % L.n_jobs;
         const SatJobView J = sat_job(L, job);
         const int rows = static_cast<int>(J.rows);
-        const int c = strip * kStripCols + lane;
-        const bool live = c < cols;
+        const int c = strip * kStripCols + 2 * lane;     // my first column
+        const int nvalid = max(0, min(2, cols - c));     // my columns inside the map
         double* table = J.table;
         const int64_t tld = L.table_ld;
+        const int64_t ld = L.ld;
+        const T* src = static_cast<const T*>(J.src);
 
-        if (live) table[kTabShift + 1 + c] = 0.0; // padded row 0 is identically zero
+        if (nvalid > 0) table[kTabShift + 1 + c] = 0.0; // padded row 0 is identically zero
+        if (nvalid > 1) table[kTabShift + 2 + c] = 0.0;
         if (strip == 0 && lane == 0) table[kTabShift] = 0.0;
 
         const unsigned* prog_in = strip > 0 ? L.gprog + job * L.strips + strip - 1 : nullptr;
@@ -138,120 +158,178 @@ sat_systolic_kernel(SatLaunch L) {
         const double* ge_in = prog_in ? L.gedge + (job * L.strips + strip - 1) * L.edge_stride : nullptr;
         double* ge_out = prog_out ? L.gedge + (job * L.strips + strip) * L.edge_stride : nullptr;
         unsigned avail = 0;
-        // left values for rows [blk, blk+32) live in lane k's register (row blk + k)
-        auto fetch_left = [&](int base) -> double {
-            if (!prog_in || base >= rows) return 0.0; // warp-uniform
-            const unsigned need = static_cast<unsigned>(min(rows, base + kWarp));
-            if (avail < need) { // lane 0 acquires; the warp barrier extends the ordering to all lanes
-                if (lane == 0)
-                    while (avail < need) avail = ld_acquire_u32(prog_in);
-                avail = __shfl_sync(0xffffffffu, avail, 0);
+        // left-strip edge for rows [base, base+32) -> edge_smem (lane k: row base + k)
+        auto fetch_left = [&](int base) {
+            double v = 0.0;
+            if (prog_in && base < rows) { // warp-uniform
+                const unsigned need = static_cast<unsigned>(min(rows, base + kWarp));
+                if (avail < need) { // lane 0 acquires; the warp barrier extends the ordering
+                    if (lane == 0)
+                        while (avail < need) avail = ld_acquire_u32(prog_in);
+                    avail = __shfl_sync(0xffffffffu, avail, 0);
+                }
+                if (base + lane < rows) v = ge_in[base + lane];
             }
-            const int rr = base + lane;
-            return rr < rows ? ge_in[rr] : 0.0;
+            return v;
         };
-        double lcur = fetch_left(0);
-        double lnext = fetch_left(kWarp);
 
-        const int64_t ld = L.ld;
-        const T* xsrc = static_cast<const T*>(J.src) + c; // row 0 of my column
-        // full strips with 16-byte aligned rows stage each row segment with
-        // 16-byte copies by the first 32*sizeof(T)/16 lanes
-        constexpr int kVecLanes = kWarp * static_cast<int>(sizeof(T)) / 16;
-        constexpr int kElemsPerVec = 16 / static_cast<int>(sizeof(T));
-        const bool vec = (strip + 1) * kStripCols <= cols && (ld * sizeof(T)) % 16 == 0 &&
-                         (reinterpret_cast<uintptr_t>(J.src) % 16) == 0;
-        const bool vec_lane = lane < kVecLanes;
-        const unsigned vdst_off = (16u - static_cast<unsigned>(sizeof(T))) * static_cast<unsigned>(lane);
-        const int vsrc_off = lane * (kElemsPerVec - 1);
-        auto stage = [&](unsigned dst, const T* src) { // source row segment -> ring slot
-            if (vec) {
-                if (vec_lane) cp_async_16(dst + vdst_off, src + vsrc_off);
-            } else if (live) {
-                cp_async_cell<T>(dst, src);
+        // L2 prefetch of the strip's row segment, kPrefetch rows ahead (lane 0)
+        const unsigned pf_bytes = static_cast<unsigned>(min(kStripCols, cols - strip * kStripCols)) * sizeof(T);
+        const unsigned pf_bytes16 = (pf_bytes + 15u) & ~15u;
+        const T* pfrow = src + strip * kStripCols + static_cast<int64_t>(kPrefetch) * ld;
+        const bool pf_aligned = !(L.flags & 1u) && (reinterpret_cast<uintptr_t>(src) % 16) == 0 && (ld * sizeof(T)) % 16 == 0;
+        if (lane == 0 && pf_aligned)
+            for (int r = 0; r < min(rows, kPrefetch); ++r)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + strip * kStripCols +
+                                                                                   static_cast<int64_t>(r) * ld),
+                             "r"(pf_bytes16)
+                             : "memory");
+        // staging: group g copies, at step s, source row s + kAhead - 8g
+        const bool pair_ok = nvalid == 2 && (reinterpret_cast<uintptr_t>(src) % (2 * sizeof(T))) == 0 &&
+                             (ld % 2) == 0;
+        const bool warp_fast = __all_sync(0xffffffffu, pair_ok);
+        const T* xrow = src + c + static_cast<int64_t>(kAhead - 8 * grp) * ld; // row staged at step 0
+        // a copy issued at step s lands in slot s mod 32
+        auto stage = [&](unsigned slot_off, int row, const T* p, bool checked) {
+            const unsigned dst = x_lane + slot_off;
+            if (!checked) {
+                cp_async_pair(dst, p);
+            } else if (row >= 0 && row < rows) {
+                if (warp_fast) {
+                    cp_async_pair(dst, p);
+                } else {
+                    if (nvalid > 0) cp_async_one(dst, p);
+                    if (nvalid > 1) cp_async_one(dst + sizeof(T), p + 1);
+                }
             }
         };
+        // prologue: virtual steps -kAhead..-1 stage rows -8g .. kAhead-1-8g
 #pragma unroll
-        for (int u = 0; u < kAhead; ++u) {
-            if (u < rows) stage(xin_base + u * kWarp * sizeof(T), xsrc + u * ld);
+        for (int v = -kAhead; v < 0; ++v) {
+            const int row = v + kAhead - 8 * grp;
+            stage(static_cast<unsigned>(((v + kXSlots) & (kXSlots - 1)) * kXSlotBytes), row,
+                  xrow + static_cast<int64_t>(v) * ld, true);
             cp_async_commit();
         }
-        const T* xnext = xsrc + kAhead * ld;                                // row s + kAhead
-        unsigned xin_next = xin_base + kAhead * kWarp * sizeof(T);          // its ring slot
-        unsigned xin_cur = xin_base + ((kInSlots - lane) % kInSlots) * kWarp * sizeof(T); // slot of row s - lane
-        double* tflush = table + tld + kTabShift + 1 + c;                   // table row rf + 1, rf = s - 31
-        double* zflush = table + tld + kTabShift;                           // padded column 0
 
-        double prev = 0.0;      // S(r-1, c)
-        double left_prev = 0.0; // S(r-1, c-1)
-        double my_last = 0.0;   // S(r, c), shuffled right next step
-        int first_bad = INT_MAX; // first row of my column holding a non-finite value
-        const bool corner = strip == 0 && lane == 0;
+        double prev0 = 0.0, prev1 = 0.0; // S(r-1, c), S(r-1, c+1)
+        double left_prev = 0.0;          // S(r-1, c-1)
+        double last1 = 0.0;              // S(r, c+1), shuffled right next step
+        double last0 = 0.0;
+        bool scanned = false;            // non-finite rescan done
+        // flush pointer: table row rf + 1 for rf = s - 8g - 8 (my pair)
+        double* tflush = table + static_cast<int64_t>(1 - 8 * grp - 8) * tld + kTabShift + 1 + c;
         const int steps = rows + kWarp;
+        // lane l needs at step s the row copied at step s - kAhead - (l mod 8)
+        const unsigned x_rbase_lane = static_cast<unsigned>(2 * kXSlots - kAhead - (lane & 7));
+        const unsigned o_rbase_lane = static_cast<unsigned>(kWarp - lane); // (u - l) mod 8
+        const bool pf_ok_lane = lane == 0 && pf_aligned;
+        const bool edge_lane = lane == kWarp - 1 && ge_out != nullptr;
+        auto load_x = [&](unsigned u, T& a, T& b) {
+            lds_pair(x_lane + ((u + x_rbase_lane) & (kXSlots - 1)) * kXSlotBytes, a, b);
+        };
+        T x0n, x1n; // source pair of the next step (loaded one step ahead)
+        double edge_n = 0.0; // lane 0: left strip's edge for the next step
 
-        // One systolic step. kSteady: every lane's row and the flushed row are
-        // inside the table and the prefetched row exists (no range checks).
-        auto step = [&](const int s, const int u, auto steady_tag) {
-            constexpr bool kSteady = decltype(steady_tag)::value;
+        // One systolic step. kChecked: range checks on rows (prologue/epilogue blocks).
+        auto step = [&](const int s0, const int u, auto checked_tag) {
+            constexpr bool kChecked = decltype(checked_tag)::value;
+            const int s = s0 + u;
             const int r = s - lane;
-            // stream in source row s + kAhead
-            if (kSteady || s + kAhead < rows) stage(xin_next, xnext);
+            // (1) group g writes back row s - 8g - 8 (slot u mod 8, stored >= 1 step ago)
+            const int rf = s - 8 * grp - 8;
+            if (!kChecked || (rf >= 0 && rf < rows)) {
+                double a, b;
+                lds_dpair(o_lane + static_cast<unsigned>(u & (kOSlots - 1)) * kOSlotBytes, a, b);
+                if (!kChecked || nvalid == 2) {
+                    *reinterpret_cast<double2*>(tflush) = make_double2(a, b);
+                } else if (nvalid == 1) {
+                    *tflush = a;
+                }
+            }
+            tflush += tld;
+            // (2) stage source row s + kAhead - 8g into slot u (s0 is a multiple of 32)
+            stage(static_cast<unsigned>(u * kXSlotBytes), s + kAhead - 8 * grp, xrow, kChecked);
             cp_async_commit();
-            xnext += ld;
-            xin_next += kWarp * sizeof(T);
-            if (xin_next == xin_end) xin_next = xin_base;
-            cp_async_wait<kAhead>();
-            __syncwarp(); // rows staged by other lanes' 16-byte copies
-            const double from_left_strip = __shfl_sync(0xffffffffu, lcur, u);
-            double left = __shfl_up_sync(0xffffffffu, my_last, 1);
+            xrow += ld;
+            if (pf_ok_lane && (!kChecked || s + kPrefetch < rows))
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pfrow), "r"(pf_bytes16) : "memory");
+            pfrow += ld;
+            // (3) this step's inputs were loaded one step ahead; load the next step's
+            const T x0 = x0n, x1 = x1n;
+            const double from_left_strip = edge_n;
+            cp_async_wait<kAhead - 1>();
+            load_x(static_cast<unsigned>(u + 1), x0n, x1n);
+            if (u + 1 < kWarp) edge_n = lds_d(edge_smem + static_cast<unsigned>(u + 1) * 8u);
+            // (4) left neighbour S(r, c-1): lane l-1's newest S(., c+1); lane 0: left strip's edge
+            double left = __shfl_up_sync(0xffffffffu, last1, 1);
             if (lane == 0) left = from_left_strip;
-            const double v = lds_x<T>(xin_cur);
-            // sat.cpp:33: out[c+1] = v + above[c+1] + out[c] - above[c]
-            const double sv = dsub(dadd(dadd(v, prev), left), left_prev);
-            const bool act = kSteady ? live : (live && r >= 0 && r < rows);
+            // (5) sat.cpp:33, twice: out[c+1] = v + above[c+1] + out[c] - above[c]
+            const double v0 = widen(x0), v1 = widen(x1);
+            const double s0v = dsub(dadd(dadd(v0, prev0), left), left_prev);
+            const double s1v = dsub(dadd(dadd(v1, prev1), s0v), prev0);
+            const bool act = !kChecked || (r >= 0 && r < rows);
             if (act) {
-                first_bad = (!isfinite(v) && r < first_bad) ? r : first_bad;
-                prev = sv;
+                // (6) edge column for the strip to the right (two rows per 16-byte store)
+                if (edge_lane) {
+                    if (kChecked) {
+                        ge_out[r] = s1v;
+                        if (u == 0 && r >= 1) ge_out[r - 1] = prev1; // row a fast block left unstored
+                    }
+                    else if ((u & 1) == 0) // r = s - 31 is odd
+                        *reinterpret_cast<double2*>(ge_out + r - 1) = make_double2(prev1, s1v);
+                }
                 left_prev = left;
-                my_last = sv;
-                sts_f64(sout_base + static_cast<unsigned>(r & (kWarp - 1)) * kWarp * 8u, sv);
-                if (lane == kWarp - 1 && ge_out) ge_out[r] = sv;
-            }
-            xin_cur += kWarp * sizeof(T);
-            if (xin_cur == xin_end) xin_cur = xin_base;
-            // flush the completed row rf = s - 31 (own column; the warp stores one segment)
-            const int rf = s - (kWarp - 1);
-            if (kSteady || (rf >= 0 && rf < rows)) {
-                if (live) *tflush = lds_f64(sout_base + static_cast<unsigned>(rf & (kWarp - 1)) * kWarp * 8u);
-                if (corner) *zflush = 0.0;
-            }
-            if (kSteady || rf >= 0) {
-                tflush += tld;
-                zflush += tld;
+                prev0 = s0v;
+                prev1 = s1v;
+                last0 = s0v;
+                last1 = s1v;
+                sts_pair(o_lane + ((static_cast<unsigned>(u) + o_rbase_lane) & (kOSlots - 1)) * kOSlotBytes, s0v,
+                         s1v);
             }
         };
 
+        // left-strip edge values, one block ahead (lane k: row s0 + k)
+        double e_cur = fetch_left(0);
+        double e_next = fetch_left(kWarp);
+        cp_async_wait<kAhead - 1>();
+        load_x(0u, x0n, x1n);
         for (int s0 = 0; s0 < steps; s0 += kWarp) {
-            if (s0 > 0) { // left-strip values for rows [s0, s0 + 32) come from the previous fetch
-                lcur = lnext;
-                lnext = fetch_left(s0 + kWarp);
-            }
-            if (s0 >= kWarp && s0 + kWarp + kAhead <= rows) {
+            // left-strip edge values for rows [s0, s0 + 32) (lane 0 reads row s at step s)
+            __syncwarp();
+            asm volatile("st.shared.f64 [%0], %1;" ::"r"(edge_smem + 8u * lane), "d"(e_cur) : "memory");
+            __syncwarp();
+            edge_n = lds_d(edge_smem);
+            e_cur = e_next;
+            e_next = fetch_left(s0 + 2 * kWarp);
+            // padded column 0 of the rows group 0 writes back in this block
+            if (strip == 0 && s0 - 8 + lane >= 0 && s0 - 8 + lane < rows)
+                table[static_cast<int64_t>(s0 - 8 + lane + 1) * tld + kTabShift] = 0.0;
+            const bool fast = s0 >= kWarp && s0 + kWarp + kAhead <= rows && warp_fast;
+            if (fast) {
 #pragma unroll
-                for (int u = 0; u < kWarp; ++u) step(s0 + u, u, std::true_type{});
+                for (int u = 0; u < kWarp; ++u) step(s0, u, std::false_type{});
             } else {
 #pragma unroll 1
-                for (int u = 0; u < kWarp && s0 + u < steps; ++u) step(s0 + u, u, std::false_type{});
+                for (int u = 0; u < kWarp && s0 + u < steps; ++u) step(s0, u, std::true_type{});
             }
-            // publish the flushed row count for the strip to the right (warp-uniform)
+            // non-finite inputs poison every later S of their column (see header)
+            if (!scanned && nvalid > 0 && !(isfinite(last0) && (nvalid < 2 || isfinite(last1)))) {
+                scanned = true;
+                const int row_end = min(rows, s0 + kWarp);
+                const int bad = first_nonfinite_row<T>(src, ld, c, nvalid, row_end);
+                if (bad != INT_MAX) {
+                    const int k = isfinite(widen(src[static_cast<int64_t>(bad) * ld + c])) ? 1 : 0;
+                    report_min(J.nonfinite, static_cast<unsigned long long>((J.row0 + bad) * L.cols + c + k));
+                }
+            }
+            // hand over the edge rows stored so far (warp-uniform); a fast block
+            // leaves its last row for the next block's paired store
             const int s_end = min(s0 + kWarp, steps);
-            if ((s_end & (kPublishEvery - 1)) == 0 || s_end == steps) {
-                if (prog_out) publish_rows(prog_out, min(rows, s_end - (kWarp - 1)), lane);
-            }
+            if (prog_out && ((s_end & (kPublishEvery - 1)) == 0 || s_end == steps))
+                publish_rows(prog_out, min(rows, s_end - (kWarp - 1) - (fast ? 1 : 0)), lane);
         }
         cp_async_wait<0>();
-        if (first_bad != INT_MAX)
-            report_min(J.nonfinite, static_cast<unsigned long long>((J.row0 + first_bad) * L.cols + c));
         __syncwarp();
     }
 }
@@ -263,7 +341,7 @@ std::atomic<uint64_t> g_kernel_launches{0};
 template <typename T>
 static cudaError_t launch_sat_t(const SatLaunch& L, cudaStream_t stream) {
     const int64_t n_tiles = L.n_jobs * L.strips;
-    const size_t smem = sizeof(WarpSmem<T>) * kWarpsPerCta;
+    const size_t smem = SatSmem<T>::bytes();
     cudaError_t e = cudaFuncSetAttribute(sat_systolic_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
@@ -273,8 +351,10 @@ static cudaError_t launch_sat_t(const SatLaunch& L, cudaStream_t stream) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sat_systolic_kernel<T>, kWarpsPerCta * kWarp, smem);
     const int64_t ctas = (n_tiles + kWarpsPerCta - 1) / kWarpsPerCta;
     const int64_t grid = imin(ctas, static_cast<int64_t>(sms) * (per_sm > 0 ? per_sm : 1));
+    SatLaunch L2 = L;
+    if (const char* f = getenv("UWB_SAT_FLAGS")) L2.flags = static_cast<unsigned>(atoi(f));
     ++g_kernel_launches;
-    sat_systolic_kernel<T><<<static_cast<unsigned>(grid), kWarpsPerCta * kWarp, smem, stream>>>(L);
+    sat_systolic_kernel<T><<<static_cast<unsigned>(grid), kWarpsPerCta * kWarp, smem, stream>>>(L2);
     return cudaGetLastError();
 }
 

@@ -1,4 +1,4 @@
-# Sweep CFAR ring knobs (env read by launch_cfar_ring) on a reduced batch;
+# Sweep tuning knobs (env read by the launchers) on a reduced batch;
 # prints one line per setting: Gcell/s, ms/step, phase ms.
 MAPS=${MAPS:-1024}
 run() {
@@ -6,6 +6,5 @@ run() {
   env "$@" timeout -s KILL 300 python bench.py --maps $MAPS --steps 5 --warmup 3 --no-e2e --no-cpu-baseline 2>&1 | tail -1 | \
     python -c "import sys,json; d=json.loads(sys.stdin.read()); print(round(d['value'],2), round(d['ms_per_step'],3), {k: round(v,3) for k,v in d['phases_ms'].items()})" 2>&1 | tail -1
 }
-run UWB_RING_SG=1
-run UWB_RING_SG=2
-run UWB_RING_SG=2 UWB_RING_DEBUG=1
+run UWB_SAT_FLAGS=0
+run UWB_SAT_FLAGS=1
