@@ -256,8 +256,8 @@ def run_b200(args):
         if world > 1:
             dist.barrier()
 
-    for _ in range(max(args.warmup, 0)):
-        step()
+    for i in range(max(args.warmup, 0)):
+        step(phase=(i == args.warmup - 1))  # the last warm-up also creates the phase events
     torch.cuda.synchronize()
     runner.check_inputs()
     phase_ms(4096)  # clear the ring

@@ -220,7 +220,7 @@ uwb_status uwb_host_cfar2d_batch(const uwb_map_batch* host_batch, const uwb_cfar
 
 /* Instrumentation. uwb_kernel_launches: number of kernels this library has
  * launched in the process. With flags bit 1 set, uwb_dev_cfar2d records CUDA
- * events around its phases (SAT, CFAR, sort) into a 4096-slot ring without
+ * events around its phases (SAT, CFAR, sort) into a 1024-slot ring without
  * synchronising; uwb_dev_phase_ms synchronises on them, writes up to max_calls
  * triples {sat_ms, cfar_ms, sort_ms} and clears the ring. Returns the count. */
 uint64_t uwb_kernel_launches(void);

@@ -261,7 +261,7 @@ uwb_status check_batch(const uwb_map_batch* b) {
 
 // Phase-event ring (flags bit 1 of uwb_dev_cfar2d).
 struct PhaseRing {
-    static constexpr int kSlots = 4096;
+    static constexpr int kSlots = 1024;
     std::mutex mu;
     std::vector<cudaEvent_t> ev; // 4 per slot
     int used = 0;

@@ -16,10 +16,10 @@
 //     column of the strip to the left, fetched 32 rows at a time;
 //   * lanes form 4 groups of 8. Group g stages, with 8-byte cp.async per lane,
 //     the row its lanes need kAhead..kAhead+7 steps later (one 64-byte
-//     segment per group and step) into lane-private slots of a 32-step ring
-//     (slot = copy step mod 32), so no lane ever reads data another lane
-//     copied; lane 0 also prefetches the strip's row kPrefetch steps ahead
-//     into L2 so the staging copies hit L2. Results go through a
+//     segment per group and step) into lane-private slots of a 16-step ring
+//     (slot = copy step mod 16), so no lane ever reads data another lane
+//     copied (optionally, flags bit 0, lane 0 also prefetches the strip's row
+//     kPrefetch steps ahead into L2; measured slower on B200). Results go through a
 //     lane-private 8-row delay ring; group g writes back row s - 8g - 7, so each
 //     group stores one whole 128-byte line of the table per step;
 //   * all ring slots used inside the 32-step unrolled block are compile-time
@@ -47,11 +47,12 @@ namespace {
 
 constexpr int kStripCols = 2 * kWarp;   // 64 columns per unit of work
 constexpr int kWarpsPerCta = 4;         // independent warps per CTA
-constexpr int kAhead = 24;              // staging distance in steps (<= kXSlots - 8)
-constexpr int kXSlots = 32;             // lane-private source ring (copy steps)
+constexpr int kAhead = 8;               // staging distance in steps (<= kXSlots - 8)
+constexpr int kXSlots = 16;             // lane-private source ring (copy steps)
 constexpr int kPrefetch = 64;           // L2 prefetch distance (rows)
 constexpr int kOSlots = 8;              // lane-private result delay ring (rows)
 constexpr int kPublishEvery = 64;       // steps between edge hand-overs
+constexpr int kSatCtasPerSm = 4;        // occupancy target (registers: 128 per thread)
 
 // Shared memory per CTA: the warps' source rings, the result rings and the
 // edge staging.
@@ -112,7 +113,7 @@ __device__ __noinline__ int first_nonfinite_row(const T* src, int64_t ld, int c,
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kWarpsPerCta * kWarp)
+__global__ void __launch_bounds__(kWarpsPerCta * kWarp, kSatCtasPerSm)
 sat_systolic_kernel(SatLaunch L) {
     extern __shared__ __align__(16) unsigned char sat_smem_raw[];
     using SM = SatSmem<T>;
@@ -177,7 +178,7 @@ sat_systolic_kernel(SatLaunch L) {
         const unsigned pf_bytes = static_cast<unsigned>(min(kStripCols, cols - strip * kStripCols)) * sizeof(T);
         const unsigned pf_bytes16 = (pf_bytes + 15u) & ~15u;
         const T* pfrow = src + strip * kStripCols + static_cast<int64_t>(kPrefetch) * ld;
-        const bool pf_aligned = !(L.flags & 1u) && (reinterpret_cast<uintptr_t>(src) % 16) == 0 && (ld * sizeof(T)) % 16 == 0;
+        const bool pf_aligned = (L.flags & 1u) && (reinterpret_cast<uintptr_t>(src) % 16) == 0 && (ld * sizeof(T)) % 16 == 0;
         if (lane == 0 && pf_aligned)
             for (int r = 0; r < min(rows, kPrefetch); ++r)
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + strip * kStripCols +
@@ -249,7 +250,7 @@ sat_systolic_kernel(SatLaunch L) {
             }
             tflush += tld;
             // (2) stage source row s + kAhead - 8g into slot u (s0 is a multiple of 32)
-            stage(static_cast<unsigned>(u * kXSlotBytes), s + kAhead - 8 * grp, xrow, kChecked);
+            stage(static_cast<unsigned>((u & (kXSlots - 1)) * kXSlotBytes), s + kAhead - 8 * grp, xrow, kChecked);
             cp_async_commit();
             xrow += ld;
             if (pf_ok_lane && (!kChecked || s + kPrefetch < rows))
@@ -307,7 +308,7 @@ sat_systolic_kernel(SatLaunch L) {
                 table[static_cast<int64_t>(s0 - 8 + lane + 1) * tld + kTabShift] = 0.0;
             const bool fast = s0 >= kWarp && s0 + kWarp + kAhead <= rows && warp_fast;
             if (fast) {
-#pragma unroll
+#pragma unroll 16
                 for (int u = 0; u < kWarp; ++u) step(s0, u, std::false_type{});
             } else {
 #pragma unroll 1

@@ -7,4 +7,3 @@ run() {
     python -c "import sys,json; d=json.loads(sys.stdin.read()); print(round(d['value'],2), round(d['ms_per_step'],3), {k: round(v,3) for k,v in d['phases_ms'].items()})" 2>&1 | tail -1
 }
 run UWB_SAT_FLAGS=0
-run UWB_SAT_FLAGS=1
