@@ -10,8 +10,8 @@
 // columns of one job's table), and the CUT rows into a second ring (one box = 4
 // map rows x 128 columns); each box completes on one "full" mbarrier. Ring
 // slots are handed back through "empty" mbarriers, so producer and consumers
-// never meet at a CTA barrier, and the producer checks both rings without
-// blocking so neither stream waits for the other. Both streams are also
+// never meet at a CTA barrier; the producer always issues the load the
+// consumers will read first and sleeps only on that load's slot. Both streams are also
 // prefetched into L2 kPfGroups boxes ahead. The consumer warps evaluate 4 output
 // rows per step; the eight taps of a cell are shared-memory reads
 //     RS = (t[r0][c0] + t[r1+1][c1+1]) - (t[r0][c1+1] + t[r1+1][c0])   (sat.hpp:32-33)
@@ -68,19 +68,6 @@ inline size_t ring_smem_bytes(int hr, int boxc, int sg) {
            sizeof(T) * static_cast<size_t>(kCutGroups) * kG * kW + 2 * sizeof(uint64_t) * (g.ng + kCutGroups);
 }
 
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
-    unsigned ok;
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        "selp.u32 %0, 1, 0, p;\n"
-        "}\n"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
 // Blocking wait that suspends the thread in the barrier unit (up to hint_ns per
 // try) instead of spinning through issue slots the other warps need.
 __device__ __forceinline__ void mbar_wait_susp(uint64_t* bar, unsigned parity, unsigned hint_ns) {
@@ -93,20 +80,6 @@ __device__ __forceinline__ void mbar_wait_susp(uint64_t* bar, unsigned parity, u
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity), "r"(hint_ns)
         : "memory");
-}
-// One suspended try (returns whether the phase completed).
-__device__ __forceinline__ bool mbar_try_susp(uint64_t* bar, unsigned parity, unsigned hint_ns) {
-    unsigned ok;
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
-        "selp.u32 %0, 1, 0, p;\n"
-        "}\n"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity), "r"(hint_ns)
-        : "memory");
-    return ok != 0;
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -293,9 +266,14 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
             tma_prefetch3(&tmap_cut, c0, ra + g * kG, static_cast<int>(map));
         int grp = 0, gslot = 0, gphase = 0;   // next table group, its slot and empty-phase
         int cstep = 0, cslot = 0, cphase = 0; // next CUT group
+        // Issue order: always the load the consumers need first; block (suspended)
+        // only on that load's ring slot. Table group grp is first read at step
+        // (i_lo + 4 grp - ra - hr - 1) / RS, CUT group cstep at step cstep / SG.
         while (grp <= last_grp || cstep < n_cg) {
-            bool progress = false;
-            if (grp <= last_grp && (grp < G.ng || mbar_test(&empty_t[gslot], static_cast<unsigned>(gphase ^ 1)))) {
+            const int need_tab = grp <= last_grp ? max(0, (i_lo + kG * grp - ra - hr - 1)) / RS : INT_MAX;
+            const int need_cut = cstep < n_cg ? cstep / SG : INT_MAX;
+            if (need_tab <= need_cut) {
+                if (grp >= G.ng) mbar_wait_susp(&empty_t[gslot], static_cast<unsigned>(gphase ^ 1), L.sleep_ns);
                 const int first = i_lo + grp * kG;
                 // the first SG groups are mirrored after the last slot, so RS
                 // consecutive ring rows are always contiguous in memory
@@ -309,10 +287,8 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
                     tma_prefetch3(&tmap_tab, e_lo, first + kPfGroups * kG - trow0, static_cast<int>(job));
                 if (++gslot == G.ng) { gslot = 0; gphase ^= 1; }
                 ++grp;
-                progress = true;
-            }
-            if (cstep < n_cg &&
-                (cstep < kCutGroups || mbar_test(&empty_c[cslot], static_cast<unsigned>(cphase ^ 1)))) {
+            } else {
+                if (cstep >= kCutGroups) mbar_wait_susp(&empty_c[cslot], static_cast<unsigned>(cphase ^ 1), L.sleep_ns);
                 const int first = ra + cstep * kG;
                 mbar_expect_tx(&full_c[cslot], kCutBox);
                 tma_box3(cuts + static_cast<size_t>(cslot) * kG * kW, &tmap_cut, c0, first, static_cast<int>(map),
@@ -321,18 +297,6 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
                     tma_prefetch3(&tmap_cut, c0, first + kPfGroups * kG, static_cast<int>(map));
                 if (++cslot == kCutGroups) { cslot = 0; cphase ^= 1; }
                 ++cstep;
-                progress = true;
-            }
-            if (!progress) {
-                // both rings full: sleep on the slot the consumers free first
-                // (CUT slot of cstep frees after step cstep - kCutGroups; table
-                // group grp's slot after the step whose window leaves group grp - ng)
-                const int s_cut = cstep < n_cg ? (cstep - kCutGroups) / SG : INT_MAX;
-                const int s_tab = grp <= last_grp ? ((grp - G.ng + 1) + (hr + i_lo - ra) / kG) / SG : INT_MAX;
-                if (s_tab <= s_cut)
-                    mbar_try_susp(&empty_t[gslot], static_cast<unsigned>(gphase ^ 1), L.sleep_ns);
-                else
-                    mbar_try_susp(&empty_c[cslot], static_cast<unsigned>(cphase ^ 1), L.sleep_ns);
             }
         }
         return;
