@@ -260,7 +260,7 @@ def run_b200(args):
         step(phase=(i == args.warmup - 1))  # the last warm-up also creates the phase events
     torch.cuda.synchronize()
     runner.check_inputs()
-    phase_ms(4096)  # clear the ring
+    phase_ms(1024)  # clear the ring
 
     sampler = ClockSampler(dev.index)
     sampler.start()
@@ -287,7 +287,7 @@ def run_b200(args):
     cells_total = N_MAPS * ROWS * COLS
     value = cells_total / (ms_per_step / 1e3) / 1e9
 
-    ph = phase_ms(4096)
+    ph = phase_ms(1024)
     sat_ms, cfar_ms, sort_ms = (float(np.mean(ph[:, i])) for i in range(3)) if len(ph) else (0.0, 0.0, 0.0)
     peak, peak_src = _peaks()
     cells_local = n_local * ROWS * COLS

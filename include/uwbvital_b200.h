@@ -200,6 +200,29 @@ uwb_status uwb_dev_cfar2d(const uwb_map_batch* batch, const uwb_cfar_params* par
                           const uwb_cfar_outputs* out, void* workspace, uint64_t workspace_bytes,
                           uint32_t flags, void* stream);
 
+/* Row window of larger maps (one rank's share of a map sharded by rows,
+ * SURVEY 8e / BASELINE config 4): the batch buffer holds global rows
+ * [buf_row0, buf_row0 + batch->rows) of maps that have global_rows rows, and
+ * the call owns rows [row_begin, row_end). The buffer must hold the owned rows
+ * plus g_r + b_r halo rows on each side (clipped to the map). Tables are
+ * slab-local (UWB_SAT_SLAB semantics, slab_rows 0 = one slab for the window),
+ * windows clamp with the global row count, detections carry global rows, and
+ * mask rows / per-cell outputs are indexed by row - row_begin. */
+typedef struct uwb_row_window {
+    uint64_t global_rows;
+    uint64_t buf_row0;
+    uint64_t row_begin;
+    uint64_t row_end;
+} uwb_row_window;
+
+uint64_t uwb_dev_cfar2d_window_workspace(const uwb_map_batch* batch, const uwb_row_window* win,
+                                         const uwb_cfar_params* params, uint64_t slab_rows,
+                                         uint64_t det_capacity);
+uwb_status uwb_dev_cfar2d_window(const uwb_map_batch* batch, const uwb_row_window* win,
+                                 const uwb_cfar_params* params, const double* alpha_dev, uint64_t slab_rows,
+                                 const uwb_cfar_outputs* out, void* workspace, uint64_t workspace_bytes,
+                                 uint32_t flags, void* stream);
+
 /* The global (M+1)x(N+1) tables of a batch in the device layout used by the
  * CFAR kernels: map i's padded element (i_r, j) at sat[i*sat_map_stride +
  * i_r*sat_ld + 31 + j] (the 31-element shift puts every 32-column group of a

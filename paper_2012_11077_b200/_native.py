@@ -63,6 +63,11 @@ class uwb_map_batch(C.Structure):
                 ("ld", C.c_uint64), ("map_stride", C.c_uint64)]
 
 
+class uwb_row_window(C.Structure):
+    _fields_ = [("global_rows", C.c_uint64), ("buf_row0", C.c_uint64), ("row_begin", C.c_uint64),
+                ("row_end", C.c_uint64)]
+
+
 class uwb_cfar_outputs(C.Structure):
     _fields_ = [("mask_bits", C.c_void_p), ("words_per_row", C.c_uint64),
                 ("mask_map_stride", C.c_uint64), ("mask_u8", C.c_void_p),
@@ -98,6 +103,8 @@ SIGNATURES = {
     "uwb_detect": (_S, [_P, _U64, _U64, _D, _D, _P, _U64, _P, _P, _P, _P, _P, _P, _P, _U64, _P]),
     "uwb_dev_cfar2d_workspace": (_U64, [_P, _P, C.c_int32, _U64, _U64]),
     "uwb_dev_cfar2d": (_S, [_P, _P, _P, C.c_int32, _U64, _P, _P, _U64, C.c_uint32, _P]),
+    "uwb_dev_cfar2d_window_workspace": (_U64, [_P, _P, _P, _U64, _U64]),
+    "uwb_dev_cfar2d_window": (_S, [_P, _P, _P, _P, _U64, _P, _P, _U64, C.c_uint32, _P]),
     "uwb_dev_build_sat": (_S, [_P, _P, _U64, _U64, _P, _P, _U64, _P]),
     "uwb_dev_build_sat_workspace": (_U64, [_P]),
     "uwb_host_cfar2d_batch": (_S, [_P, _P, C.c_int32, _U64, _P, _P, _U64, _P, _U64]),

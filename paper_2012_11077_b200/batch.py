@@ -25,7 +25,11 @@ class BatchCfar:
     def __init__(self, n_maps: int, rows: int, cols: int, params: CfarParams,
                  dtype: torch.dtype = torch.float32, sat_mode: str = "global", slab_rows: int = 0,
                  det_capacity: int = 1024, device=None, want_mask_u8: bool = False,
-                 want_thresholds: bool = False):
+                 want_thresholds: bool = False, window: tuple[int, int, int, int] | None = None):
+        """``window = (global_rows, buf_row0, row_begin, row_end)``: the maps passed
+        to each call hold rows [buf_row0, buf_row0 + rows) of maps with
+        ``global_rows`` rows and the call owns rows [row_begin, row_end) (one
+        rank's row slab); outputs then cover the owned rows only."""
         if dtype not in _DT:
             raise ValueError("maps must be float32 or float64")
         params.validate()
@@ -37,24 +41,32 @@ class BatchCfar:
         self.slab_rows = int(slab_rows)
         self.det_capacity = int(det_capacity)
         self.words_per_row = (self.cols + 31) // 32
+        self.window = None if window is None else N.uwb_row_window(*(int(x) for x in window))
+        out_rows = self.rows if window is None else int(window[3]) - int(window[2])
+        self.out_rows = out_rows
         dev = self.device
         self.alpha = torch.from_numpy(params.alpha_table()).to(dev)
-        self.mask_bits = torch.zeros((self.n_maps, self.rows, self.words_per_row), dtype=torch.int32, device=dev)
+        self.mask_bits = torch.zeros((self.n_maps, out_rows, self.words_per_row), dtype=torch.int32, device=dev)
         self.dets = torch.zeros((self.n_maps, max(1, self.det_capacity), 32), dtype=torch.uint8, device=dev)
         self.counts = torch.zeros(self.n_maps, dtype=torch.int64, device=dev)
         self.first_bad = torch.zeros((self.n_maps, 2), dtype=torch.int64, device=dev)
-        self.mask_u8 = (torch.zeros((self.n_maps, self.rows, self.cols), dtype=torch.uint8, device=dev)
+        self.mask_u8 = (torch.zeros((self.n_maps, out_rows, self.cols), dtype=torch.uint8, device=dev)
                         if want_mask_u8 else None)
-        self.thresholds = (torch.zeros((self.n_maps, self.rows, self.cols), dtype=torch.float64, device=dev)
+        self.thresholds = (torch.zeros((self.n_maps, out_rows, self.cols), dtype=torch.float64, device=dev)
                            if want_thresholds else None)
         self._cparams = params.to_c()
         self._batch = N.uwb_map_batch(None, _DT[dtype], 0, self.n_maps, self.rows, self.cols, self.cols,
                                       self.rows * self.cols)
-        ws = N.lib.uwb_dev_cfar2d_workspace(C.byref(self._batch), C.byref(self._cparams), self.sat_mode,
-                                            C.c_uint64(self.slab_rows), C.c_uint64(self.det_capacity))
+        if self.window is None:
+            ws = N.lib.uwb_dev_cfar2d_workspace(C.byref(self._batch), C.byref(self._cparams), self.sat_mode,
+                                                C.c_uint64(self.slab_rows), C.c_uint64(self.det_capacity))
+        else:
+            ws = N.lib.uwb_dev_cfar2d_window_workspace(C.byref(self._batch), C.byref(self.window),
+                                                       C.byref(self._cparams), C.c_uint64(self.slab_rows),
+                                                       C.c_uint64(self.det_capacity))
         self.workspace = torch.empty(int(ws), dtype=torch.uint8, device=dev)
         self._out = N.uwb_cfar_outputs(
-            self.mask_bits.data_ptr(), self.words_per_row, self.rows * self.words_per_row,
+            self.mask_bits.data_ptr(), self.words_per_row, out_rows * self.words_per_row,
             self.mask_u8.data_ptr() if self.mask_u8 is not None else None,
             self.thresholds.data_ptr() if self.thresholds is not None else None,
             self.dets.data_ptr(), self.det_capacity, self.counts.data_ptr(), self.first_bad.data_ptr())
@@ -69,10 +81,17 @@ class BatchCfar:
             raise ValueError("maps must be a contiguous CUDA tensor")
         self._batch.maps = maps.data_ptr()
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
-        st = N.lib.uwb_dev_cfar2d(C.byref(self._batch), C.byref(self._cparams), self.alpha.data_ptr(),
-                                  self.sat_mode, C.c_uint64(self.slab_rows), C.byref(self._out),
-                                  self.workspace.data_ptr(), C.c_uint64(self.workspace.numel()),
-                                  (0 if sort else 1) | (2 if phase_events else 0), C.c_void_p(s.cuda_stream))
+        flags = (0 if sort else 1) | (2 if phase_events else 0)
+        if self.window is None:
+            st = N.lib.uwb_dev_cfar2d(C.byref(self._batch), C.byref(self._cparams), self.alpha.data_ptr(),
+                                      self.sat_mode, C.c_uint64(self.slab_rows), C.byref(self._out),
+                                      self.workspace.data_ptr(), C.c_uint64(self.workspace.numel()), flags,
+                                      C.c_void_p(s.cuda_stream))
+        else:
+            st = N.lib.uwb_dev_cfar2d_window(C.byref(self._batch), C.byref(self.window), C.byref(self._cparams),
+                                             self.alpha.data_ptr(), C.c_uint64(self.slab_rows), C.byref(self._out),
+                                             self.workspace.data_ptr(), C.c_uint64(self.workspace.numel()),
+                                             flags, C.c_void_p(s.cuda_stream))
         raise_for(st)
 
     # ---- host views (synchronising) ----
@@ -98,13 +117,13 @@ class BatchCfar:
         return np.frombuffer(raw.tobytes(), dtype=DETECTION_DTYPE, count=n).copy()
 
     def mask(self, i: int) -> np.ndarray:
-        """Unpack map i's bit mask into a rows x cols uint8 array."""
+        """Unpack map i's bit mask into an (owned rows) x cols uint8 array."""
         words = self.mask_bits[i].cpu().numpy().view(np.uint32)
-        bits = np.unpackbits(words.view(np.uint8).reshape(self.rows, -1), axis=1, bitorder="little")
+        bits = np.unpackbits(words.view(np.uint8).reshape(self.out_rows, -1), axis=1, bitorder="little")
         return bits[:, : self.cols].astype(np.uint8)
 
 
-def phase_ms(max_calls: int = 4096) -> np.ndarray:
+def phase_ms(max_calls: int = 1024) -> np.ndarray:
     """(calls, 3) array of {sat, cfar, sort} milliseconds of the calls made with
     ``phase_events=True`` since the last read (synchronises on them)."""
     out = np.zeros((max_calls, 3), dtype=np.float32)

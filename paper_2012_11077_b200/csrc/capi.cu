@@ -153,20 +153,29 @@ struct Plan {
     size_t off_tables, off_edge, off_prog, off_counter, off_scratch, total;
 };
 
+// win == nullptr: the batch holds whole maps. Otherwise the batch buffer holds
+// rows [win->buf_row0, +b.rows) of maps with win->global_rows rows and the call
+// owns rows [win->row_begin, win->row_end) (always slab-local tables with halo).
 Plan make_plan(const uwb_map_batch& b, const uwb_cfar_params* p, int sat_mode, uint64_t slab_rows,
-               int64_t det_cap) {
+               int64_t det_cap, const uwb_row_window* win = nullptr) {
     Plan P{};
     P.n_maps = static_cast<int64_t>(b.n_maps);
     P.cols = static_cast<int64_t>(b.cols);
-    P.geo.rows = static_cast<int64_t>(b.rows);
-    if (sat_mode == UWB_SAT_SLAB && slab_rows > 0 && slab_rows < b.rows) {
-        P.geo.slab_rows = static_cast<int64_t>(slab_rows);
+    P.geo.rows = static_cast<int64_t>(win ? win->global_rows : b.rows);
+    P.geo.row_lo = static_cast<int64_t>(win ? win->row_begin : 0);
+    P.geo.row_hi = static_cast<int64_t>(win ? win->row_end : b.rows);
+    P.geo.buf_row0 = static_cast<int64_t>(win ? win->buf_row0 : 0);
+    P.geo.buf_rows = static_cast<int64_t>(b.rows);
+    const int64_t owned = P.geo.row_hi - P.geo.row_lo;
+    if (win || (sat_mode == UWB_SAT_SLAB && slab_rows > 0 && static_cast<int64_t>(slab_rows) < owned)) {
+        P.geo.slab_rows = slab_rows > 0 && static_cast<int64_t>(slab_rows) < owned ? static_cast<int64_t>(slab_rows)
+                                                                                  : (owned > 0 ? owned : 1);
         P.geo.halo = p ? p->guard_rows + p->background_rows : 0;
     } else {
-        P.geo.slab_rows = P.geo.rows > 0 ? P.geo.rows : 1;
+        P.geo.slab_rows = owned > 0 ? owned : 1;
         P.geo.halo = 0;
     }
-    P.geo.n_slabs = P.geo.rows > 0 ? (P.geo.rows + P.geo.slab_rows - 1) / P.geo.slab_rows : 0;
+    P.geo.n_slabs = owned > 0 ? (owned + P.geo.slab_rows - 1) / P.geo.slab_rows : 0;
     P.n_jobs = P.n_maps * P.geo.n_slabs;
     P.max_rows = P.geo.max_table_rows();
     P.table_ld = table_ld_for(P.cols);
@@ -280,9 +289,10 @@ PhaseRing g_phase;
 // Device-resident CFAR of a batch (no validation beyond layout; see uwb_dev_cfar2d).
 uwb_status dev_cfar(const uwb_map_batch& b, const uwb_cfar_params& p, const double* alpha,
                     int backend, int sat_mode, uint64_t slab_rows, const uwb_cfar_outputs& o,
-                    void* workspace, uint64_t ws_bytes, uint32_t flags, cudaStream_t s) {
+                    void* workspace, uint64_t ws_bytes, uint32_t flags, cudaStream_t s,
+                    const uwb_row_window* win = nullptr) {
     const Plan P = make_plan(b, &p, backend == UWB_INTEGRAL ? sat_mode : UWB_SAT_GLOBAL, slab_rows,
-                             static_cast<int64_t>(o.det_capacity));
+                             static_cast<int64_t>(o.det_capacity), win);
     if (P.n_jobs > 65535) return fail(UWB_INVALID_ARGUMENT, "uwb: more than 65535 (map, slab) jobs per call");
     if (backend == UWB_INTEGRAL && ws_bytes < P.total) return fail(UWB_INVALID_ARGUMENT, "uwb: workspace too small");
     char* ws = static_cast<char*>(workspace);
@@ -501,6 +511,44 @@ uwb_status uwb_dev_cfar2d(const uwb_map_batch* b, const uwb_cfar_params* p, cons
     if (ws_bytes < P.total) return fail(UWB_INVALID_ARGUMENT, "uwb: workspace too small (need " + S(static_cast<uint64_t>(P.total)) + ")");
     if (uwb_status s = dev_cfar(*b, *p, alpha_dev, UWB_INTEGRAL, sat_mode, slab_rows, *out, workspace,
                                 ws_bytes, flags, static_cast<cudaStream_t>(stream)))
+        return s;
+    return ok();
+}
+
+static uwb_status check_window(const uwb_map_batch* b, const uwb_row_window* w, const uwb_cfar_params* p) {
+    if (!w) return fail(UWB_INVALID_ARGUMENT, "uwb: null row window");
+    if (w->row_begin >= w->row_end || w->row_end > w->global_rows)
+        return fail(UWB_BOUNDS_ERROR, "uwb: row window [" + S(w->row_begin) + ", " + S(w->row_end) +
+                                          ") outside a map of " + S(w->global_rows) + " rows");
+    const uint64_t halo = static_cast<uint64_t>(p->guard_rows + p->background_rows);
+    const uint64_t need0 = w->row_begin > halo ? w->row_begin - halo : 0;
+    const uint64_t need1 = std::min(w->global_rows, w->row_end + halo);
+    if (w->buf_row0 > need0 || w->buf_row0 + b->rows < need1)
+        return fail(UWB_BOUNDS_ERROR, "uwb: the buffer holds rows [" + S(w->buf_row0) + ", " +
+                                          S(w->buf_row0 + b->rows) + "), the window needs [" + S(need0) + ", " +
+                                          S(need1) + ")");
+    return UWB_OK;
+}
+
+uint64_t uwb_dev_cfar2d_window_workspace(const uwb_map_batch* b, const uwb_row_window* win,
+                                         const uwb_cfar_params* p, uint64_t slab_rows, uint64_t det_capacity) {
+    return make_plan(*b, p, UWB_SAT_SLAB, slab_rows, static_cast<int64_t>(det_capacity), win).total;
+}
+
+uwb_status uwb_dev_cfar2d_window(const uwb_map_batch* b, const uwb_row_window* win, const uwb_cfar_params* p,
+                                 const double* alpha_dev, uint64_t slab_rows, const uwb_cfar_outputs* out,
+                                 void* workspace, uint64_t ws_bytes, uint32_t flags, void* stream) {
+    if (uwb_status s = check_batch(b)) return s;
+    if (uwb_status s = validate_params(*p)) return s;
+    if (b->rows == 0 || b->cols == 0) return fail(UWB_DIMENSION_ERROR, "cfar2d: power map must be at least 1x1");
+    if (uwb_status s = check_window(b, win, p)) return s;
+    if (degenerate(*p, win->global_rows, b->cols))
+        return fail(UWB_CONFIGURATION_ERROR, degenerate_msg(*p, win->global_rows, b->cols));
+    if (uwb_status s = need_device()) return s;
+    const Plan P = make_plan(*b, p, UWB_SAT_SLAB, slab_rows, static_cast<int64_t>(out->det_capacity), win);
+    if (ws_bytes < P.total) return fail(UWB_INVALID_ARGUMENT, "uwb: workspace too small (need " + S(static_cast<uint64_t>(P.total)) + ")");
+    if (uwb_status s = dev_cfar(*b, *p, alpha_dev, UWB_INTEGRAL, UWB_SAT_SLAB, slab_rows, *out, workspace, ws_bytes,
+                                flags, static_cast<cudaStream_t>(stream), win))
         return s;
     return ok();
 }

@@ -74,7 +74,7 @@ cfar_integral_kernel(CfarLaunch L) {
             const double sum = dsub(rs_o, rs_g);
             const double mean = ddiv(sum, static_cast<double>(n));
             thr = dmul(__ldg(L.alpha + n), mean);
-            v = load_cell(cut_base + static_cast<int64_t>(r) * L.ld + c);
+            v = load_cell(cut_base + (r - L.geo.buf_row0) * L.ld + c);
             hit = v > thr; // cfar.cpp:125, ties -> H0
             if (v < 0.0)
                 report_min(L.first_bad + 2 * map + 1, static_cast<unsigned long long>(static_cast<int64_t>(r) * cols + c));

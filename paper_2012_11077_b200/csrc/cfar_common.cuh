@@ -25,10 +25,10 @@ __device__ __forceinline__ void emit_cells(const CfarLaunch& L, int64_t map, int
     if (lane == 0 && L.mask_bits) {
         const int word = c >> 5;
         if (word < L.words_per_row)
-            L.mask_bits[map * L.mask_map_stride + static_cast<int64_t>(r) * L.words_per_row + word] = bits;
+            L.mask_bits[map * L.mask_map_stride + (r - L.geo.row_lo) * L.words_per_row + word] = bits;
     }
     if (valid && (L.mask_u8 || L.thresholds)) {
-        const int64_t cell = map * L.geo.rows * L.cols + static_cast<int64_t>(r) * L.cols + c;
+        const int64_t cell = (map * L.geo.out_rows() + (r - L.geo.row_lo)) * L.cols + c;
         if (L.mask_u8) L.mask_u8[cell] = hit ? 1 : 0;
         if (L.thresholds) L.thresholds[cell] = thr;
     }

@@ -155,7 +155,7 @@ __device__ __forceinline__ void emit_block(const CfarLaunch& L, int64_t map, int
     const int wk = lane / CPT, wj = lane % CPT;
     const int wc = c_word0 + wj * kWarp; // first column of the word
     if (lane < CPT * RS && r0 + wk <= r_last && wc < cols && L.mask_bits)
-        L.mask_bits[map * L.mask_map_stride + static_cast<int64_t>(r0 + wk) * L.words_per_row + (wc >> 5)] = my_word;
+        L.mask_bits[map * L.mask_map_stride + (r0 + wk - L.geo.row_lo) * L.words_per_row + (wc >> 5)] = my_word;
     if (per_cell) { // parity runs only
 #pragma unroll
         for (int k = 0; k < RS; ++k) {
@@ -163,7 +163,7 @@ __device__ __forceinline__ void emit_block(const CfarLaunch& L, int64_t map, int
             for (int j = 0; j < CPT; ++j) {
                 if (okc[j] && r0 + k <= r_last) {
                     const int64_t cell =
-                        map * L.geo.rows * L.cols + static_cast<int64_t>(r0 + k) * cols + c_first + j * kWarp;
+                        (map * L.geo.out_rows() + (r0 + k - L.geo.row_lo)) * cols + c_first + j * kWarp;
                     if (L.mask_u8) L.mask_u8[cell] = hit[k][j] ? 1 : 0;
                     if (L.thresholds) L.thresholds[cell] = thr[k][j];
                 }
@@ -262,8 +262,9 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
         const int last_grp = (i_hi - i_lo) / kG;
         for (int g = 0; g <= min(last_grp, kPfGroups - 1); ++g)
             tma_prefetch3(&tmap_tab, e_lo, i_lo + g * kG - trow0, static_cast<int>(job));
+        const int buf0 = static_cast<int>(L.geo.buf_row0);
         for (int g = 0; g < min(n_cg, kPfGroups); ++g)
-            tma_prefetch3(&tmap_cut, c0, ra + g * kG, static_cast<int>(map));
+            tma_prefetch3(&tmap_cut, c0, ra + g * kG - buf0, static_cast<int>(map));
         int grp = 0, gslot = 0, gphase = 0;   // next table group, its slot and empty-phase
         int cstep = 0, cslot = 0, cphase = 0; // next CUT group
         // Issue order: always the load the consumers need first; block (suspended)
@@ -291,10 +292,10 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
                 if (cstep >= kCutGroups) mbar_wait_susp(&empty_c[cslot], static_cast<unsigned>(cphase ^ 1), L.sleep_ns);
                 const int first = ra + cstep * kG;
                 mbar_expect_tx(&full_c[cslot], kCutBox);
-                tma_box3(cuts + static_cast<size_t>(cslot) * kG * kW, &tmap_cut, c0, first, static_cast<int>(map),
-                         &full_c[cslot]);
+                tma_box3(cuts + static_cast<size_t>(cslot) * kG * kW, &tmap_cut, c0, first - buf0,
+                         static_cast<int>(map), &full_c[cslot]);
                 if (cstep + kPfGroups < n_cg)
-                    tma_prefetch3(&tmap_cut, c0, first + kPfGroups * kG, static_cast<int>(map));
+                    tma_prefetch3(&tmap_cut, c0, first + kPfGroups * kG - buf0, static_cast<int>(map));
                 if (++cslot == kCutGroups) { cslot = 0; cphase ^= 1; }
                 ++cstep;
             }
@@ -400,7 +401,7 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
                     emit_block<RS, CPT>(L, map, r0, r_last, wc0, c0 + tc, okc, hit, v, thr, false);
                 } else if (lane < CPT * RS && L.mask_bits) { // no hit in the block: zero mask words
                     const int wk = lane / CPT, wc = wc0 + (lane % CPT) * kWarp;
-                    L.mask_bits[map * L.mask_map_stride + static_cast<int64_t>(r0 + wk) * L.words_per_row +
+                    L.mask_bits[map * L.mask_map_stride + (r0 + wk - L.geo.row_lo) * L.words_per_row +
                                 (wc >> 5)] = 0u;
                 }
             } else {
@@ -545,9 +546,9 @@ cudaError_t go(const CfarLaunch& L0, cudaStream_t stream) {
                  L.table_stride, BOXC, kG))
         return cudaErrorNotSupported;
     // a single map's stride is never used; give the encoder a valid one
-    const int64_t mstride = n_maps > 1 ? L.map_stride : (L.ld * L.geo.rows + 1) / 2 * 2;
+    const int64_t mstride = n_maps > 1 ? L.map_stride : (L.ld * L.geo.buf_rows + 1) / 2 * 2;
     if (!encode3(&tmap_cut, sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
-                 sizeof(T), L.maps, L.cols, L.geo.rows, n_maps, L.ld, mstride, kW, kG))
+                 sizeof(T), L.maps, L.cols, L.geo.buf_rows, n_maps, L.ld, mstride, kW, kG))
         return cudaErrorNotSupported;
     const size_t smem = ring_smem_bytes<T>(L.hr, BOXC, SG);
     if (smem > 227 * 1024) return cudaErrorNotSupported;

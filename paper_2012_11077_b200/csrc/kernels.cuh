@@ -26,17 +26,27 @@ __host__ __device__ constexpr int64_t table_ld_for(int64_t cols) {
 // A batch is split into jobs: job = (map, slab). GLOBAL mode has one slab per
 // map covering all rows; SLAB mode owns rows [s*slab_rows, (s+1)*slab_rows) and
 // builds its table over the owned rows plus `halo` rows on each side (clipped).
+//
+// A call may also cover only a row window of larger maps (one rank's share of a
+// map sharded by rows): the buffer then holds global rows
+// [buf_row0, buf_row0 + buf_rows), the call owns rows [row_lo, row_hi), windows
+// clamp with the global row count `rows`, and outputs are indexed by row - row_lo.
 struct JobGeometry {
-    int64_t rows;       // map rows
-    int64_t slab_rows;  // owned rows per slab (== rows in GLOBAL mode)
+    int64_t rows;       // global map rows (clamp bounds)
+    int64_t slab_rows;  // owned rows per slab (== owned rows in GLOBAL mode)
     int64_t n_slabs;
     int64_t halo;       // g_r + b_r in SLAB mode, 0 in GLOBAL mode
+    int64_t row_lo;     // first owned row of the call
+    int64_t row_hi;     // end of the owned rows
+    int64_t buf_row0;   // global row of the input buffer's row 0
+    int64_t buf_rows;   // rows present in the input buffer
 
-    __host__ __device__ int64_t owned_begin(int64_t s) const { return s * slab_rows; }
+    __host__ __device__ int64_t owned_begin(int64_t s) const { return row_lo + s * slab_rows; }
     __host__ __device__ int64_t owned_end(int64_t s) const {
-        const int64_t e = (s + 1) * slab_rows;
-        return e < rows ? e : rows;
+        const int64_t e = row_lo + (s + 1) * slab_rows;
+        return e < row_hi ? e : row_hi;
     }
+    __host__ __device__ int64_t out_rows() const { return row_hi - row_lo; }
     __host__ __device__ int64_t table_begin(int64_t s) const {
         const int64_t b = owned_begin(s) - halo;
         return b > 0 ? b : 0;
@@ -86,7 +96,7 @@ __host__ __device__ inline SatJobView sat_job(const SatLaunch& L, int64_t job) {
     const int64_t s = job % L.geo.n_slabs;
     const int64_t b = L.geo.table_begin(s);
     SatJobView v;
-    v.src = static_cast<const char*>(L.maps) + (m * L.map_stride + b * L.ld) * L.elem_bytes;
+    v.src = static_cast<const char*>(L.maps) + (m * L.map_stride + (b - L.geo.buf_row0) * L.ld) * L.elem_bytes;
     v.rows = L.geo.table_end(s) - b;
     v.row0 = b;
     v.table = L.table + job * L.table_stride;

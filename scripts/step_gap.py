@@ -15,7 +15,7 @@ runner = BatchCfar(n, 1024, 1024, params, torch.float32, det_capacity=512, devic
 for _ in range(3):
     runner(maps)
 torch.cuda.synchronize()
-phase_ms(4096)
+phase_ms(1024)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 for phase in (False, True):
     torch.cuda.synchronize()
@@ -30,4 +30,4 @@ for phase in (False, True):
     print(f"phase_events={phase}: device {e0.elapsed_time(e1) / 5:.3f} ms/step, host submit {(t1 - t0) * 1e3 / 5:.3f} ms/step,"
           f" wall {(t2 - t0) * 1e3 / 5:.3f}")
     if phase:
-        print(phase_ms(4096))
+        print(phase_ms(1024))

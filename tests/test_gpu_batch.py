@@ -153,3 +153,52 @@ def test_host_batch_e2e_matches_device_batch(uwb, cuda):
     for i in range(n):
         k = int(counts[i])
         assert torch.equal(dets[i, :k], b.dets[i, :k].cpu())
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_window_ranks_vs_restatement(uwb, oracle, cuda, world):
+    """Config 4 sharded by rows: each "rank" holds only its owned rows
+    plus the g+b halo (shard.row_slab) and runs uwb_dev_cfar2d_window with global
+    row clamps. Ranks run one after another on this GPU; every slab is
+    bit-identical to the restatement with the same row range and slab-local table,
+    and detections carry global rows."""
+    from paper_2012_11077_b200 import synth
+    from paper_2012_11077_b200.batch import BatchCfar
+    from paper_2012_11077_b200.shard import row_slab
+    rows, cols = 1500, 700
+    m = synth.cfg4_map(seed=11, device=cuda, rows=rows, cols=cols)
+    p = uwb.CfarParams(4, 32, 1e-5)
+    host = m.double().cpu().numpy()
+    halo = 4 + 32
+    total = 0
+    for rank in range(world):
+        s = row_slab(rows, world, rank, halo)
+        local = m[s.load_begin:s.load_end].contiguous().unsqueeze(0)
+        b = BatchCfar(1, s.load_end - s.load_begin, cols, p, torch.float32, det_capacity=8192,
+                      want_mask_u8=True, want_thresholds=True,
+                      window=(rows, s.load_begin, s.owned_begin, s.owned_end))
+        b(local)
+        torch.cuda.synchronize()
+        r = oracle.cfar(host, 4, 4, 32, 32, 1e-5, row_begin=s.owned_begin, row_end=s.owned_end, slab_local=True)
+        own = slice(s.owned_begin, s.owned_end)
+        assert_bitwise(b.thresholds[0].cpu().numpy(), r.threshold_map[own], f"rank {rank} thresholds")
+        assert np.array_equal(b.mask_u8[0].cpu().numpy(), r.mask[own])
+        assert np.array_equal(b.mask(0), r.mask[own])
+        d = b.detections(0)
+        exp = r.detections
+        assert len(d) == len(exp)
+        assert np.array_equal(d["row"], exp["row"]) and np.array_equal(d["col"], exp["col"])
+        assert_bitwise(d["threshold"], exp["threshold"], "detection thresholds")
+        total += len(d)
+    assert total > 0
+
+
+def test_row_window_rejects_missing_halo(uwb, cuda):
+    from paper_2012_11077_b200.batch import BatchCfar
+    from paper_2012_11077_b200.errors import BoundsError
+    p = uwb.CfarParams(2, 8, 1e-4)
+    local = torch.ones((1, 100, 64), device=cuda)
+    # owned rows [200, 300) need rows [190, 310); the buffer starts at 200
+    with pytest.raises(BoundsError):
+        b = BatchCfar(1, 100, 64, p, torch.float32, window=(1000, 200, 200, 300))
+        b(local)
