@@ -17,6 +17,8 @@ Launch: ``python bench.py [--gpus N --steps K --warmup W]``; for N > 1 under
 in 64-map blocks across ranks (strong scaling) and each step ends with the
 detection-count all-reduce. ``--impl reference`` times the reference C++ code
 (oracle/_ref, compiled from /root/reference) on the host cores instead.
+``--config {1,2,4,5}`` measures the other BASELINE.json configurations
+(bench_configs.py) with the same JSON schema.
 """
 from __future__ import annotations
 
@@ -380,8 +382,13 @@ def main():
     ap.add_argument("--maps", type=int, default=N_MAPS, help="batch size (profiling runs only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5],
+                    help="BASELINE.json configuration (3 = the headline line; see bench_configs.py)")
     args = ap.parse_args()
     globals()["N_MAPS"] = args.maps
+    if args.config != 3:
+        import bench_configs
+        return bench_configs.run(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_b200(args)

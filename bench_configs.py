@@ -1,0 +1,421 @@
+"""bench.py --config {1,2,4,5}: the other BASELINE.json workloads.
+
+bench.py's default line is config 3 (the throughput config BASELINE's metric is
+quoted on). These lines measure the remaining configurations with the same
+JSON schema so every row of SURVEY 8d has a number:
+
+* config 4 - one 16384 x 16384 fp32 map, g4 b32 Pfa 1e-5. One rank per GPU owns
+  a row slab (shard.row_slab) and holds only its rows plus the g+b halo; the
+  device path is uwb_dev_cfar2d_window (slab-local table, global clamps), then
+  the detection-count all-reduce. value = whole-map cells / device time (max
+  over ranks). At N=1 the window is the whole map, i.e. the reference-exact
+  global table.
+* config 5 - 64 K-clutter fp32 maps 8192 x 2048, the four runs (g_r,g_c,b_r,b_c)
+  in {(1,3,4,16), (3,1,16,4)} x Pfa in {1e-3, 1e-5}; one step = all four runs;
+  maps sharded across ranks. The reference cannot express per-axis windows, so
+  its CPU baseline is the C restatement (kind "port").
+* config 1 - one 256 x 512 fp64 map (launch-bound; ms_per_step is per map).
+* config 2 - front end + CFAR of one 512 x 1024 record through the host-level
+  detect() drop-in (value in records/s; H2D/D2H inside, so it is also e2e).
+"""
+from __future__ import annotations
+
+import json
+import statistics
+import time
+
+import numpy as np
+
+import bench as B
+
+
+def _line(**kw):
+    base = {"n_gpus": 1, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded BASELINE generator)"}
+    base.update(kw)
+    print(json.dumps(base), flush=True)
+
+
+def _events_time(fn, steps, warmup, world, dist):
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    return float(ms.item())
+
+
+def _phases(n):
+    from paper_2012_11077_b200.batch import phase_ms
+    ph = phase_ms(1024)[:n]
+    return {k: float(np.mean(ph[:, i])) for i, k in enumerate(("sat", "cfar", "sort"))} if len(ph) else {}
+
+
+def _roof(phases, cells, peak, peak_src):
+    kernels = {"sat_systolic_kernel": (phases.get("sat", 0.0), B.SAT_BYTES_PER_CELL * cells),
+               "cfar_ws_kernel": (phases.get("cfar", 0.0), B.CFAR_BYTES_PER_CELL * cells)}
+    dom = max(kernels, key=lambda k: kernels[k][0])
+    ms, by = kernels[dom]
+    ach = by / (ms / 1e3) / 1e9 if ms > 0 else 0.0
+    return {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "traffic": None, "bytes_per_cell": B.SAT_BYTES_PER_CELL if dom.startswith("sat") else
+            B.CFAR_BYTES_PER_CELL, "launch_ms": ms, "peak_source": peak_src}
+
+
+def _init_dist():
+    import torch
+    import torch.distributed as dist
+    world, rank, local = B._dist()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local if world > 1 else 0)
+    return world, rank, dist
+
+
+# ------------------------------------------------------------------ config 4 --
+def run_cfg4(args):
+    import torch
+    import paper_2012_11077_b200 as uwb
+    from paper_2012_11077_b200 import synth
+    from paper_2012_11077_b200.batch import BatchCfar, kernel_launches
+    from paper_2012_11077_b200.shard import reduce_count, row_slab
+    world, rank, dist = _init_dist()
+    R = C = 16384
+    g, b, pfa = 4, 32, 1e-5
+    s = row_slab(R, world, rank, g + b)
+    full = synth.cfg4_map(seed=4, device="cuda", rows=R, cols=C)
+    local = full[s.load_begin:s.load_end].contiguous().unsqueeze(0)
+    host_full = full.cpu() if (rank == 0 and world == 1 and not args.no_cpu_baseline) else None
+    del full
+    p = uwb.CfarParams(g, b, pfa)
+    runner = BatchCfar(1, s.load_end - s.load_begin, C, p, torch.float32, det_capacity=1 << 16,
+                       window=(R, s.load_begin, s.owned_begin, s.owned_end))
+    count = torch.zeros(1, dtype=torch.int64, device="cuda")
+
+    def step(phase=False):
+        runner(local, phase_events=phase)
+        count.copy_(runner.counts.sum().view(1))
+        reduce_count(count)
+
+    step(phase=True)
+    from paper_2012_11077_b200.batch import phase_ms
+    phase_ms(1024)
+    sampler = B.ClockSampler(torch.cuda.current_device())
+    sampler.start()
+    l0 = kernel_launches()
+    ms = _events_time(lambda: step(phase=True), args.steps, max(args.warmup - 1, 0), world, dist)
+    launches = kernel_launches() - l0
+    clocks = sampler.stop()
+    ph = _phases(args.steps + max(args.warmup - 1, 0))
+    owned_cells = (s.owned_end - s.owned_begin) * C
+    peak, src = B._peaks()
+
+    # end to end: pinned host slab -> H2D -> SAT+CFAR+sort -> D2H of mask and counts
+    host = torch.empty(local.shape, dtype=torch.float32, pin_memory=True)
+    host.copy_(local)
+    dev_in = torch.empty_like(local)
+    mask_host = torch.empty(runner.mask_bits.shape, dtype=torch.int32, pin_memory=True)
+    cnt_host = torch.empty(1, dtype=torch.int64, pin_memory=True)
+
+    def e2e_step():
+        dev_in.copy_(host, non_blocking=True)
+        runner(dev_in)
+        mask_host.copy_(runner.mask_bits, non_blocking=True)
+        cnt_host.copy_(runner.counts, non_blocking=True)
+        torch.cuda.synchronize()
+
+    e2e_step()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        e2e_step()
+    e_ms = torch.tensor([(time.perf_counter() - t0) * 1e3 / args.e2e_steps], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+    e_ms = float(e_ms.item())
+
+    cpu = None
+    if host_full is not None:
+        from oracle.pyoracle import RefLib
+        cores = B._cpu_threads()
+        secs, _ = RefLib().time_cfar_batch(host_full.numpy()[None], g, b, pfa, 1, ref_threads=cores)
+        cpu = {"value": R * C / secs / 1e9, "unit": B.UNIT, "cores": cores, "kind": "reference",
+               "sample": f"the whole config-4 map, uwbvital_ref::cfar2d_integral(map, params, {cores}) "
+                         f"(the reference's own row threads; build_sat is serial), {secs:.2f} s"}
+    if rank == 0:
+        _line(metric=B.METRIC, value=R * C / (ms / 1e3) / 1e9, unit=B.UNIT, n_gpus=world, steps=args.steps,
+              warmup=args.warmup, ms_per_step=ms,
+              config={"workload": "cfg4: one 16384x16384 fp32 map, Exp(1) + 1000 3x3 targets at U(6,18) dB, "
+                                  "guard 4, train 32, Pfa 1e-5",
+                      "parallelism": f"row slabs over {world} GPU(s), halo {g + b} rows, slab-local tables, "
+                                     "global clamps (uwb_dev_cfar2d_window)",
+                      "sat": "global table (reference-exact)" if world == 1 else "slab-local tables",
+                      "l2": "1 GiB input + 2.1 GiB table per pass >> 126 MB L2",
+                      "detections_per_step": int(count.item())},
+              roofline=_roof(ph, owned_cells, peak, src), phases_ms=ph, cpu_baseline=cpu,
+              e2e={"value": R * C / (e_ms / 1e3) / 1e9, "unit": B.UNIT,
+                   "h2d_bytes_per_step": int(host.numel() * 4) * world,
+                   "d2h_bytes_per_step": int(mask_host.numel() * 4 + 8) * world, "ms_per_step": e_ms,
+                   "timer": "host wall clock, H2D + compute + D2H, max over ranks"},
+              gpu_launches=int(launches), clocks=clocks)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+# ------------------------------------------------------------------ config 5 --
+CFG5_RUNS = [((1, 3, 4, 16), 1e-3), ((1, 3, 4, 16), 1e-5), ((3, 1, 16, 4), 1e-3), ((3, 1, 16, 4), 1e-5)]
+
+
+def run_cfg5(args):
+    import torch
+    import paper_2012_11077_b200 as uwb
+    from paper_2012_11077_b200 import synth
+    from paper_2012_11077_b200.batch import BatchCfar, host_cfar2d_batch, kernel_launches
+    from paper_2012_11077_b200.shard import map_shard, reduce_count
+    world, rank, dist = _init_dist()
+    n_all, R, C = 64, 8192, 2048
+    m0, m1 = map_shard(n_all, world, rank, block=8)
+    maps = torch.empty((m1 - m0, R, C), dtype=torch.float32, device="cuda")
+    for blk in range(m0 // 8, m1 // 8):
+        maps[blk * 8 - m0:(blk + 1) * 8 - m0] = synth.cfg5_maps(8, seed=5_000 + blk, device="cuda", rows=R, cols=C)
+    runners = []
+    for (gr, gc, br, bc), pfa in CFG5_RUNS:
+        p = uwb.CfarParams(guard_radius=gr, background_radius=br, pfa=pfa, guard_cols=gc, background_cols=bc)
+        runners.append(BatchCfar(m1 - m0, R, C, p, torch.float32, det_capacity=1 << 15))
+    count = torch.zeros(1, dtype=torch.int64, device="cuda")
+
+    def step(phase=False):
+        count.zero_()
+        for rn in runners:
+            rn(maps, phase_events=phase)
+            count.add_(rn.counts.sum())
+        reduce_count(count)
+
+    step(phase=True)
+    from paper_2012_11077_b200.batch import phase_ms
+    phase_ms(1024)
+    sampler = B.ClockSampler(torch.cuda.current_device())
+    sampler.start()
+    l0 = kernel_launches()
+    ms = _events_time(lambda: step(phase=True), args.steps, max(args.warmup - 1, 0), world, dist)
+    launches = kernel_launches() - l0
+    clocks = sampler.stop()
+    ph = _phases(4 * (args.steps + max(args.warmup - 1, 0)))
+    cells_local = (m1 - m0) * R * C
+    peak, src = B._peaks()
+
+    # end to end through the host API, all four runs
+    host = torch.empty(maps.shape, dtype=torch.float32, pin_memory=True)
+    host.copy_(maps)
+    outs = [(torch.empty(rn.mask_bits.shape, dtype=torch.int32, pin_memory=True),
+             torch.empty((m1 - m0, rn.det_capacity, 32), dtype=torch.uint8, pin_memory=True),
+             torch.empty(m1 - m0, dtype=torch.int64, pin_memory=True)) for rn in runners]
+
+    def e2e_step():
+        for rn, (bits, dets, cnt) in zip(runners, outs):
+            host_cfar2d_batch(host, rn.params, bits, dets, cnt, rn.det_capacity, maps_per_chunk=4)
+
+    e2e_step()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        e2e_step()
+    e_ms = torch.tensor([(time.perf_counter() - t0) * 1e3 / args.e2e_steps], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+    e_ms = float(e_ms.item())
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle.pyoracle import OracleLib
+        o = OracleLib()
+        one = maps[0].double().cpu().numpy()
+        t0 = time.perf_counter()
+        for (gr, gc, br, bc), pfa in CFG5_RUNS:
+            o.cfar(one, gr, gc, br, bc, pfa)
+        secs = time.perf_counter() - t0
+        cpu = {"value": 4 * R * C / secs / 1e9, "unit": B.UNIT, "cores": 1, "kind": "port",
+               "sample": f"one config-5 map x the 4 runs through the C restatement (uwbo_cfar, 1 thread; the "
+                         f"reference has no per-axis windows), {secs:.2f} s"}
+    if rank == 0:
+        total_cells = 4 * n_all * R * C
+        _line(metric=B.METRIC, value=total_cells / (ms / 1e3) / 1e9, unit=B.UNIT, n_gpus=world, steps=args.steps,
+              warmup=args.warmup, ms_per_step=ms,
+              config={"workload": "cfg5: 64 K-clutter fp32 maps 8192x2048 (Gamma(0.5) texture, 16x16 box, "
+                                  "x Exp(1) speckle) + 64 clusters/map at U(10,25) dB; windows (g_r,g_c,b_r,b_c) "
+                                  "(1,3,4,16),(3,1,16,4) x Pfa 1e-3,1e-5; one step = the 4 runs",
+                      "parallelism": f"dp{world} (maps sharded in 8-map blocks)",
+                      "l2": "4 GiB input per run >> 126 MB L2", "detections_per_step": int(count.item())},
+              roofline=_roof(ph, cells_local, peak, src), phases_ms=ph, cpu_baseline=cpu,
+              e2e={"value": total_cells / (e_ms / 1e3) / 1e9, "unit": B.UNIT,
+                   "h2d_bytes_per_step": int(4 * host.numel() * 4) * world,
+                   "d2h_bytes_per_step": int(sum(o[0].numel() * 4 + o[1].numel() + o[2].numel() * 8
+                                                 for o in outs)) * world,
+                   "ms_per_step": e_ms, "timer": "host wall clock around the synchronous calls"},
+              gpu_launches=int(launches), clocks=clocks)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+# ------------------------------------------------------------------ config 1 --
+def run_cfg1(args):
+    import torch
+    import paper_2012_11077_b200 as uwb
+    from paper_2012_11077_b200 import synth
+    from paper_2012_11077_b200.batch import BatchCfar, kernel_launches
+    world, rank, dist = _init_dist()
+    m = synth.cfg1_map(seed=1, device="cuda").unsqueeze(0).contiguous()
+    p = uwb.CfarParams(2, 8, 1e-4)
+    runner = BatchCfar(1, 256, 512, p, torch.float64, det_capacity=4096)
+    l0 = kernel_launches()
+    ms = _events_time(lambda: runner(m), args.steps, args.warmup, world, dist)
+    launches = (kernel_launches() - l0) * args.steps // (args.steps + args.warmup)
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        from oracle.pyoracle import RefLib
+        ref = RefLib()
+        host = m[0].cpu().numpy()
+        ref.cfar2d(host, 2, 8, 1e-4)
+        t0 = time.perf_counter()
+        reps = 20
+        for _ in range(reps):
+            ref.cfar2d(host, 2, 8, 1e-4)
+        secs = (time.perf_counter() - t0) / reps
+        cpu = {"value": 256 * 512 / secs / 1e9, "unit": B.UNIT, "cores": 1, "kind": "reference",
+               "sample": f"the config-1 map, uwbvital_ref::cfar2d_integral(map, params, 1) incl. threshold map, "
+                         f"{secs * 1e3:.2f} ms"}
+    if rank == 0:
+        _line(metric=B.METRIC, value=256 * 512 / (ms / 1e3) / 1e9, unit=B.UNIT, n_gpus=world, steps=args.steps,
+              warmup=args.warmup, ms_per_step=ms,
+              config={"workload": "cfg1: one fp64 map 256x512, Exp(1) + 5 targets at 15 dB, guard 2, train 8, "
+                                  "Pfa 1e-4 (launch-bound; ms_per_step is per map)", "parallelism": "replicas"},
+              roofline=None, cpu_baseline=cpu, e2e=None, gpu_launches=int(launches), clocks=None)
+    return 0
+
+
+# ------------------------------------------------------------------ config 2 --
+def run_cfg2(args):
+    import paper_2012_11077_b200 as uwb
+    from paper_2012_11077_b200 import synth
+    world, rank, _ = B._dist()
+    rec = synth.cfg2_record(seed=2, device="cpu").double().numpy()
+    frame = uwb.RadarFrame(rec, fast_rate=39e9, prf=20.0)
+    cfg = uwb.PipelineConfig(mean_filter_window=5, fft_length=1024, band_low_hz=0.3, band_high_hz=0.8,
+                             cfar=uwb.CfarParams(1, 4, 1e-3))
+    for _ in range(args.warmup):
+        uwb.detect(frame, cfg)
+    t = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        out = uwb.detect(frame, cfg)
+        t.append(time.perf_counter() - t0)
+    step = statistics.median(t)
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        from oracle.pyoracle import RefLib
+        ref = RefLib()
+        kw = dict(fast_rate=39e9, prf=20.0, mean_filter_window=5, fft_length=1024, guard_radius=1,
+                  background_radius=4, pfa=1e-3)
+        ref.detect(rec, **kw)
+        t0 = time.perf_counter()
+        for _ in range(5):
+            ref.detect(rec, **kw)
+        secs = (time.perf_counter() - t0) / 5
+        cpu = {"value": 1.0 / secs, "unit": "records/s", "cores": 1, "kind": "reference",
+               "sample": f"one config-2 record through uwbvital_ref::detect (FFT: the FFTW-API shim, not FFTW), "
+                         f"{secs * 1e3:.1f} ms"}
+    if rank == 0:
+        _line(metric="front end + CA-CFAR records/s (detect(), config 2)", value=1.0 / step, unit="records/s",
+              n_gpus=1, steps=args.steps, warmup=args.warmup, ms_per_step=step * 1e3,
+              config={"workload": "cfg2: raw fp32 record 512x1024 at 20 Hz -> DC, detrend, mean filter 5, "
+                                  "normalise, FFT L=1024, band 0.3-0.8 Hz (K=25), CFAR g1 b4 Pfa 1e-3",
+                      "band_bins": int(np.shape(out.band_map.power)[1]),
+                      "parallelism": "replicas (one record)"},
+              roofline=None, cpu_baseline=cpu,
+              e2e={"value": 1.0 / step, "unit": "records/s", "h2d_bytes_per_step": int(rec.size * 8),
+                   "d2h_bytes_per_step": None, "note": "host-level detect(): every step copies in and out"},
+              gpu_launches=None, clocks=None)
+    return 0
+
+
+def run_reference_cfg(args):
+    """--impl reference for configs 4/5/1/2: the reference CPU path on the host cores."""
+    world, rank, _ = B._dist()
+    if rank != 0:
+        return 0
+    import torch
+    from oracle.pyoracle import OracleLib, RefLib
+    from paper_2012_11077_b200 import synth
+    cores = B._cpu_threads()
+    ref = RefLib()
+    if args.config == 4:
+        m = synth.cfg4_map(seed=4, device="cpu", rows=4096, cols=16384).numpy()[None]
+        times = [ref.time_cfar_batch(m, 4, 32, 1e-5, 1, ref_threads=cores)[0] for _ in range(args.steps)]
+        cells, what = m[0].size, f"4096 of the 16384 rows of the config-4 map per step, cfar2d_integral(threads={cores})"
+    elif args.config == 5:
+        o = OracleLib()
+        m = synth.cfg5_maps(1, seed=5_000, device="cpu", rows=8192, cols=2048)[0].double().numpy()
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            for (gr, gc, br, bc), pfa in CFG5_RUNS:
+                o.cfar(m, gr, gc, br, bc, pfa)
+            times.append(time.perf_counter() - t0)
+        cells, what = 4 * m.size, "one config-5 map x 4 runs, C restatement (reference has no per-axis windows)"
+        cores = 1
+    elif args.config == 1:
+        m = synth.cfg1_map(seed=1, device="cpu").numpy()
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            ref.cfar2d(m, 2, 8, 1e-4)
+            times.append(time.perf_counter() - t0)
+        cells, what, cores = m.size, "the config-1 map, cfar2d_integral(threads=1)", 1
+    else:
+        rec = synth.cfg2_record(seed=2, device="cpu").double().numpy()
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            ref.detect(rec, fast_rate=39e9, prf=20.0, mean_filter_window=5, fft_length=1024, guard_radius=1,
+                       background_radius=4, pfa=1e-3)
+            times.append(time.perf_counter() - t0)
+        step = statistics.mean(times)
+        _line(impl="reference", metric="front end + CA-CFAR records/s (detect(), config 2)", value=1.0 / step,
+              unit="records/s", steps=args.steps, warmup=args.warmup, ms_per_step=step * 1e3,
+              config={"workload": "cfg2 record through uwbvital_ref::detect (FFTW-API shim)"},
+              cpu_baseline={"value": 1.0 / step, "unit": "records/s", "cores": 1, "kind": "reference",
+                            "sample": "one config-2 record per step"},
+              e2e={"value": 1.0 / step, "unit": "records/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
+        return 0
+    step = statistics.mean(times)
+    v = cells / step / 1e9
+    _line(impl="reference", metric=B.METRIC, value=v, unit=B.UNIT, steps=args.steps, warmup=args.warmup,
+          ms_per_step=step * 1e3, config={"workload": f"config {args.config}", "sample": what},
+          cpu_baseline={"value": v, "unit": B.UNIT, "cores": cores, "kind": "reference" if args.config != 5 else "port",
+                        "sample": what},
+          e2e={"value": v, "unit": B.UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
+    return 0
+
+
+def run(args):
+    if args.impl == "reference":
+        return run_reference_cfg(args)
+    return {4: run_cfg4, 5: run_cfg5, 1: run_cfg1, 2: run_cfg2}[args.config](args)
