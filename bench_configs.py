@@ -194,16 +194,19 @@ def run_cfg5(args):
     maps = torch.empty((m1 - m0, R, C), dtype=torch.float32, device="cuda")
     for blk in range(m0 // 8, m1 // 8):
         maps[blk * 8 - m0:(blk + 1) * 8 - m0] = synth.cfg5_maps(8, seed=5_000 + blk, device="cuda", rows=R, cols=C)
+    # the four runs share one workspace: the integral image of each map is built
+    # once per step and read by the four parameter sets (flags bit 2)
     runners = []
     for (gr, gc, br, bc), pfa in CFG5_RUNS:
         p = uwb.CfarParams(guard_radius=gr, background_radius=br, pfa=pfa, guard_cols=gc, background_cols=bc)
-        runners.append(BatchCfar(m1 - m0, R, C, p, torch.float32, det_capacity=1 << 15))
+        runners.append(BatchCfar(m1 - m0, R, C, p, torch.float32, det_capacity=1 << 15,
+                                 workspace=runners[0].workspace if runners else None))
     count = torch.zeros(1, dtype=torch.int64, device="cuda")
 
     def step(phase=False):
         count.zero_()
-        for rn in runners:
-            rn(maps, phase_events=phase)
+        for i, rn in enumerate(runners):
+            rn(maps, phase_events=phase, reuse_tables=i > 0)
             count.add_(rn.counts.sum())
         reduce_count(count)
 
@@ -217,6 +220,7 @@ def run_cfg5(args):
     launches = kernel_launches() - l0
     clocks = sampler.stop()
     ph = _phases(4 * (args.steps + max(args.warmup - 1, 0)))
+    ph["sat"] = ph.get("sat", 0.0) * 4  # the SAT phase is recorded by the first run only (others ~0)
     cells_local = (m1 - m0) * R * C
     peak, src = B._peaks()
 
@@ -260,7 +264,8 @@ def run_cfg5(args):
               warmup=args.warmup, ms_per_step=ms,
               config={"workload": "cfg5: 64 K-clutter fp32 maps 8192x2048 (Gamma(0.5) texture, 16x16 box, "
                                   "x Exp(1) speckle) + 64 clusters/map at U(10,25) dB; windows (g_r,g_c,b_r,b_c) "
-                                  "(1,3,4,16),(3,1,16,4) x Pfa 1e-3,1e-5; one step = the 4 runs",
+                                  "(1,3,4,16),(3,1,16,4) x Pfa 1e-3,1e-5; one step = the 4 runs (one SAT per "
+                                  "map, reused by the 4 parameter sets; the e2e leg runs 4 independent calls)",
                       "parallelism": f"dp{world} (maps sharded in 8-map blocks)",
                       "l2": "4 GiB input per run >> 126 MB L2", "detections_per_step": int(count.item())},
               roofline=_roof(ph, cells_local, peak, src), phases_ms=ph, cpu_baseline=cpu,

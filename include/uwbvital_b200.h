@@ -194,7 +194,12 @@ uint64_t uwb_dev_cfar2d_workspace(const uwb_map_batch* batch, const uwb_cfar_par
  * Parameters are validated on the host; input errors are reported per map in
  * outputs->first_bad (the call itself does not synchronise). alpha: device
  * array from uwb_alpha_table, length interior_train_count+1.
- * flags bit 0: skip the detection sort (list left in unspecified order). */
+ * flags bit 0: skip the detection sort (list left in unspecified order).
+ * flags bit 2: reuse the summed-area tables already in `workspace` from the
+ *   previous call on the same maps with the same table geometry (GLOBAL mode, or
+ *   SLAB mode with the same slab_rows and g_r + b_r): one table, several CFAR
+ *   parameter sets (the integral image's point). Non-finite inputs are reported
+ *   only by the call that built the tables. */
 uwb_status uwb_dev_cfar2d(const uwb_map_batch* batch, const uwb_cfar_params* params,
                           const double* alpha_dev, int32_t sat_mode, uint64_t slab_rows,
                           const uwb_cfar_outputs* out, void* workspace, uint64_t workspace_bytes,

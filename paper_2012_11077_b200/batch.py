@@ -25,7 +25,8 @@ class BatchCfar:
     def __init__(self, n_maps: int, rows: int, cols: int, params: CfarParams,
                  dtype: torch.dtype = torch.float32, sat_mode: str = "global", slab_rows: int = 0,
                  det_capacity: int = 1024, device=None, want_mask_u8: bool = False,
-                 want_thresholds: bool = False, window: tuple[int, int, int, int] | None = None):
+                 want_thresholds: bool = False, window: tuple[int, int, int, int] | None = None,
+                 workspace: torch.Tensor | None = None):
         """``window = (global_rows, buf_row0, row_begin, row_end)``: the maps passed
         to each call hold rows [buf_row0, buf_row0 + rows) of maps with
         ``global_rows`` rows and the call owns rows [row_begin, row_end) (one
@@ -64,16 +65,24 @@ class BatchCfar:
             ws = N.lib.uwb_dev_cfar2d_window_workspace(C.byref(self._batch), C.byref(self.window),
                                                        C.byref(self._cparams), C.c_uint64(self.slab_rows),
                                                        C.c_uint64(self.det_capacity))
-        self.workspace = torch.empty(int(ws), dtype=torch.uint8, device=dev)
+        if workspace is not None:  # shared with another BatchCfar (table reuse, see __call__)
+            if workspace.numel() < int(ws) or workspace.dtype != torch.uint8:
+                raise ValueError(f"workspace needs {int(ws)} bytes")
+            self.workspace = workspace
+        else:
+            self.workspace = torch.empty(int(ws), dtype=torch.uint8, device=dev)
         self._out = N.uwb_cfar_outputs(
             self.mask_bits.data_ptr(), self.words_per_row, out_rows * self.words_per_row,
             self.mask_u8.data_ptr() if self.mask_u8 is not None else None,
             self.thresholds.data_ptr() if self.thresholds is not None else None,
             self.dets.data_ptr(), self.det_capacity, self.counts.data_ptr(), self.first_bad.data_ptr())
 
-    def __call__(self, maps: torch.Tensor, sort: bool = True, stream=None, phase_events: bool = False) -> None:
+    def __call__(self, maps: torch.Tensor, sort: bool = True, stream=None, phase_events: bool = False,
+                 reuse_tables: bool = False) -> None:
         """Launch SAT + CFAR (+ sort) for ``maps`` of shape (n_maps, rows, cols).
-        ``phase_events`` records per-phase CUDA events (read with :func:`phase_ms`)."""
+        ``phase_events`` records per-phase CUDA events (read with :func:`phase_ms`).
+        ``reuse_tables`` skips the SAT: the (shared) workspace already holds the
+        tables of these maps from the previous call (another parameter set)."""
         if maps.dtype != self.dtype or tuple(maps.shape) != (self.n_maps, self.rows, self.cols):
             raise ValueError(f"expected {(self.n_maps, self.rows, self.cols)} {self.dtype}, got "
                              f"{tuple(maps.shape)} {maps.dtype}")
@@ -81,7 +90,7 @@ class BatchCfar:
             raise ValueError("maps must be a contiguous CUDA tensor")
         self._batch.maps = maps.data_ptr()
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
-        flags = (0 if sort else 1) | (2 if phase_events else 0)
+        flags = (0 if sort else 1) | (2 if phase_events else 0) | (4 if reuse_tables else 0)
         if self.window is None:
             st = N.lib.uwb_dev_cfar2d(C.byref(self._batch), C.byref(self._cparams), self.alpha.data_ptr(),
                                       self.sat_mode, C.c_uint64(self.slab_rows), C.byref(self._out),

@@ -301,8 +301,10 @@ uwb_status dev_cfar(const uwb_map_batch& b, const uwb_cfar_params& p, const doub
     if (o.first_bad) UWB_CUDA_TRY(cudaMemsetAsync(o.first_bad, 0xff, sizeof(uint64_t) * 2 * b.n_maps, s));
     if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[0], s));
     if (backend == UWB_INTEGRAL) {
-        const SatLaunch SL = sat_launch(P, b, ws, reinterpret_cast<unsigned long long*>(o.first_bad));
-        UWB_CUDA_TRY(run_sat(P, SL, b.dtype, s));
+        if (!(flags & 4u)) { // bit 2: the workspace already holds this batch's tables
+            const SatLaunch SL = sat_launch(P, b, ws, reinterpret_cast<unsigned long long*>(o.first_bad));
+            UWB_CUDA_TRY(run_sat(P, SL, b.dtype, s));
+        }
         if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[1], s));
         UWB_CUDA_TRY(launch_cfar_integral(cfar_launch(P, b, p, alpha, ws, o), b.dtype, s));
     } else {

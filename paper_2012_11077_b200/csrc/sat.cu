@@ -291,8 +291,11 @@ sat_systolic_kernel(SatLaunch L) {
         };
 
         // left-strip edge values, one block ahead (lane k: row s0 + k)
+        // (low-latency mode, for batches too small to fill the GPU: one block
+        // ahead and hand-overs every 32 steps, which shortens the strip chain)
+        const bool low_latency = (L.flags & 2u) != 0;
         double e_cur = fetch_left(0);
-        double e_next = fetch_left(kWarp);
+        double e_next = low_latency ? 0.0 : fetch_left(kWarp);
         cp_async_wait<kAhead - 1>();
         load_x(0u, x0n, x1n);
         for (int s0 = 0; s0 < steps; s0 += kWarp) {
@@ -301,8 +304,12 @@ sat_systolic_kernel(SatLaunch L) {
             asm volatile("st.shared.f64 [%0], %1;" ::"r"(edge_smem + 8u * lane), "d"(e_cur) : "memory");
             __syncwarp();
             edge_n = lds_d(edge_smem);
-            e_cur = e_next;
-            e_next = fetch_left(s0 + 2 * kWarp);
+            if (low_latency) {
+                e_cur = fetch_left(s0 + kWarp);
+            } else {
+                e_cur = e_next;
+                e_next = fetch_left(s0 + 2 * kWarp);
+            }
             // padded column 0 of the rows group 0 writes back in this block
             if (strip == 0 && s0 - 8 + lane >= 0 && s0 - 8 + lane < rows)
                 table[static_cast<int64_t>(s0 - 8 + lane + 1) * tld + kTabShift] = 0.0;
@@ -327,7 +334,8 @@ sat_systolic_kernel(SatLaunch L) {
             // hand over the edge rows stored so far (warp-uniform); a fast block
             // leaves its last row for the next block's paired store
             const int s_end = min(s0 + kWarp, steps);
-            if (prog_out && ((s_end & (kPublishEvery - 1)) == 0 || s_end == steps))
+            const int every = low_latency ? kWarp : kPublishEvery;
+            if (prog_out && ((s_end & (every - 1)) == 0 || s_end == steps))
                 publish_rows(prog_out, min(rows, s_end - (kWarp - 1) - (fast ? 1 : 0)), lane);
         }
         cp_async_wait<0>();
@@ -353,6 +361,8 @@ static cudaError_t launch_sat_t(const SatLaunch& L, cudaStream_t stream) {
     const int64_t ctas = (n_tiles + kWarpsPerCta - 1) / kWarpsPerCta;
     const int64_t grid = imin(ctas, static_cast<int64_t>(sms) * (per_sm > 0 ? per_sm : 1));
     SatLaunch L2 = L;
+    // batches that cannot fill the resident warps are latency-bound on the strip chain
+    if (n_tiles < 2LL * sms * (per_sm > 0 ? per_sm : 1) * kWarpsPerCta) L2.flags |= 2u;
     if (const char* f = getenv("UWB_SAT_FLAGS")) L2.flags = static_cast<unsigned>(atoi(f));
     ++g_kernel_launches;
     sat_systolic_kernel<T><<<static_cast<unsigned>(grid), kWarpsPerCta * kWarp, smem, stream>>>(L2);

@@ -202,3 +202,23 @@ def test_row_window_rejects_missing_halo(uwb, cuda):
     with pytest.raises(BoundsError):
         b = BatchCfar(1, 100, 64, p, torch.float32, window=(1000, 200, 200, 300))
         b(local)
+
+
+def test_reused_tables_match_fresh_call(uwb, oracle, cuda):
+    """flags bit 2: a second parameter set on the tables left in a shared
+    workspace gives exactly the outputs of a fresh call."""
+    from paper_2012_11077_b200 import synth
+    from paper_2012_11077_b200.batch import BatchCfar
+    maps = synth.cfg5_maps(2, seed=9, device=cuda, rows=600, cols=500)
+    pa = uwb.CfarParams(guard_radius=1, background_radius=4, pfa=1e-3, guard_cols=3, background_cols=16)
+    pb = uwb.CfarParams(guard_radius=3, background_radius=16, pfa=1e-5, guard_cols=1, background_cols=4)
+    a = BatchCfar(2, 600, 500, pa, torch.float32, det_capacity=8192, want_mask_u8=True, want_thresholds=True)
+    b = BatchCfar(2, 600, 500, pb, torch.float32, det_capacity=8192, want_mask_u8=True, want_thresholds=True,
+                  workspace=a.workspace)
+    a(maps)
+    b(maps, reuse_tables=True)
+    torch.cuda.synchronize()
+    host = maps.double().cpu().numpy()
+    for i in range(2):
+        _check_map(b, i, oracle.cfar(host[i], 3, 1, 16, 4, 1e-5), f"reused tables map {i}")
+        _check_map(a, i, oracle.cfar(host[i], 1, 3, 4, 16, 1e-3), f"first call map {i}")
