@@ -81,8 +81,21 @@ __device__ __forceinline__ void mbar_wait_susp(uint64_t* bar, unsigned parity, u
         "r"(parity), "r"(hint_ns)
         : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+// Same on shared-window addresses (no generic->shared conversion per use).
+template <unsigned kHintNs>
+__device__ __forceinline__ void mbar_wait_u(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "UWB_WAITU_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra UWB_WAITU_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity), "n"(kHintNs)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_u(unsigned bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 // 3-D tensor box -> L2 (no shared memory, no completion tracking).
 __device__ __forceinline__ void tma_prefetch3(const CUtensorMap* map, int x, int y, int z) {
@@ -326,6 +339,11 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
     // ring slots of the (unclamped) tap rows of output row r0, advanced 4 rows per step
     auto slot0 = [&](int i) { return ((i - i_lo) % G.nr + G.nr) % G.nr; };
     int sA = slot0(ra - hr), sB = slot0(ra + hr + 1), sC = slot0(ra - gr), sD = slot0(ra + gr + 1);
+    constexpr unsigned kHint = 20000; // ns a waiting consumer may sleep in the barrier unit
+    const unsigned full_t_u = smem_u32(full_t), full_c_u = smem_u32(full_c);
+    const unsigned empty_t_u = smem_u32(empty_t), empty_c_u = smem_u32(empty_c);
+    // table groups needed through step s: min(last, need_base + s) in the interior
+    const int last_grp_c = (i_hi - i_lo) / kG;
     int waited = -1, wslot = 0, wphase = 0; // full_t groups known resident
     int released = -1, rslot = 0;            // table groups handed back
     int cslot = 0, cphase = 0;
@@ -342,9 +360,9 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
         const int r0 = ra + step * RS;
         const int r_last = min(r0 + RS, rb) - 1;
         {
-            const int need = (clamp_hi32(r_last, hr, rows) + 1 - i_lo) / kG;
+            const int need = min(last_grp_c, (min(r_last + hr, rows - 1) + 1 - i_lo) / kG);
             while (waited < need) {
-                mbar_wait_susp(&full_t[wslot], static_cast<unsigned>(wphase), L.sleep_ns);
+                mbar_wait_u<kHint>(full_t_u + 8u * wslot, static_cast<unsigned>(wphase));
                 ++waited;
                 if (++wslot == G.ng) { wslot = 0; wphase ^= 1; }
             }
@@ -352,7 +370,7 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
 #pragma unroll
         for (int q = 0; q < SG; ++q)
             if (q == 0 || r0 + q * kG <= r_last)
-                mbar_wait_susp(&full_c[cslot + q], static_cast<unsigned>(cphase), L.sleep_ns);
+                mbar_wait_u<kHint>(full_c_u + 8u * (cslot + q), static_cast<unsigned>(cphase));
         const T* cut_grp = cuts + static_cast<size_t>(cslot) * kG * kW;
         double v[RS][CPT], thr[RS][CPT];
         bool hit[RS][CPT];
@@ -482,13 +500,13 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
         if (lane == 0) {
 #pragma unroll
             for (int q = 0; q < SG; ++q)
-                if (q == 0 || r0 + q * kG <= r_last) mbar_arrive(&empty_c[cslot + q]);
+                if (q == 0 || r0 + q * kG <= r_last) mbar_arrive_u(empty_c_u + 8u * (cslot + q));
             if (step + 1 < n_steps) {
                 const int keep_row = max(0, r_last + 1 - hr);
                 const int done = (keep_row - i_lo) / kG - 1; // groups entirely below keep_row
                 while (released < done) {
                     ++released;
-                    mbar_arrive(&empty_t[rslot]);
+                    mbar_arrive_u(empty_t_u + 8u * rslot);
                     if (++rslot == G.ng) rslot = 0;
                 }
             }

@@ -6,6 +6,4 @@ run() {
   env "$@" timeout -s KILL 300 python bench.py --maps $MAPS --steps 5 --warmup 3 --no-e2e --no-cpu-baseline 2>&1 | tail -1 | \
     python -c "import sys,json; d=json.loads(sys.stdin.read()); print(round(d['value'],2), round(d['ms_per_step'],3), {k: round(v,3) for k,v in d['phases_ms'].items()})" 2>&1 | tail -1
 }
-run UWB_RING_SLEEP_NS=20000
-run UWB_RING_SLEEP_NS=0
-run UWB_RING_SLEEP_NS=500
+run UWB_X=0
