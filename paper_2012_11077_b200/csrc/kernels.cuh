@@ -80,7 +80,7 @@ struct SatLaunch {
     unsigned long long* first_bad; // per map 2 slots; slot 0 = first non-finite
     bool vec_ok;         // 16-byte vector loads legal
     int elem_bytes;
-    unsigned flags;      // bit 0: L2 prefetch of source rows (probe, off); bit 1: low-latency strip chain
+    unsigned flags;      // bit 1: low-latency strip chain (set by the launcher)
 };
 
 struct SatJobView {

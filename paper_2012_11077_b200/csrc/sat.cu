@@ -7,21 +7,20 @@
 // that respects those dependencies and performs the same three IEEE additions
 // reproduces the reference table bit for bit. This kernel runs the recurrence
 // as a systolic wavefront:
-//   * the unit of work is one warp on a 64-column strip of one table; lane l
-//     owns columns 2l and 2l+1 and handles row r = s - l at step s, so the
-//     warp sweeps an anti-diagonal band down the whole strip. Warps are
-//     independent (no CTA barrier). Per step a lane does 6 dependent-pair
-//     additions; S(r, 2l-1) comes from lane l-1 by a register shuffle of the
-//     value it produced one step earlier, and lane 0 takes it from the edge
-//     column of the strip to the left, fetched 32 rows at a time;
-//   * lanes form 4 groups of 8. Group g stages, with 8-byte cp.async per lane,
-//     the row its lanes need kAhead..kAhead+7 steps later (one 64-byte
+//   * the unit of work is one warp on a 128-column strip of one table; lane l
+//     owns columns 4l..4l+3 and handles row r = s - l at step s, so the warp
+//     sweeps an anti-diagonal band down the whole strip. Warps are
+//     independent (no CTA barrier). Per step a lane evaluates its 4 cells left
+//     to right (12 additions); S(r, 4l-1) comes from lane l-1 by a register
+//     shuffle of the value it produced one step earlier, and lane 0 takes it
+//     from the edge column of the strip to the left, fetched 32 rows at a time;
+//   * lanes form 4 groups of 8. Group g stages, with 16-byte cp.async per lane,
+//     the row its lanes need kAhead..kAhead+7 steps later (one 128-byte
 //     segment per group and step) into lane-private slots of a 16-step ring
 //     (slot = copy step mod 16), so no lane ever reads data another lane
-//     copied (optionally, flags bit 0, lane 0 also prefetches the strip's row
-//     kPrefetch steps ahead into L2; measured slower on B200). Results go through a
-//     lane-private 8-row delay ring; group g writes back row s - 8g - 7, so each
-//     group stores one whole 128-byte line of the table per step;
+//     copied. Results go through a lane-private 8-row delay ring; group g
+//     writes back row s - 8g - 8, so each group stores two whole 128-byte lines
+//     of the table per step;
 //   * all ring slots used inside the 32-step unrolled block are compile-time
 //     offsets or one ADD/AND away from a per-lane base;
 //   * strips are claimed from an atomic counter in strip-major order, so the
@@ -45,33 +44,43 @@ namespace uwb {
 
 namespace {
 
-constexpr int kStripCols = 2 * kWarp;   // 64 columns per unit of work
+constexpr int kCpl = 4;                 // columns per lane
+constexpr int kStripCols = kCpl * kWarp; // 128 columns per unit of work
 constexpr int kWarpsPerCta = 4;         // independent warps per CTA
 constexpr int kAhead = 8;               // staging distance in steps (<= kXSlots - 8)
 constexpr int kXSlots = 16;             // lane-private source ring (copy steps)
-constexpr int kPrefetch = 64;           // L2 prefetch distance (rows)
 constexpr int kOSlots = 8;              // lane-private result delay ring (rows)
 constexpr int kPublishEvery = 64;       // steps between edge hand-overs
-constexpr int kSatCtasPerSm = 4;        // occupancy target (registers: 128 per thread)
+constexpr int kSatCtasPerSm = 3;        // occupancy target (registers and shared memory)
 
 // Shared memory per CTA: the warps' source rings, the result rings and the
 // edge staging.
 template <typename T>
 struct SatSmem {
-    static constexpr unsigned kXSlotBytes = kWarp * 2 * sizeof(T);
+    static constexpr unsigned kXLane = kCpl * sizeof(T);              // source bytes per lane and row
+    static constexpr unsigned kXSlotBytes = kWarp * kXLane;
     static constexpr unsigned kXRing = kXSlots * kXSlotBytes;        // 8 KB (f32) / 16 KB (f64)
-    static constexpr unsigned kOSlotBytes = kWarp * 2 * sizeof(double);
-    static constexpr unsigned kORing = kOSlots * kOSlotBytes;        // 4 KB
+    static constexpr unsigned kOLane = kCpl * sizeof(double);
+    static constexpr unsigned kOSlotBytes = kWarp * kOLane;
+    static constexpr unsigned kORing = kOSlots * kOSlotBytes;        // 8 KB
     static constexpr size_t bytes() {
         return 16 /* alignment slack */ + kWarpsPerCta * (kXRing + kORing + kWarp * sizeof(double));
     }
 };
 
-__device__ __forceinline__ void cp_async_pair(unsigned dst, const float* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_pair(unsigned dst, const double* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+// cp.async of a lane's kCpl source values (16-byte pieces; 8 bytes when that is all)
+template <typename T>
+__device__ __forceinline__ void cp_async_lane(unsigned dst, const T* src) {
+    constexpr unsigned kBytes = kCpl * sizeof(T);
+    if constexpr (kBytes == 8) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+    } else {
+#pragma unroll
+        for (unsigned q = 0; q < kBytes / 16; ++q)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * q),
+                         "l"(reinterpret_cast<const char*>(src) + 16u * q)
+                         : "memory");
+    }
 }
 __device__ __forceinline__ void cp_async_one(unsigned dst, const float* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
@@ -79,17 +88,33 @@ __device__ __forceinline__ void cp_async_one(unsigned dst, const float* src) {
 __device__ __forceinline__ void cp_async_one(unsigned dst, const double* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
 }
-__device__ __forceinline__ void lds_pair(unsigned addr, float& a, float& b) {
-    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(a), "=f"(b) : "r"(addr));
+__device__ __forceinline__ void lds_lane(unsigned addr, float (&x)[kCpl]) {
+    if constexpr (kCpl == 4) {
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3])
+                     : "r"(addr));
+    } else {
+#pragma unroll
+        for (int q = 0; q < kCpl / 2; ++q)
+            asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(x[2 * q]), "=f"(x[2 * q + 1]) : "r"(addr + 8u * q));
+    }
 }
-__device__ __forceinline__ void lds_pair(unsigned addr, double& a, double& b) {
-    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "r"(addr));
+__device__ __forceinline__ void lds_lane(unsigned addr, double (&x)[kCpl]) {
+#pragma unroll
+    for (int q = 0; q < kCpl / 2; ++q)
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x[2 * q]), "=d"(x[2 * q + 1]) : "r"(addr + 16u * q));
 }
-__device__ __forceinline__ void sts_pair(unsigned addr, double a, double b) {
-    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(a), "d"(b) : "memory");
+__device__ __forceinline__ void sts_out(unsigned addr, const double (&v)[kCpl]) {
+#pragma unroll
+    for (int q = 0; q < kCpl / 2; ++q)
+        asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr + 16u * q), "d"(v[2 * q]), "d"(v[2 * q + 1])
+                     : "memory");
 }
-__device__ __forceinline__ void lds_dpair(unsigned addr, double& a, double& b) {
-    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "r"(addr) : "memory");
+__device__ __forceinline__ void lds_out(unsigned addr, double (&v)[kCpl]) {
+#pragma unroll
+    for (int q = 0; q < kCpl / 2; ++q)
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[2 * q]), "=d"(v[2 * q + 1]) : "r"(addr + 16u * q)
+                     : "memory");
 }
 __device__ __forceinline__ double lds_d(unsigned addr) {
     double v;
@@ -103,12 +128,15 @@ __device__ __noinline__ void publish_rows(unsigned* prog, int rows_done, int lan
     __syncwarp();
 }
 
-// First non-finite row of columns [c, c + n) in source rows [0, rows_end).
+// First non-finite cell (row-major) of columns [c, c + n) in source rows [0, rows_end).
 template <typename T>
-__device__ __noinline__ int first_nonfinite_row(const T* src, int64_t ld, int c, int n, int rows_end) {
+__device__ __noinline__ int first_nonfinite(const T* src, int64_t ld, int c, int n, int rows_end, int* col) {
     for (int r = 0; r < rows_end; ++r)
         for (int k = 0; k < n; ++k)
-            if (!isfinite(widen(src[static_cast<int64_t>(r) * ld + c + k]))) return r;
+            if (!isfinite(widen(src[static_cast<int64_t>(r) * ld + c + k]))) {
+                *col = c + k;
+                return r;
+            }
     return INT_MAX;
 }
 
@@ -124,8 +152,8 @@ sat_systolic_kernel(SatLaunch L) {
     const int grp = lane >> 3; // lane group: stages and flushes together
     const unsigned raw = smem_u32(sat_smem_raw);
     const unsigned base = (raw + 15u) & ~15u;
-    const unsigned x_lane = base + warp * SM::kXRing + lane * 2 * sizeof(T); // slot 0, my pair
-    const unsigned o_lane = base + kWarpsPerCta * SM::kXRing + warp * SM::kORing + lane * 2 * sizeof(double);
+    const unsigned x_lane = base + warp * SM::kXRing + lane * SM::kXLane; // slot 0, my columns
+    const unsigned o_lane = base + kWarpsPerCta * SM::kXRing + warp * SM::kORing + lane * SM::kOLane;
     const unsigned edge_smem = base + kWarpsPerCta * (SM::kXRing + SM::kORing) + warp * kWarp * sizeof(double);
     const int64_t n_tiles = L.n_jobs * L.strips;
     const int cols = static_cast<int>(L.cols);
@@ -141,15 +169,14 @@ sat_systolic_kernel(SatLaunch L) {
         const int64_t job = tile % L.n_jobs;
         const SatJobView J = sat_job(L, job);
         const int rows = static_cast<int>(J.rows);
-        const int c = strip * kStripCols + 2 * lane;     // my first column
-        const int nvalid = max(0, min(2, cols - c));     // my columns inside the map
+        const int c = strip * kStripCols + kCpl * lane;   // my first column
+        const int nvalid = max(0, min(kCpl, cols - c));    // my columns inside the map
         double* table = J.table;
         const int64_t tld = L.table_ld;
         const int64_t ld = L.ld;
         const T* src = static_cast<const T*>(J.src);
 
-        if (nvalid > 0) table[kTabShift + 1 + c] = 0.0; // padded row 0 is identically zero
-        if (nvalid > 1) table[kTabShift + 2 + c] = 0.0;
+        for (int k = 0; k < nvalid; ++k) table[kTabShift + 1 + c + k] = 0.0; // padded row 0 is zero
         if (strip == 0 && lane == 0) table[kTabShift] = 0.0;
 
         const unsigned* prog_in = strip > 0 ? L.gprog + job * L.strips + strip - 1 : nullptr;
@@ -159,7 +186,7 @@ sat_systolic_kernel(SatLaunch L) {
         const double* ge_in = prog_in ? L.gedge + (job * L.strips + strip - 1) * L.edge_stride : nullptr;
         double* ge_out = prog_out ? L.gedge + (job * L.strips + strip) * L.edge_stride : nullptr;
         unsigned avail = 0;
-        // left-strip edge for rows [base, base+32) -> edge_smem (lane k: row base + k)
+        // left-strip edge for rows [base, base+32) (lane k: row base + k)
         auto fetch_left = [&](int base) {
             double v = 0.0;
             if (prog_in && base < rows) { // warp-uniform
@@ -174,33 +201,22 @@ sat_systolic_kernel(SatLaunch L) {
             return v;
         };
 
-        // L2 prefetch of the strip's row segment, kPrefetch rows ahead (lane 0)
-        const unsigned pf_bytes = static_cast<unsigned>(min(kStripCols, cols - strip * kStripCols)) * sizeof(T);
-        const unsigned pf_bytes16 = (pf_bytes + 15u) & ~15u;
-        const T* pfrow = src + strip * kStripCols + static_cast<int64_t>(kPrefetch) * ld;
-        const bool pf_aligned = (L.flags & 1u) && (reinterpret_cast<uintptr_t>(src) % 16) == 0 && (ld * sizeof(T)) % 16 == 0;
-        if (lane == 0 && pf_aligned)
-            for (int r = 0; r < min(rows, kPrefetch); ++r)
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + strip * kStripCols +
-                                                                                   static_cast<int64_t>(r) * ld),
-                             "r"(pf_bytes16)
-                             : "memory");
         // staging: group g copies, at step s, source row s + kAhead - 8g
-        const bool pair_ok = nvalid == 2 && (reinterpret_cast<uintptr_t>(src) % (2 * sizeof(T))) == 0 &&
-                             (ld % 2) == 0;
-        const bool warp_fast = __all_sync(0xffffffffu, pair_ok);
+        constexpr unsigned kVecAlign = SM::kXLane >= 16 ? 16 : SM::kXLane;
+        const bool vec_ok = nvalid == kCpl && (reinterpret_cast<uintptr_t>(src + c) % kVecAlign) == 0 &&
+                            ((ld * sizeof(T)) % kVecAlign) == 0;
+        const bool warp_fast = __all_sync(0xffffffffu, vec_ok);
         const T* xrow = src + c + static_cast<int64_t>(kAhead - 8 * grp) * ld; // row staged at step 0
-        // a copy issued at step s lands in slot s mod 32
+        // a copy issued at step s lands in slot s mod 16
         auto stage = [&](unsigned slot_off, int row, const T* p, bool checked) {
             const unsigned dst = x_lane + slot_off;
             if (!checked) {
-                cp_async_pair(dst, p);
+                cp_async_lane<T>(dst, p);
             } else if (row >= 0 && row < rows) {
                 if (warp_fast) {
-                    cp_async_pair(dst, p);
+                    cp_async_lane<T>(dst, p);
                 } else {
-                    if (nvalid > 0) cp_async_one(dst, p);
-                    if (nvalid > 1) cp_async_one(dst + sizeof(T), p + 1);
+                    for (int k = 0; k < nvalid; ++k) cp_async_one(dst + k * sizeof(T), p + k);
                 }
             }
         };
@@ -213,23 +229,20 @@ sat_systolic_kernel(SatLaunch L) {
             cp_async_commit();
         }
 
-        double prev0 = 0.0, prev1 = 0.0; // S(r-1, c), S(r-1, c+1)
-        double left_prev = 0.0;          // S(r-1, c-1)
-        double last1 = 0.0;              // S(r, c+1), shuffled right next step
-        double last0 = 0.0;
-        bool scanned = false;            // non-finite rescan done
-        // flush pointer: table row rf + 1 for rf = s - 8g - 8 (my pair)
+        double prev[kCpl];       // S(r-1, c + k)
+        double last[kCpl];       // S(r, c + k), newest; last[kCpl-1] is shuffled right
+#pragma unroll
+        for (int k = 0; k < kCpl; ++k) prev[k] = last[k] = 0.0;
+        double left_prev = 0.0;  // S(r-1, c-1)
+        bool scanned = false;    // non-finite rescan done
+        // write-back pointer: table row rf + 1 for rf = s - 8g - 8 (my columns)
         double* tflush = table + static_cast<int64_t>(1 - 8 * grp - 8) * tld + kTabShift + 1 + c;
         const int steps = rows + kWarp;
         // lane l needs at step s the row copied at step s - kAhead - (l mod 8)
         const unsigned x_rbase_lane = static_cast<unsigned>(2 * kXSlots - kAhead - (lane & 7));
         const unsigned o_rbase_lane = static_cast<unsigned>(kWarp - lane); // (u - l) mod 8
-        const bool pf_ok_lane = lane == 0 && pf_aligned;
         const bool edge_lane = lane == kWarp - 1 && ge_out != nullptr;
-        auto load_x = [&](unsigned u, T& a, T& b) {
-            lds_pair(x_lane + ((u + x_rbase_lane) & (kXSlots - 1)) * kXSlotBytes, a, b);
-        };
-        T x0n, x1n; // source pair of the next step (loaded one step ahead)
+        T xn[kCpl];          // source values of the next step (loaded one step ahead)
         double edge_n = 0.0; // lane 0: left strip's edge for the next step
 
         // One systolic step. kChecked: range checks on rows (prologue/epilogue blocks).
@@ -240,12 +253,16 @@ sat_systolic_kernel(SatLaunch L) {
             // (1) group g writes back row s - 8g - 8 (slot u mod 8, stored >= 1 step ago)
             const int rf = s - 8 * grp - 8;
             if (!kChecked || (rf >= 0 && rf < rows)) {
-                double a, b;
-                lds_dpair(o_lane + static_cast<unsigned>(u & (kOSlots - 1)) * kOSlotBytes, a, b);
-                if (!kChecked || nvalid == 2) {
-                    *reinterpret_cast<double2*>(tflush) = make_double2(a, b);
-                } else if (nvalid == 1) {
-                    *tflush = a;
+                double o[kCpl];
+                lds_out(o_lane + static_cast<unsigned>(u & (kOSlots - 1)) * kOSlotBytes, o);
+                if (!kChecked || nvalid == kCpl) {
+#pragma unroll
+                    for (int q = 0; q < kCpl / 2; ++q)
+                        reinterpret_cast<double2*>(tflush)[q] = make_double2(o[2 * q], o[2 * q + 1]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < kCpl; ++k)
+                        if (k < nvalid) tflush[k] = o[k];
                 }
             }
             tflush += tld;
@@ -253,40 +270,37 @@ sat_systolic_kernel(SatLaunch L) {
             stage(static_cast<unsigned>((u & (kXSlots - 1)) * kXSlotBytes), s + kAhead - 8 * grp, xrow, kChecked);
             cp_async_commit();
             xrow += ld;
-            if (pf_ok_lane && (!kChecked || s + kPrefetch < rows))
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pfrow), "r"(pf_bytes16) : "memory");
-            pfrow += ld;
             // (3) this step's inputs were loaded one step ahead; load the next step's
-            const T x0 = x0n, x1 = x1n;
+            T x[kCpl];
+#pragma unroll
+            for (int k = 0; k < kCpl; ++k) x[k] = xn[k];
             const double from_left_strip = edge_n;
             cp_async_wait<kAhead - 1>();
-            load_x(static_cast<unsigned>(u + 1), x0n, x1n);
+            lds_lane(x_lane + ((static_cast<unsigned>(u + 1) + x_rbase_lane) & (kXSlots - 1)) * kXSlotBytes, xn);
             if (u + 1 < kWarp) edge_n = lds_d(edge_smem + static_cast<unsigned>(u + 1) * 8u);
-            // (4) left neighbour S(r, c-1): lane l-1's newest S(., c+1); lane 0: left strip's edge
-            double left = __shfl_up_sync(0xffffffffu, last1, 1);
+            // (4) left neighbour S(r, c-1): lane l-1's newest S(., c+kCpl-1); lane 0: left strip's edge
+            double left = __shfl_up_sync(0xffffffffu, last[kCpl - 1], 1);
             if (lane == 0) left = from_left_strip;
-            // (5) sat.cpp:33, twice: out[c+1] = v + above[c+1] + out[c] - above[c]
-            const double v0 = widen(x0), v1 = widen(x1);
-            const double s0v = dsub(dadd(dadd(v0, prev0), left), left_prev);
-            const double s1v = dsub(dadd(dadd(v1, prev1), s0v), prev0);
+            // (5) sat.cpp:33 for each of my columns: out[c+1] = v + above[c+1] + out[c] - above[c]
+            double sv[kCpl];
+            sv[0] = dsub(dadd(dadd(widen(x[0]), prev[0]), left), left_prev);
+#pragma unroll
+            for (int k = 1; k < kCpl; ++k) sv[k] = dsub(dadd(dadd(widen(x[k]), prev[k]), sv[k - 1]), prev[k - 1]);
             const bool act = !kChecked || (r >= 0 && r < rows);
             if (act) {
                 // (6) edge column for the strip to the right (two rows per 16-byte store)
                 if (edge_lane) {
                     if (kChecked) {
-                        ge_out[r] = s1v;
-                        if (u == 0 && r >= 1) ge_out[r - 1] = prev1; // row a fast block left unstored
+                        ge_out[r] = sv[kCpl - 1];
+                        if (u == 0 && r >= 1) ge_out[r - 1] = prev[kCpl - 1]; // row a fast block left unstored
+                    } else if ((u & 1) == 0) { // r = s - 31 is odd
+                        *reinterpret_cast<double2*>(ge_out + r - 1) = make_double2(prev[kCpl - 1], sv[kCpl - 1]);
                     }
-                    else if ((u & 1) == 0) // r = s - 31 is odd
-                        *reinterpret_cast<double2*>(ge_out + r - 1) = make_double2(prev1, s1v);
                 }
                 left_prev = left;
-                prev0 = s0v;
-                prev1 = s1v;
-                last0 = s0v;
-                last1 = s1v;
-                sts_pair(o_lane + ((static_cast<unsigned>(u) + o_rbase_lane) & (kOSlots - 1)) * kOSlotBytes, s0v,
-                         s1v);
+#pragma unroll
+                for (int k = 0; k < kCpl; ++k) prev[k] = last[k] = sv[k];
+                sts_out(o_lane + ((static_cast<unsigned>(u) + o_rbase_lane) & (kOSlots - 1)) * kOSlotBytes, sv);
             }
         };
 
@@ -297,7 +311,7 @@ sat_systolic_kernel(SatLaunch L) {
         double e_cur = fetch_left(0);
         double e_next = low_latency ? 0.0 : fetch_left(kWarp);
         cp_async_wait<kAhead - 1>();
-        load_x(0u, x0n, x1n);
+        lds_lane(x_lane + (x_rbase_lane & (kXSlots - 1)) * kXSlotBytes, xn);
         for (int s0 = 0; s0 < steps; s0 += kWarp) {
             // left-strip edge values for rows [s0, s0 + 32) (lane 0 reads row s at step s)
             __syncwarp();
@@ -322,14 +336,15 @@ sat_systolic_kernel(SatLaunch L) {
                 for (int u = 0; u < kWarp && s0 + u < steps; ++u) step(s0, u, std::true_type{});
             }
             // non-finite inputs poison every later S of their column (see header)
-            if (!scanned && nvalid > 0 && !(isfinite(last0) && (nvalid < 2 || isfinite(last1)))) {
+            bool finite = true;
+#pragma unroll
+            for (int k = 0; k < kCpl; ++k) finite &= k >= nvalid || isfinite(last[k]);
+            if (!scanned && nvalid > 0 && !finite) {
                 scanned = true;
-                const int row_end = min(rows, s0 + kWarp);
-                const int bad = first_nonfinite_row<T>(src, ld, c, nvalid, row_end);
-                if (bad != INT_MAX) {
-                    const int k = isfinite(widen(src[static_cast<int64_t>(bad) * ld + c])) ? 1 : 0;
-                    report_min(J.nonfinite, static_cast<unsigned long long>((J.row0 + bad) * L.cols + c + k));
-                }
+                int col = c;
+                const int bad = first_nonfinite<T>(src, ld, c, nvalid, min(rows, s0 + kWarp), &col);
+                if (bad != INT_MAX)
+                    report_min(J.nonfinite, static_cast<unsigned long long>((J.row0 + bad) * L.cols + col));
             }
             // hand over the edge rows stored so far (warp-uniform); a fast block
             // leaves its last row for the next block's paired store
