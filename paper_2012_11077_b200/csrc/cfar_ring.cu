@@ -41,10 +41,11 @@ namespace {
 constexpr int kRingRows = 256;  // output rows per CTA
 constexpr int kG = 4;           // rows per group (output step, TMA box height)
 constexpr int kW = 128;         // output columns per CTA
-constexpr int kTableAhead = 1;  // table groups of look-ahead beyond the window
-constexpr int kCutGroups = 4;   // CUT ring depth (groups)
+// Occupancy profiles (CTAs per SM): the shared memory left after the resident
+// window goes to look-ahead (table groups beyond the window, CUT ring depth).
+__host__ __device__ constexpr int occ_ahead(int occ) { return occ >= 4 ? 1 : occ == 3 ? 4 : 10; }
+__host__ __device__ constexpr int occ_cut(int occ) { return occ >= 4 ? 4 : occ == 3 ? 6 : 8; }
 constexpr int kPfGroups = 6;    // L2 prefetch distance of both streams (groups)
-constexpr int kCtasPerSm = 4;   // occupancy target at 4-row steps (registers and shared memory)
 
 struct RingGeom {
     int ng;     // table row groups in the ring
@@ -52,18 +53,19 @@ struct RingGeom {
 };
 
 // sg = groups per consumer step (rows per step rs = 4 sg)
-__host__ __device__ inline RingGeom ring_geom(int hr, int sg) {
+__host__ __device__ inline RingGeom ring_geom(int hr, int sg, int ahead) {
     RingGeom g;
     // output rows r..r+rs-1 read table rows r-hr .. r+rs+hr: 2hr+rs+1 rows,
     // spread over at most ceil((2hr+rs+1)/4)+1 groups
-    g.ng = (2 * hr + kG * sg + 1 + kG - 1) / kG + 1 + kTableAhead;
+    g.ng = (2 * hr + kG * sg + 1 + kG - 1) / kG + 1 + ahead;
     g.nr = g.ng * kG;
     return g;
 }
 
 template <typename T>
-inline size_t ring_smem_bytes(int hr, int boxc, int sg) {
-    const RingGeom g = ring_geom(hr, sg);
+inline size_t ring_smem_bytes(int hr, int boxc, int sg, int occ) {
+    const int kCutGroups = occ_cut(occ);
+    const RingGeom g = ring_geom(hr, sg, occ_ahead(occ));
     return 128 /* alignment slack */ + sizeof(double) * static_cast<size_t>(g.nr + kG * sg) * boxc +
            sizeof(T) * static_cast<size_t>(kCutGroups) * kG * kW + 2 * sizeof(uint64_t) * (g.ng + kCutGroups);
 }
@@ -212,11 +214,12 @@ __device__ __forceinline__ void emit_block(const CfarLaunch& L, int64_t map, int
 
 // NCW consumer warps x CPT columns per thread = kW columns; BOXC = ring row
 // width in doubles (the table box width, >= kW + 2 hc + 4, multiple of 4).
-template <typename T, int NCW, int CPT, int BOXC, int SG>
-__global__ void __launch_bounds__((NCW + 1) * kWarp, SG == 1 ? kCtasPerSm : kCtasPerSm - 1)
+template <typename T, int NCW, int CPT, int BOXC, int SG, int OCC>
+__global__ void __launch_bounds__((NCW + 1) * kWarp, OCC)
 cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUtensorMap tmap_tab,
                const __grid_constant__ CUtensorMap tmap_cut) {
     static_assert(NCW * CPT * kWarp == kW, "tile width");
+    constexpr int kCutGroups = occ_cut(OCC);
     static_assert(kCutGroups % SG == 0, "CUT ring depth");
     constexpr int RS = kG * SG; // output rows per consumer step
     constexpr unsigned kRowBytes = 8u * BOXC;
@@ -225,7 +228,7 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
     extern __shared__ unsigned char ring_raw[];
     unsigned char* ring_smem =
         ring_raw + ((128u - (static_cast<unsigned>(__cvta_generic_to_shared(ring_raw)) & 127u)) & 127u);
-    const RingGeom G = ring_geom(L.hr, SG);
+    const RingGeom G = ring_geom(L.hr, SG, occ_ahead(OCC));
     double* slots = reinterpret_cast<double*>(ring_smem);
     const char* ring = reinterpret_cast<const char*>(ring_smem);
     T* cuts = reinterpret_cast<T*>(slots + static_cast<size_t>(G.nr + RS) * BOXC);
@@ -271,6 +274,8 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
 
     if (warp == NCW) {
         // =========================== producer thread ===========================
+        // compute-only probe (debug bit 1): fill each ring once, consumers then
+        // recompute on the resident (valid, stale) rows without waiting
         if (lane != 0) return;
         const int last_grp = (i_hi - i_lo) / kG;
         for (int g = 0; g <= min(last_grp, kPfGroups - 1); ++g)
@@ -283,9 +288,11 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
         // Issue order: always the load the consumers need first; block (suspended)
         // only on that load's ring slot. Table group grp is first read at step
         // (i_lo + 4 grp - ra - hr - 1) / RS, CUT group cstep at step cstep / SG.
-        while (grp <= last_grp || cstep < n_cg) {
-            const int need_tab = grp <= last_grp ? max(0, (i_lo + kG * grp - ra - hr - 1)) / RS : INT_MAX;
-            const int need_cut = cstep < n_cg ? cstep / SG : INT_MAX;
+        const bool once = (L.debug & 2u) != 0;
+        while ((grp <= last_grp && !(once && grp >= G.ng)) || (cstep < n_cg && !(once && cstep >= kCutGroups))) {
+            const int need_tab =
+                grp <= last_grp && !(once && grp >= G.ng) ? max(0, (i_lo + kG * grp - ra - hr - 1)) / RS : INT_MAX;
+            const int need_cut = cstep < n_cg && !(once && cstep >= kCutGroups) ? cstep / SG : INT_MAX;
             if (need_tab <= need_cut) {
                 if (grp >= G.ng) mbar_wait_susp(&empty_t[gslot], static_cast<unsigned>(gphase ^ 1), L.sleep_ns);
                 const int first = i_lo + grp * kG;
@@ -362,14 +369,15 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
         {
             const int need = min(last_grp_c, (min(r_last + hr, rows - 1) + 1 - i_lo) / kG);
             while (waited < need) {
-                mbar_wait_u<kHint>(full_t_u + 8u * wslot, static_cast<unsigned>(wphase));
+                if (!(L.debug & 2u) || waited < G.ng - 1)
+                    mbar_wait_u<kHint>(full_t_u + 8u * wslot, static_cast<unsigned>(wphase));
                 ++waited;
                 if (++wslot == G.ng) { wslot = 0; wphase ^= 1; }
             }
         }
 #pragma unroll
         for (int q = 0; q < SG; ++q)
-            if (q == 0 || r0 + q * kG <= r_last)
+            if ((q == 0 || r0 + q * kG <= r_last) && (!(L.debug & 2u) || step < kCutGroups))
                 mbar_wait_u<kHint>(full_c_u + 8u * (cslot + q), static_cast<unsigned>(cphase));
         const T* cut_grp = cuts + static_cast<size_t>(cslot) * kG * kW;
         double v[RS][CPT], thr[RS][CPT];
@@ -548,7 +556,7 @@ bool encode3(CUtensorMap* m, CUtensorMapDataType dt, size_t esz, const void* bas
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <typename T, int NCW, int CPT, int BOXC, int SG>
+template <typename T, int NCW, int CPT, int BOXC, int SG, int OCC>
 cudaError_t go(const CfarLaunch& L0, cudaStream_t stream) {
     CfarLaunch L = L0;
     L.sleep_ns = 20000;
@@ -568,23 +576,37 @@ cudaError_t go(const CfarLaunch& L0, cudaStream_t stream) {
     if (!encode3(&tmap_cut, sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
                  sizeof(T), L.maps, L.cols, L.geo.buf_rows, n_maps, L.ld, mstride, kW, kG))
         return cudaErrorNotSupported;
-    const size_t smem = ring_smem_bytes<T>(L.hr, BOXC, SG);
+    const size_t smem = ring_smem_bytes<T>(L.hr, BOXC, SG, OCC);
     if (smem > 227 * 1024) return cudaErrorNotSupported;
     const dim3 grid(static_cast<unsigned>(L.col_tiles * L.row_chunks), static_cast<unsigned>(L.n_jobs), 1);
-    cudaError_t e = cudaFuncSetAttribute(cfar_ws_kernel<T, NCW, CPT, BOXC, SG>,
+    cudaError_t e = cudaFuncSetAttribute(cfar_ws_kernel<T, NCW, CPT, BOXC, SG, OCC>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     ++g_kernel_launches;
-    cfar_ws_kernel<T, NCW, CPT, BOXC, SG><<<grid, (NCW + 1) * kWarp, smem, stream>>>(L, tmap_tab, tmap_cut);
+    cfar_ws_kernel<T, NCW, CPT, BOXC, SG, OCC><<<grid, (NCW + 1) * kWarp, smem, stream>>>(L, tmap_tab, tmap_cut);
     return cudaGetLastError();
 }
 
 template <typename T, int BOXC>
 cudaError_t go_ncw(const CfarLaunch& L, int ncw, cudaStream_t stream) {
-    int sg = 1;
-    if (const char* a = getenv("UWB_RING_SG")) sg = atoi(a) == 2 ? 2 : 1;
-    if (ncw == 2) return go<T, 2, 2, BOXC, 1>(L, stream);
-    return sg == 1 ? go<T, 4, 1, BOXC, 1>(L, stream) : go<T, 4, 1, BOXC, 2>(L, stream);
+    (void)ncw;
+    // the most CTAs per SM whose rings fit (UWB_RING_OCC pins one for tuning)
+    int occ = 0;
+    const int pinned = getenv("UWB_RING_OCC") ? atoi(getenv("UWB_RING_OCC")) : 0;
+    for (int o : {4, 3, 2, 1}) {
+        if (pinned && o != pinned) continue;
+        if (ring_smem_bytes<T>(L.hr, BOXC, 1, o) <= static_cast<size_t>(233472 / o - 1024)) {
+            occ = o;
+            break;
+        }
+    }
+    switch (occ) {
+        case 4: return go<T, 4, 1, BOXC, 1, 4>(L, stream);
+        case 3: return go<T, 4, 1, BOXC, 1, 3>(L, stream);
+        case 2: return go<T, 4, 1, BOXC, 1, 2>(L, stream);
+        case 1: return go<T, 4, 1, BOXC, 1, 1>(L, stream);
+        default: return cudaErrorNotSupported;
+    }
 }
 
 template <typename T>
