@@ -274,8 +274,6 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
 
     if (warp == NCW) {
         // =========================== producer thread ===========================
-        // compute-only probe (debug bit 1): fill each ring once, consumers then
-        // recompute on the resident (valid, stale) rows without waiting
         if (lane != 0) return;
         const int last_grp = (i_hi - i_lo) / kG;
         for (int g = 0; g <= min(last_grp, kPfGroups - 1); ++g)
@@ -288,11 +286,9 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
         // Issue order: always the load the consumers need first; block (suspended)
         // only on that load's ring slot. Table group grp is first read at step
         // (i_lo + 4 grp - ra - hr - 1) / RS, CUT group cstep at step cstep / SG.
-        const bool once = (L.debug & 2u) != 0;
-        while ((grp <= last_grp && !(once && grp >= G.ng)) || (cstep < n_cg && !(once && cstep >= kCutGroups))) {
-            const int need_tab =
-                grp <= last_grp && !(once && grp >= G.ng) ? max(0, (i_lo + kG * grp - ra - hr - 1)) / RS : INT_MAX;
-            const int need_cut = cstep < n_cg && !(once && cstep >= kCutGroups) ? cstep / SG : INT_MAX;
+        while (grp <= last_grp || cstep < n_cg) {
+            const int need_tab = grp <= last_grp ? max(0, (i_lo + kG * grp - ra - hr - 1)) / RS : INT_MAX;
+            const int need_cut = cstep < n_cg ? cstep / SG : INT_MAX;
             if (need_tab <= need_cut) {
                 if (grp >= G.ng) mbar_wait_susp(&empty_t[gslot], static_cast<unsigned>(gphase ^ 1), L.sleep_ns);
                 const int first = i_lo + grp * kG;
@@ -369,15 +365,14 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
         {
             const int need = min(last_grp_c, (min(r_last + hr, rows - 1) + 1 - i_lo) / kG);
             while (waited < need) {
-                if (!(L.debug & 2u) || waited < G.ng - 1)
-                    mbar_wait_u<kHint>(full_t_u + 8u * wslot, static_cast<unsigned>(wphase));
+                mbar_wait_u<kHint>(full_t_u + 8u * wslot, static_cast<unsigned>(wphase));
                 ++waited;
                 if (++wslot == G.ng) { wslot = 0; wphase ^= 1; }
             }
         }
 #pragma unroll
         for (int q = 0; q < SG; ++q)
-            if ((q == 0 || r0 + q * kG <= r_last) && (!(L.debug & 2u) || step < kCutGroups))
+            if (q == 0 || r0 + q * kG <= r_last)
                 mbar_wait_u<kHint>(full_c_u + 8u * (cslot + q), static_cast<unsigned>(cphase));
         const T* cut_grp = cuts + static_cast<size_t>(cslot) * kG * kW;
         double v[RS][CPT], thr[RS][CPT];
