@@ -382,8 +382,9 @@ def main():
     ap.add_argument("--maps", type=int, default=N_MAPS, help="batch size (profiling runs only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5],
-                    help="BASELINE.json configuration (3 = the headline line; see bench_configs.py)")
+    ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5, 6],
+                    help="BASELINE.json configuration (3 = the headline line; 6 = the paper's Table I; "
+                         "see bench_configs.py)")
     args = ap.parse_args()
     globals()["N_MAPS"] = args.maps
     if args.config != 3:

@@ -17,6 +17,8 @@ JSON schema so every row of SURVEY 8d has a number:
 * config 1 - one 256 x 512 fp64 map (launch-bound; ms_per_step is per map).
 * config 2 - front end + CFAR of one 512 x 1024 record through the host-level
   detect() drop-in (value in records/s; H2D/D2H inside, so it is also e2e).
+* --config 6 - the paper's Table I: naive vs integral-image CA-CFAR on a
+  1024 x 600 map for (g, b) in {(4,8), (4,12), (8,8), (8,12)}, GPU and reference.
 """
 from __future__ import annotations
 
@@ -361,6 +363,54 @@ def run_cfg2(args):
     return 0
 
 
+# ------------------------------------------------------------------ Table I --
+TABLE1 = [(4, 8), (4, 12), (8, 8), (8, 12)]
+
+
+def run_table1(args):
+    """The paper's Table I on one 1024 x 600 fp64 map: naive
+    ring-sum CA-CFAR vs the integral-image CA-CFAR, same mask, on the GPU
+    (device-resident map, CUDA events) and with the reference on one host core
+    (uwbvital_ref::cfar2d_naive / cfar2d_integral, threads=1)."""
+    import torch
+    import paper_2012_11077_b200 as uwb
+    from paper_2012_11077_b200 import synth
+    from paper_2012_11077_b200.batch import BatchCfar
+    from oracle.pyoracle import RefLib
+    world, rank, dist = _init_dist()
+    R, C, pfa = 1024, 600, 1e-4
+    m = synth.exponential_maps(1, R, C, seed=77, dtype=torch.float64, device="cuda")
+    host = m[0].cpu().numpy()
+    ref = None if args.no_cpu_baseline else RefLib()
+    table = []
+    for g, b in TABLE1:
+        runner = BatchCfar(1, R, C, uwb.CfarParams(g, b, pfa), torch.float64, det_capacity=1 << 14,
+                           want_mask_u8=True)
+        ii = _events_time(lambda: runner(m), args.steps, args.warmup, world, dist)
+        mask_ii = runner.mask_u8[0].clone()
+        nv = _events_time(lambda: runner(m, naive=True), args.steps, args.warmup, world, dist)
+        same = bool(torch.equal(mask_ii, runner.mask_u8[0]))
+        row = {"guard": g, "train": b, "gpu_naive_ms": nv, "gpu_integral_ms": ii, "gpu_speedup": nv / ii,
+               "masks_equal": same}
+        if ref is not None:
+            t0 = time.perf_counter()
+            ref.cfar2d(host, g, b, pfa, "naive")
+            t1 = time.perf_counter()
+            ref.cfar2d(host, g, b, pfa, "integral")
+            t2 = time.perf_counter()
+            row.update({"cpu_naive_ms": (t1 - t0) * 1e3, "cpu_integral_ms": (t2 - t1) * 1e3,
+                        "cpu_speedup": (t1 - t0) / (t2 - t1)})
+        table.append(row)
+    if rank == 0:
+        _line(metric="Table I (PAPER.md:77-81): naive / integral-image CA-CFAR time ratio, 1024x600 fp64",
+              value=min(r["gpu_speedup"] for r in table), unit="x (min over rows)", steps=args.steps,
+              warmup=args.warmup, ms_per_step=None,
+              config={"workload": "one Exp(1) fp64 map 1024 x 600, Pfa 1e-4, (guard, train) per PAPER.md Table I",
+                      "spec": "II >= 2x naive on every row (SPEC.md:483-484)"},
+              table=table, cpu_baseline=None, e2e=None, roofline=None, gpu_launches=None, clocks=None)
+    return 0
+
+
 def run_reference_cfg(args):
     """--impl reference for configs 4/5/1/2: the reference CPU path on the host cores."""
     world, rank, _ = B._dist()
@@ -421,6 +471,8 @@ def run_reference_cfg(args):
 
 
 def run(args):
+    if args.config == 6:
+        return run_table1(args)
     if args.impl == "reference":
         return run_reference_cfg(args)
     return {4: run_cfg4, 5: run_cfg5, 1: run_cfg1, 2: run_cfg2}[args.config](args)

@@ -199,7 +199,9 @@ uint64_t uwb_dev_cfar2d_workspace(const uwb_map_batch* batch, const uwb_cfar_par
  *   previous call on the same maps with the same table geometry (GLOBAL mode, or
  *   SLAB mode with the same slab_rows and g_r + b_r): one table, several CFAR
  *   parameter sets (the integral image's point). Non-finite inputs are reported
- *   only by the call that built the tables. */
+ *   only by the call that built the tables.
+ * flags bit 3: the naive backend instead (cfar.cpp:200-216: explicit ring sums,
+ *   no table; GLOBAL mode only) - the baseline of the paper's Table I. */
 uwb_status uwb_dev_cfar2d(const uwb_map_batch* batch, const uwb_cfar_params* params,
                           const double* alpha_dev, int32_t sat_mode, uint64_t slab_rows,
                           const uwb_cfar_outputs* out, void* workspace, uint64_t workspace_bytes,

@@ -511,8 +511,10 @@ uwb_status uwb_dev_cfar2d(const uwb_map_batch* b, const uwb_cfar_params* p, cons
     if (uwb_status s = need_device()) return s;
     const Plan P = make_plan(*b, p, sat_mode, slab_rows, static_cast<int64_t>(out->det_capacity));
     if (ws_bytes < P.total) return fail(UWB_INVALID_ARGUMENT, "uwb: workspace too small (need " + S(static_cast<uint64_t>(P.total)) + ")");
-    if (uwb_status s = dev_cfar(*b, *p, alpha_dev, UWB_INTEGRAL, sat_mode, slab_rows, *out, workspace,
-                                ws_bytes, flags, static_cast<cudaStream_t>(stream)))
+    // flags bit 3: the naive backend (cfar2d_naive, cfar.cpp:200-216; no table)
+    const int backend = (flags & 8u) ? UWB_NAIVE : UWB_INTEGRAL;
+    if (uwb_status s = dev_cfar(*b, *p, alpha_dev, backend, sat_mode, slab_rows, *out, workspace, ws_bytes, flags,
+                                static_cast<cudaStream_t>(stream)))
         return s;
     return ok();
 }

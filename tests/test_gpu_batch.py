@@ -222,3 +222,17 @@ def test_reused_tables_match_fresh_call(uwb, oracle, cuda):
     for i in range(2):
         _check_map(b, i, oracle.cfar(host[i], 3, 1, 16, 4, 1e-5), f"reused tables map {i}")
         _check_map(a, i, oracle.cfar(host[i], 1, 3, 4, 16, 1e-3), f"first call map {i}")
+
+
+def test_naive_backend_flag_matches_reference_naive(uwb, ref, cuda):
+    """flags bit 3 (naive backend, cfar.cpp:200-216) on the device batch path."""
+    from paper_2012_11077_b200.batch import BatchCfar
+    g = torch.Generator(device="cuda").manual_seed(23)
+    maps = torch.empty((2, 96, 130), device="cuda", dtype=torch.float64).exponential_(1.0, generator=g)
+    p = uwb.CfarParams(4, 8, 1e-3)
+    b = BatchCfar(2, 96, 130, p, torch.float64, det_capacity=4096, want_mask_u8=True, want_thresholds=True)
+    b(maps, naive=True)
+    torch.cuda.synchronize()
+    host = maps.cpu().numpy()
+    for i in range(2):
+        _check_map(b, i, ref.cfar2d(host[i], 4, 8, 1e-3, "naive"), f"naive map {i}")
