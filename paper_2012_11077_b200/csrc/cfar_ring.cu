@@ -41,10 +41,8 @@ namespace {
 constexpr int kRingRows = 256;  // output rows per CTA
 constexpr int kG = 4;           // rows per group (output step, TMA box height)
 constexpr int kW = 128;         // output columns per CTA
-// Occupancy profiles (CTAs per SM): the shared memory left after the resident
-// window goes to look-ahead (table groups beyond the window, CUT ring depth).
-__host__ __device__ constexpr int occ_ahead(int occ) { return occ >= 4 ? 1 : occ == 3 ? 4 : 10; }
-__host__ __device__ constexpr int occ_cut(int occ) { return occ >= 4 ? 4 : occ == 3 ? 6 : 8; }
+constexpr int kCutGroups = 4;   // CUT ring depth (groups)
+constexpr int kMaxAhead = 8;    // most table groups of look-ahead beyond the window
 constexpr int kPfGroups = 6;    // L2 prefetch distance of both streams (groups)
 
 struct RingGeom {
@@ -63,9 +61,8 @@ __host__ __device__ inline RingGeom ring_geom(int hr, int sg, int ahead) {
 }
 
 template <typename T>
-inline size_t ring_smem_bytes(int hr, int boxc, int sg, int occ) {
-    const int kCutGroups = occ_cut(occ);
-    const RingGeom g = ring_geom(hr, sg, occ_ahead(occ));
+inline size_t ring_smem_bytes(int hr, int boxc, int sg, int ahead) {
+    const RingGeom g = ring_geom(hr, sg, ahead);
     return 128 /* alignment slack */ + sizeof(double) * static_cast<size_t>(g.nr + kG * sg) * boxc +
            sizeof(T) * static_cast<size_t>(kCutGroups) * kG * kW + 2 * sizeof(uint64_t) * (g.ng + kCutGroups);
 }
@@ -219,7 +216,6 @@ __global__ void __launch_bounds__((NCW + 1) * kWarp, OCC)
 cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUtensorMap tmap_tab,
                const __grid_constant__ CUtensorMap tmap_cut) {
     static_assert(NCW * CPT * kWarp == kW, "tile width");
-    constexpr int kCutGroups = occ_cut(OCC);
     static_assert(kCutGroups % SG == 0, "CUT ring depth");
     constexpr int RS = kG * SG; // output rows per consumer step
     constexpr unsigned kRowBytes = 8u * BOXC;
@@ -228,7 +224,7 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
     extern __shared__ unsigned char ring_raw[];
     unsigned char* ring_smem =
         ring_raw + ((128u - (static_cast<unsigned>(__cvta_generic_to_shared(ring_raw)) & 127u)) & 127u);
-    const RingGeom G = ring_geom(L.hr, SG, occ_ahead(OCC));
+    const RingGeom G = ring_geom(L.hr, SG, L.ring_ahead);
     double* slots = reinterpret_cast<double*>(ring_smem);
     const char* ring = reinterpret_cast<const char*>(ring_smem);
     T* cuts = reinterpret_cast<T*>(slots + static_cast<size_t>(G.nr + RS) * BOXC);
@@ -571,7 +567,7 @@ cudaError_t go(const CfarLaunch& L0, cudaStream_t stream) {
     if (!encode3(&tmap_cut, sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
                  sizeof(T), L.maps, L.cols, L.geo.buf_rows, n_maps, L.ld, mstride, kW, kG))
         return cudaErrorNotSupported;
-    const size_t smem = ring_smem_bytes<T>(L.hr, BOXC, SG, OCC);
+    const size_t smem = ring_smem_bytes<T>(L.hr, BOXC, SG, L.ring_ahead);
     if (smem > 227 * 1024) return cudaErrorNotSupported;
     const dim3 grid(static_cast<unsigned>(L.col_tiles * L.row_chunks), static_cast<unsigned>(L.n_jobs), 1);
     cudaError_t e = cudaFuncSetAttribute(cfar_ws_kernel<T, NCW, CPT, BOXC, SG, OCC>,
@@ -585,22 +581,30 @@ cudaError_t go(const CfarLaunch& L0, cudaStream_t stream) {
 template <typename T, int BOXC>
 cudaError_t go_ncw(const CfarLaunch& L, int ncw, cudaStream_t stream) {
     (void)ncw;
-    // the most CTAs per SM whose rings fit (UWB_RING_OCC pins one for tuning)
+    // The most CTAs per SM whose rings fit with one group of look-ahead, then
+    // the deepest look-ahead that still fits at that occupancy (measured: CTAs
+    // per SM matter more than look-ahead). UWB_RING_OCC pins the occupancy.
     int occ = 0;
     const int pinned = getenv("UWB_RING_OCC") ? atoi(getenv("UWB_RING_OCC")) : 0;
+    auto fits = [&](int o, int ahead) {
+        return ring_smem_bytes<T>(L.hr, BOXC, 1, ahead) <= static_cast<size_t>(233472 / o - 1024);
+    };
     for (int o : {4, 3, 2, 1}) {
         if (pinned && o != pinned) continue;
-        if (ring_smem_bytes<T>(L.hr, BOXC, 1, o) <= static_cast<size_t>(233472 / o - 1024)) {
+        if (fits(o, 1)) {
             occ = o;
             break;
         }
     }
+    if (!occ) return cudaErrorNotSupported;
+    CfarLaunch La = L;
+    La.ring_ahead = 1;
+    while (La.ring_ahead < kMaxAhead && fits(occ, La.ring_ahead + 1)) ++La.ring_ahead;
     switch (occ) {
-        case 4: return go<T, 4, 1, BOXC, 1, 4>(L, stream);
-        case 3: return go<T, 4, 1, BOXC, 1, 3>(L, stream);
-        case 2: return go<T, 4, 1, BOXC, 1, 2>(L, stream);
-        case 1: return go<T, 4, 1, BOXC, 1, 1>(L, stream);
-        default: return cudaErrorNotSupported;
+        case 4: return go<T, 4, 1, BOXC, 1, 4>(La, stream);
+        case 3: return go<T, 4, 1, BOXC, 1, 3>(La, stream);
+        case 2: return go<T, 4, 1, BOXC, 1, 2>(La, stream);
+        default: return go<T, 4, 1, BOXC, 1, 1>(La, stream);
     }
 }
 

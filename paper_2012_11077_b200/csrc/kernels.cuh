@@ -129,6 +129,7 @@ struct CfarLaunch {
     int64_t row_chunks;  // row chunks per job
     unsigned sleep_ns;   // barrier-wait suspend hint of the CFAR ring kernel (ns)
     unsigned debug;      // bit 0: consumers skip the cell arithmetic (data-movement probe)
+    int ring_ahead;      // CFAR ring: table groups of look-ahead beyond the window
     int64_t col_tiles;
 };
 
