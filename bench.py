@@ -127,6 +127,23 @@ def _dist():
     return world, rank, local
 
 
+def _init_rank(world: int, local: int):
+    """One process per GPU over NCCL. UWB_DIST_BACKEND=gloo (test hook) lets
+    several ranks share the visible GPUs to exercise the multi-rank code path
+    (no kernel of one rank waits on another rank)."""
+    import torch
+    import torch.distributed as dist
+    idx = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(idx)
+    if world > 1:
+        backend = os.environ.get("UWB_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", idx))
+        else:
+            dist.init_process_group(backend)
+    return torch.device("cuda", idx)
+
+
 def _shard(world: int, rank: int):
     """Contiguous blocks of 64-map chunks per rank (maps are independent units)."""
     chunks = N_MAPS // CHUNK
@@ -235,11 +252,7 @@ def run_b200(args):
     from paper_2012_11077_b200.batch import BatchCfar, host_cfar2d_batch, kernel_launches, phase_ms
 
     world, rank, local = _dist()
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local if world > 1 else 0)
-    torch.cuda.set_device(dev)
+    dev = _init_rank(world, local)
     m0, m1 = _shard(world, rank)
     n_local = m1 - m0
     maps = _generate(m0, m1, dev)

@@ -81,10 +81,7 @@ def _init_dist():
     import torch
     import torch.distributed as dist
     world, rank, local = B._dist()
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local if world > 1 else 0)
+    B._init_rank(world, local)
     return world, rank, dist
 
 
