@@ -248,7 +248,24 @@ uwb_status uwb_host_cfar2d_batch(const uwb_map_batch* host_batch, const uwb_cfar
                                  uwb_detection* dets, uint64_t det_capacity,
                                  uint64_t* det_counts, uint64_t maps_per_chunk);
 
-/* Instrumentation. uwb_kernel_launches: number of kernels this library has
+/* Batched detect() on the device (pipeline.cpp:246-275 per record; SURVEY 8f
+ * rank 1): `records` holds n_records frames of m fast-time rows x n slow-time
+ * columns (dtype f32/f64, dense). The front end writes each record's band power
+ * (m x kept fp64, kept = *kept_out) straight into `band` (n_records maps, the
+ * CFAR input), then the CFAR of the configuration runs over all band maps into
+ * `out` (one map per record). Configuration and stage errors are returned with
+ * the reference's messages before any work; per-record input errors go to
+ * out->first_bad (entry 0: first non-finite frame sample, row-major). Query the
+ * band width and workspace first (uwb_dev_detect_batch_workspace returns 0 for
+ * a configuration error). */
+uint64_t uwb_dev_detect_batch_workspace(uint64_t n_records, uint64_t m, uint64_t n, double prf,
+                                        const uwb_pipeline_config* cfg, uint64_t det_capacity);
+uwb_status uwb_dev_detect_batch(const void* records, int32_t dtype, uint64_t n_records, uint64_t m, uint64_t n,
+                                double fast_rate, double prf, const uwb_pipeline_config* cfg, double* band,
+                                uint64_t* kept_out, const uwb_cfar_outputs* out, void* workspace,
+                                uint64_t workspace_bytes, uint32_t flags, void* stream);
+
+/* Instrumentation./* Instrumentation. uwb_kernel_launches: number of kernels this library has
  * launched in the process. With flags bit 1 set, uwb_dev_cfar2d records CUDA
  * events around its phases (SAT, CFAR, sort) into a 1024-slot ring without
  * synchronising; uwb_dev_phase_ms synchronises on them, writes up to max_calls

@@ -105,6 +105,8 @@ SIGNATURES = {
     "uwb_dev_cfar2d": (_S, [_P, _P, _P, C.c_int32, _U64, _P, _P, _U64, C.c_uint32, _P]),
     "uwb_dev_cfar2d_window_workspace": (_U64, [_P, _P, _P, _U64, _U64]),
     "uwb_dev_cfar2d_window": (_S, [_P, _P, _P, _P, _U64, _P, _P, _U64, C.c_uint32, _P]),
+    "uwb_dev_detect_batch_workspace": (_U64, [_U64, _U64, _U64, _D, _P, _U64]),
+    "uwb_dev_detect_batch": (_S, [_P, C.c_int32, _U64, _U64, _U64, _D, _D, _P, _P, _P, _P, _P, _U64, C.c_uint32, _P]),
     "uwb_dev_build_sat": (_S, [_P, _P, _U64, _U64, _P, _P, _U64, _P]),
     "uwb_dev_build_sat_workspace": (_U64, [_P]),
     "uwb_host_cfar2d_batch": (_S, [_P, _P, C.c_int32, _U64, _P, _P, _U64, _P, _U64]),

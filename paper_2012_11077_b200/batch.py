@@ -133,6 +133,74 @@ class BatchCfar:
         return bits[:, : self.cols].astype(np.uint8)
 
 
+class DetectBatch:
+    """Batched detect() on the device (pipeline.cpp:246-275 per record): the
+    front end of every record writes its band power straight into the CFAR's
+    input maps, then one CFAR call covers all records. ``records`` passed to a
+    call: (n_records, m fast-time rows, n slow-time columns), float32/64, CUDA."""
+
+    def __init__(self, n_records: int, m: int, n: int, config, prf: float, fast_rate: float = 39e9,
+                 dtype: torch.dtype = torch.float32, det_capacity: int = 4096, device=None):
+        if dtype not in _DT:
+            raise ValueError("records must be float32 or float64")
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.n_records, self.m, self.n = int(n_records), int(m), int(n)
+        self.dtype, self.prf, self.fast_rate = dtype, float(prf), float(fast_rate)
+        self.det_capacity = int(det_capacity)
+        self._cfg = config.to_c()
+        kept = C.c_uint64()
+        empty = N.uwb_cfar_outputs()
+        raise_for(N.lib.uwb_dev_detect_batch(None, _DT[dtype], 0, self.m, self.n, C.c_double(self.fast_rate),
+                                             C.c_double(self.prf), C.byref(self._cfg), None, C.byref(kept),
+                                             C.byref(empty), None, 0, 0, None))
+        self.kept = int(kept.value)
+        dev = self.device
+        self.words_per_row = (self.kept + 31) // 32
+        self.band = torch.zeros((self.n_records, self.m, self.kept), dtype=torch.float64, device=dev)
+        self.mask_bits = torch.zeros((self.n_records, self.m, self.words_per_row), dtype=torch.int32, device=dev)
+        self.dets = torch.zeros((self.n_records, max(1, self.det_capacity), 32), dtype=torch.uint8, device=dev)
+        self.counts = torch.zeros(self.n_records, dtype=torch.int64, device=dev)
+        self.first_bad = torch.zeros((self.n_records, 2), dtype=torch.int64, device=dev)
+        ws = N.lib.uwb_dev_detect_batch_workspace(self.n_records, self.m, self.n, C.c_double(self.prf),
+                                                  C.byref(self._cfg), self.det_capacity)
+        self.workspace = torch.empty(max(int(ws), 16), dtype=torch.uint8, device=dev)
+        self._out = N.uwb_cfar_outputs(
+            self.mask_bits.data_ptr(), self.words_per_row, self.m * self.words_per_row, None, None,
+            self.dets.data_ptr(), self.det_capacity, self.counts.data_ptr(), self.first_bad.data_ptr())
+
+    def __call__(self, records: torch.Tensor, stream=None) -> None:
+        if records.dtype != self.dtype or tuple(records.shape) != (self.n_records, self.m, self.n):
+            raise ValueError(f"expected {(self.n_records, self.m, self.n)} {self.dtype}")
+        if not records.is_cuda or not records.is_contiguous():
+            raise ValueError("records must be a contiguous CUDA tensor")
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        kept = C.c_uint64()
+        raise_for(N.lib.uwb_dev_detect_batch(records.data_ptr(), _DT[self.dtype], self.n_records, self.m, self.n,
+                                             C.c_double(self.fast_rate), C.c_double(self.prf), C.byref(self._cfg),
+                                             self.band.data_ptr(), C.byref(kept), C.byref(self._out),
+                                             self.workspace.data_ptr(), C.c_uint64(self.workspace.numel()), 0,
+                                             C.c_void_p(s.cuda_stream)))
+
+    def check_inputs(self) -> None:
+        """Raise the reference's InputError for the first record with a non-finite sample."""
+        fb = self.first_bad.cpu().numpy().astype(np.uint64)
+        for i in range(self.n_records):
+            if fb[i, 0] != np.uint64(0xFFFFFFFFFFFFFFFF):
+                raise InputError("RadarFrame: non-finite sample")
+
+    def detections(self, i: int) -> np.ndarray:
+        n = int(self.counts[i].item())
+        if n > self.det_capacity:
+            raise CapacityError(f"record {i}: {n} detections > capacity {self.det_capacity}", n)
+        raw = self.dets[i, :n].contiguous().cpu().numpy().reshape(-1)
+        return np.frombuffer(raw.tobytes(), dtype=DETECTION_DTYPE, count=n).copy()
+
+    def mask(self, i: int) -> np.ndarray:
+        words = self.mask_bits[i].cpu().numpy().view(np.uint32)
+        bits = np.unpackbits(words.view(np.uint8).reshape(self.m, -1), axis=1, bitorder="little")
+        return bits[:, : self.kept].astype(np.uint8)
+
+
 def phase_ms(max_calls: int = 1024) -> np.ndarray:
     """(calls, 3) array of {sat, cfar, sort} milliseconds of the calls made with
     ``phase_events=True`` since the last read (synchronises on them)."""

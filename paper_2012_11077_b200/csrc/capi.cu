@@ -357,6 +357,83 @@ uwb_status set_cuda_error(cudaError_t e, const char* what) {
     return fail(UWB_CUDA_ERROR, std::string("CUDA error ") + cudaGetErrorString(e) + " in " + what);
 }
 
+// PipelineConfig::validate / effective_fft_length and the stage checks of
+// detect (pipeline.cpp:40-56, 100-105, 157-223), evaluated on the host. The
+// configuration error is reported after the frame's finiteness check and the
+// stage error after it, as in the reference.
+struct DetectPlan {
+    uint64_t L = 0, first = 0, kept = 0;
+    uwb_status cfg_status = UWB_OK, stage_status = UWB_OK;
+    std::string cfg_msg, stage_msg;
+    bool ok() const { return cfg_status == UWB_OK && stage_status == UWB_OK; }
+};
+
+DetectPlan detect_plan(uint64_t m, uint64_t n, double prf, const uwb_pipeline_config& c) {
+    (void)m;
+    DetectPlan D;
+    const uint64_t L = c.fft_length == 0 ? next_pow2(n) : c.fft_length;
+    D.L = L;
+    std::string& cfg_msg = D.cfg_msg;
+    uwb_status& cfg_status = D.cfg_status;
+    std::string& stage_msg = D.stage_msg;
+    uwb_status& stage_status = D.stage_status;
+
+    // configuration checks that do not need data; reported after the
+    // finiteness check below to keep the reference's order
+
+    if (c.mean_filter_window == 0 || c.mean_filter_window % 2 == 0) {
+        cfg_status = UWB_PARAMETER_ERROR;
+        cfg_msg = "PipelineConfig: mean_filter_window must be odd and positive, got " + S(c.mean_filter_window);
+    } else if (!(c.band_low_hz > 0.0) || !(c.band_low_hz < c.band_high_hz)) {
+        cfg_status = UWB_PARAMETER_ERROR;
+        cfg_msg = "PipelineConfig: need 0 < band_low_hz < band_high_hz";
+    } else if (!(c.normalization_epsilon > 0.0)) {
+        cfg_status = UWB_PARAMETER_ERROR;
+        cfg_msg = "PipelineConfig: normalization_epsilon must be positive";
+    } else if (validate_params(c.cfar) != UWB_OK) {
+        cfg_status = UWB_PARAMETER_ERROR;
+        cfg_msg = g_err.message;
+    } else if (!(c.band_high_hz < prf / 2.0)) {
+        cfg_status = UWB_PARAMETER_ERROR;
+        cfg_msg = "detect: band_high_hz must be below prf/2 = " + fmt_double(prf / 2.0) + " Hz";
+    }
+    const bool smooth = c.mean_filter_mode == 0;
+
+    if (cfg_status == UWB_OK) {
+        if (smooth && (c.mean_filter_window > n)) {
+            stage_status = UWB_PARAMETER_ERROR;
+            stage_msg = "mean_filter_slow: mean_filter_slow: window must be odd and in [1, " + S(n) + "], got " +
+                        S(c.mean_filter_window);
+        } else if (L < n) {
+            stage_status = UWB_PARAMETER_ERROR;
+            stage_msg = "slow_time_spectrum: slow_time_spectrum: fft_length " + S(L) + " < trace count " + S(n);
+        }
+    }
+
+    if (cfg_status == UWB_OK && stage_status == UWB_OK) {
+        const uint64_t bins = L / 2 + 1;
+        uint64_t f = bins, l = 0;
+        for (uint64_t k = 0; k < bins; ++k) {
+            const double fr = static_cast<double>(k) * prf / static_cast<double>(L);
+            if (fr >= c.band_low_hz && fr <= c.band_high_hz) {
+                if (f == bins) f = k;
+                l = k;
+            }
+        }
+        if (f == bins) {
+            const double res = bins > 1 ? (1.0 * prf / static_cast<double>(L)) - (0.0 * prf / static_cast<double>(L))
+                                        : 0.0 * prf / static_cast<double>(L);
+            stage_status = UWB_CONFIGURATION_ERROR;
+            stage_msg = "band_select: band_select: no FFT bin falls in [" + fmt_double(c.band_low_hz) + ", " +
+                        fmt_double(c.band_high_hz) + "] Hz at bin resolution " + fmt_double(res) + " Hz";
+        } else {
+            D.first = f;
+            D.kept = l - f + 1;
+        }
+    }
+    return D;
+}
+
 } // namespace uwb
 
 using namespace uwb;
@@ -821,62 +898,12 @@ uwb_status uwb_detect(const double* frame, uint64_t m, uint64_t n, double fast_r
     cudaStream_t s = host_stream();
 
     const uwb_pipeline_config& c = *cfg;
-    const uint64_t L = c.fft_length == 0 ? next_pow2(n) : c.fft_length;
-    // configuration checks that do not need data; reported after the
-    // finiteness check below to keep the reference's order
-    std::string cfg_msg;
-    uwb_status cfg_status = UWB_OK;
-    if (c.mean_filter_window == 0 || c.mean_filter_window % 2 == 0) {
-        cfg_status = UWB_PARAMETER_ERROR;
-        cfg_msg = "PipelineConfig: mean_filter_window must be odd and positive, got " + S(c.mean_filter_window);
-    } else if (!(c.band_low_hz > 0.0) || !(c.band_low_hz < c.band_high_hz)) {
-        cfg_status = UWB_PARAMETER_ERROR;
-        cfg_msg = "PipelineConfig: need 0 < band_low_hz < band_high_hz";
-    } else if (!(c.normalization_epsilon > 0.0)) {
-        cfg_status = UWB_PARAMETER_ERROR;
-        cfg_msg = "PipelineConfig: normalization_epsilon must be positive";
-    } else if (validate_params(c.cfar) != UWB_OK) {
-        cfg_status = UWB_PARAMETER_ERROR;
-        cfg_msg = g_err.message;
-    } else if (!(c.band_high_hz < prf / 2.0)) {
-        cfg_status = UWB_PARAMETER_ERROR;
-        cfg_msg = "detect: band_high_hz must be below prf/2 = " + fmt_double(prf / 2.0) + " Hz";
-    }
+    const DetectPlan D = detect_plan(m, n, prf, c);
+    const uint64_t L = D.L, first = D.first, kept = D.kept;
+    const uwb_status cfg_status = D.cfg_status, stage_status = D.stage_status;
+    const std::string& cfg_msg = D.cfg_msg;
+    const std::string& stage_msg = D.stage_msg;
     const bool smooth = c.mean_filter_mode == 0;
-    std::string stage_msg;
-    uwb_status stage_status = UWB_OK;
-    if (cfg_status == UWB_OK) {
-        if (smooth && (c.mean_filter_window > n)) {
-            stage_status = UWB_PARAMETER_ERROR;
-            stage_msg = "mean_filter_slow: mean_filter_slow: window must be odd and in [1, " + S(n) + "], got " +
-                        S(c.mean_filter_window);
-        } else if (L < n) {
-            stage_status = UWB_PARAMETER_ERROR;
-            stage_msg = "slow_time_spectrum: slow_time_spectrum: fft_length " + S(L) + " < trace count " + S(n);
-        }
-    }
-    uint64_t first = 0, kept = 0;
-    if (cfg_status == UWB_OK && stage_status == UWB_OK) {
-        const uint64_t bins = L / 2 + 1;
-        uint64_t f = bins, l = 0;
-        for (uint64_t k = 0; k < bins; ++k) {
-            const double fr = static_cast<double>(k) * prf / static_cast<double>(L);
-            if (fr >= c.band_low_hz && fr <= c.band_high_hz) {
-                if (f == bins) f = k;
-                l = k;
-            }
-        }
-        if (f == bins) {
-            const double res = bins > 1 ? (1.0 * prf / static_cast<double>(L)) - (0.0 * prf / static_cast<double>(L))
-                                        : 0.0 * prf / static_cast<double>(L);
-            stage_status = UWB_CONFIGURATION_ERROR;
-            stage_msg = "band_select: band_select: no FFT bin falls in [" + fmt_double(c.band_low_hz) + ", " +
-                        fmt_double(c.band_high_hz) + "] Hz at bin resolution " + fmt_double(res) + " Hz";
-        } else {
-            first = f;
-            kept = l - f + 1;
-        }
-    }
     const bool run_all = cfg_status == UWB_OK && stage_status == UWB_OK;
     if (run_all && L > 8192) return fail(UWB_INVALID_ARGUMENT, "uwb: fft_length > 8192 not supported on the device path");
     if (run_all && kept > band_capacity) return fail(UWB_INVALID_ARGUMENT, "uwb_detect: band_capacity too small");
@@ -1105,6 +1132,119 @@ uwb_status uwb_host_cfar2d_batch(const uwb_map_batch* hb, const uwb_cfar_params*
     for (uint64_t i = 0; i < hb->n_maps; ++i)
         if (det_counts[i] > det_capacity) result = fail(UWB_CAPACITY_ERROR, "uwb_host_cfar2d_batch: detection buffer too small");
     return result ? result : ok();
+}
+
+// ---- batched device detect() ------------------------------
+
+static uint64_t detect_ws_layout(uint64_t n_rec, uint64_t m, uint64_t n, uint64_t L, const Plan& P,
+                                 size_t* off_work, size_t* off_tw, size_t* off_bad, size_t* off_cfar) {
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off += static_cast<size_t>(round_up(static_cast<int64_t>(bytes), 256));
+        return o;
+    };
+    *off_work = take(sizeof(double) * n_rec * m * n);
+    *off_tw = take(sizeof(double) * 2 * L);
+    *off_bad = take(sizeof(uint64_t) * n_rec);
+    *off_cfar = take(P.total);
+    return off;
+}
+
+uint64_t uwb_dev_detect_batch_workspace(uint64_t n_records, uint64_t m, uint64_t n, double prf,
+                                        const uwb_pipeline_config* cfg, uint64_t det_capacity) {
+    const DetectPlan D = detect_plan(m, n, prf, *cfg);
+    if (!D.ok()) return 0;
+    uwb_map_batch b{};
+    b.dtype = UWB_F64;
+    b.n_maps = n_records;
+    b.rows = m;
+    b.cols = D.kept;
+    b.ld = D.kept;
+    b.map_stride = m * D.kept;
+    const Plan P = make_plan(b, &cfg->cfar, UWB_SAT_GLOBAL, 0, static_cast<int64_t>(det_capacity));
+    size_t a, t, bd, cf;
+    return detect_ws_layout(n_records, m, n, D.L, P, &a, &t, &bd, &cf);
+}
+
+uwb_status uwb_dev_detect_batch(const void* records, int32_t dtype, uint64_t n_records, uint64_t m, uint64_t n,
+                                double fast_rate, double prf, const uwb_pipeline_config* cfg, double* band,
+                                uint64_t* kept_out, const uwb_cfar_outputs* out, void* workspace,
+                                uint64_t ws_bytes, uint32_t flags, void* stream) {
+    if (kept_out) *kept_out = 0;
+    if (!cfg || !out || (!records && n_records)) return fail(UWB_INVALID_ARGUMENT, "uwb: null argument");
+    if (dtype != UWB_F32 && dtype != UWB_F64) return fail(UWB_INVALID_ARGUMENT, "uwb: bad dtype");
+    if (m < 2 || n < 2)
+        return fail(UWB_DIMENSION_ERROR, "RadarFrame: need at least 2x2 samples, got " + S(m) + "x" + S(n));
+    if (!(fast_rate > 0.0) || !(prf > 0.0))
+        return fail(UWB_PARAMETER_ERROR, "RadarFrame: fast_rate and prf must be positive");
+    const DetectPlan D = detect_plan(m, n, prf, *cfg);
+    if (D.cfg_status) return fail(D.cfg_status, D.cfg_msg);
+    if (D.stage_status) return fail(D.stage_status, D.stage_msg);
+    if (D.L > 8192) return fail(UWB_INVALID_ARGUMENT, "uwb: fft_length > 8192 not supported on the device path");
+    if (degenerate(cfg->cfar, m, D.kept))
+        return fail(UWB_CONFIGURATION_ERROR, "cfar2d: " + degenerate_msg(cfg->cfar, m, D.kept));
+    if (uwb_status st = need_device()) return st;
+    if (kept_out) *kept_out = D.kept;
+    if (n_records == 0) return ok();
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    uwb_map_batch b{};
+    b.maps = band;
+    b.dtype = UWB_F64;
+    b.n_maps = n_records;
+    b.rows = m;
+    b.cols = D.kept;
+    b.ld = D.kept;
+    b.map_stride = m * D.kept;
+    const Plan P = make_plan(b, &cfg->cfar, UWB_SAT_GLOBAL, 0, static_cast<int64_t>(out->det_capacity));
+    size_t off_work, off_tw, off_bad, off_cfar;
+    const uint64_t need = detect_ws_layout(n_records, m, n, D.L, P, &off_work, &off_tw, &off_bad, &off_cfar);
+    if (ws_bytes < need) return fail(UWB_INVALID_ARGUMENT, "uwb: workspace too small (need " + S(need) + ")");
+    char* ws = static_cast<char*>(workspace);
+    // twiddles (host, identical to the oracle's FFT provider) and the alpha table
+    std::vector<double> wr, wi;
+    twiddles(static_cast<int64_t>(D.L), wr, wi);
+    std::vector<double> tw(wr);
+    tw.insert(tw.end(), wi.begin(), wi.end());
+    const std::vector<double> alpha = alpha_table_host(cfg->cfar);
+    DevBuf d_alpha;
+    UWB_CUDA_TRY(d_alpha.alloc(sizeof(double) * alpha.size(), s));
+    UWB_CUDA_TRY(cudaMemcpyAsync(d_alpha.p, alpha.data(), sizeof(double) * alpha.size(), cudaMemcpyHostToDevice, s));
+    UWB_CUDA_TRY(cudaMemcpyAsync(ws + off_tw, tw.data(), sizeof(double) * tw.size(), cudaMemcpyHostToDevice, s));
+    UWB_CUDA_TRY(cudaMemsetAsync(ws + off_bad, 0xff, sizeof(uint64_t) * n_records, s));
+    // front end (pipeline.cpp:246-268): columns, then rows straight into the band maps
+    FrontendLaunch F{};
+    F.frame = records;
+    F.dtype = dtype;
+    F.m = static_cast<int64_t>(m);
+    F.n = static_cast<int64_t>(n);
+    F.n_rec = static_cast<int64_t>(n_records);
+    F.work = reinterpret_cast<double*>(ws + off_work);
+    F.first_nonfinite = reinterpret_cast<unsigned long long*>(ws + off_bad);
+    F.window = cfg->mean_filter_window;
+    F.mode = cfg->mean_filter_mode == 0 ? 0 : 1;
+    F.epsilon = cfg->normalization_epsilon;
+    F.L = static_cast<int64_t>(D.L);
+    F.wr = reinterpret_cast<const double*>(ws + off_tw);
+    F.wi = F.wr + D.L;
+    F.first_bin = static_cast<int64_t>(D.first);
+    F.kept = static_cast<int64_t>(D.kept);
+    F.band = band;
+    F.stage_mask = 3;
+    UWB_CUDA_TRY(launch_frontend_columns(F, s));
+    F.stage_mask = 4 | 8 | 16;
+    UWB_CUDA_TRY(launch_frontend_rows(F, s));
+    // CFAR over the band maps (pipeline.cpp:269-273)
+    const int backend = cfg->backend == UWB_NAIVE ? UWB_NAIVE : UWB_INTEGRAL;
+    if (uwb_status st = dev_cfar(b, cfg->cfar, d_alpha.as<double>(), backend, UWB_SAT_GLOBAL, 0, *out,
+                                 ws + off_cfar, P.total, flags & ~4u, s))
+        return st;
+    // a record's first non-finite sample (row-major over its m x n frame) is its
+    // entry 0 of first_bad (RadarFrame::validate, pipeline.cpp:27-38)
+    if (out->first_bad)
+        UWB_CUDA_TRY(cudaMemcpy2DAsync(out->first_bad, 2 * sizeof(uint64_t), ws + off_bad, sizeof(uint64_t),
+                                       sizeof(uint64_t), n_records, cudaMemcpyDeviceToDevice, s));
+    return ok();
 }
 
 uint64_t uwb_kernel_launches(void) { return g_kernel_launches.load(); }

@@ -37,8 +37,11 @@ template <typename T>
 __global__ void __launch_bounds__(128) frontend_columns_kernel(FrontendLaunch F) {
     const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (c >= F.n) return;
-    const T* x = static_cast<const T*>(F.frame);
     const int64_t m = F.m, n = F.n;
+    const int64_t rec = blockIdx.y;
+    const T* x = static_cast<const T*>(F.frame) + rec * m * n;
+    double* work = F.work + rec * m * n;
+    unsigned long long* bad = F.first_nonfinite ? F.first_nonfinite + rec : nullptr;
     const double dm = static_cast<double>(m);
 
     double mean = 0.0;
@@ -47,16 +50,16 @@ __global__ void __launch_bounds__(128) frontend_columns_kernel(FrontendLaunch F)
         for (int64_t r = 0; r < m; ++r) sum = dadd(sum, static_cast<double>(x[r * n + c]));
         mean = ddiv(sum, dm);
     }
-    if (F.first_nonfinite) {
+    if (bad) {
         for (int64_t r = 0; r < m; ++r)
             if (!isfinite(static_cast<double>(x[r * n + c])))
-                report_min(F.first_nonfinite, static_cast<unsigned long long>(r * n + c));
+                report_min(bad, static_cast<unsigned long long>(r * n + c));
     }
     const bool dc = (F.stage_mask & kStageRemoveDc) != 0;
     if (!(F.stage_mask & kStageDetrend)) {
         for (int64_t r = 0; r < m; ++r) {
             const double v = static_cast<double>(x[r * n + c]);
-            F.work[r * n + c] = dc ? dsub(v, mean) : v;
+            work[r * n + c] = dc ? dsub(v, mean) : v;
         }
         return;
     }
@@ -76,7 +79,7 @@ __global__ void __launch_bounds__(128) frontend_columns_kernel(FrontendLaunch F)
     for (int64_t r = 0; r < m; ++r) {
         const double v0 = static_cast<double>(x[r * n + c]);
         const double v = dc ? dsub(v0, mean) : v0;
-        F.work[r * n + c] = dsub(v, dadd(intercept, dmul(slope, static_cast<double>(r))));
+        work[r * n + c] = dsub(v, dadd(intercept, dmul(slope, static_cast<double>(r))));
     }
 }
 
@@ -84,8 +87,8 @@ __device__ __forceinline__ unsigned bitrev(unsigned i, int bits) { return __brev
 
 __global__ void __launch_bounds__(512) frontend_rows_kernel(FrontendLaunch F) {
     extern __shared__ double sm[];
-    const int64_t r = blockIdx.x;
     const int64_t n = F.n, L = F.L;
+    const int64_t r = static_cast<int64_t>(blockIdx.y) * F.m + blockIdx.x; // row across the batch
     double* row = sm;        // n
     double* re = sm + n;     // L
     double* im = re + L;     // L (also used as filter scratch)
@@ -205,7 +208,7 @@ __global__ void __launch_bounds__(512) frontend_rows_kernel(FrontendLaunch F) {
 } // namespace
 
 cudaError_t launch_frontend_columns(const FrontendLaunch& F, cudaStream_t stream) {
-    const unsigned blocks = static_cast<unsigned>((F.n + 127) / 128);
+    const dim3 blocks(static_cast<unsigned>((F.n + 127) / 128), static_cast<unsigned>(F.n_rec > 0 ? F.n_rec : 1));
     ++g_kernel_launches;
     if (F.dtype == UWB_F32) frontend_columns_kernel<float><<<blocks, 128, 0, stream>>>(F);
     else frontend_columns_kernel<double><<<blocks, 128, 0, stream>>>(F);
@@ -224,7 +227,8 @@ cudaError_t launch_frontend_rows(const FrontendLaunch& F, cudaStream_t stream) {
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     ++g_kernel_launches;
-    frontend_rows_kernel<<<static_cast<unsigned>(F.m), 512, smem, stream>>>(F);
+    const dim3 grid(static_cast<unsigned>(F.m), static_cast<unsigned>(F.n_rec > 0 ? F.n_rec : 1));
+    frontend_rows_kernel<<<grid, 512, smem, stream>>>(F);
     return cudaGetLastError();
 }
 

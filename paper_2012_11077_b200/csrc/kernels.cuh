@@ -160,6 +160,9 @@ struct FrontendLaunch {
     double* band;        // m x kept
     double* full_power;  // optional m x (L/2+1) (slow_time_spectrum)
     int stage_mask;      // which stages to run (see frontend.cu)
+    int64_t n_rec;       // records in the batch (0 = 1); record i's frame, work,
+                         // band and spectrum follow record i-1's densely, and its
+                         // non-finite report goes to first_nonfinite[i]
 };
 cudaError_t launch_frontend_columns(const FrontendLaunch& F, cudaStream_t stream);
 cudaError_t launch_frontend_rows(const FrontendLaunch& F, cudaStream_t stream);

@@ -202,3 +202,49 @@ def test_detect_errors_match_reference(uwb, ref, cuda):  # test_pipeline.cpp:414
             uwb.detect(F(uwb, d, prf=prf), uwb.PipelineConfig(cfar=params, **cfg))
         assert type(ge.value).__name__ == re.value.kind, cfg
         assert str(ge.value) == re.value.message
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_detect_batch_matches_reference_per_record(uwb, ref, cuda, dtype):
+    """Batched device detect: every record's band map and CFAR
+    result equal the reference detect() on that record, bit for bit."""
+    import torch
+    from paper_2012_11077_b200 import synth
+    from paper_2012_11077_b200.batch import DetectBatch
+    n_rec = 5
+    recs = torch.stack([synth.cfg2_record(seed=40 + i, device="cuda") for i in range(n_rec)])
+    recs = recs.to(getattr(torch, dtype)).contiguous()
+    config = uwb.PipelineConfig(mean_filter_window=5, fft_length=1024, band_low_hz=0.3, band_high_hz=0.8,
+                                cfar=uwb.CfarParams(1, 4, 1e-3))
+    db = DetectBatch(n_rec, 512, 1024, config, prf=20.0, dtype=recs.dtype, det_capacity=4096)
+    assert db.kept == 25
+    db(recs)
+    torch.cuda.synchronize()
+    db.check_inputs()
+    host = recs.double().cpu().numpy()
+    for i in range(n_rec):
+        exp = ref.detect(host[i], prf=20.0, mean_filter_window=5, fft_length=1024, guard_radius=1,
+                         background_radius=4, pfa=1e-3)
+        assert_bitwise(db.band[i].cpu().numpy(), exp["band_power"], f"record {i} band map")
+        assert np.array_equal(db.mask(i), exp["result"].mask), f"record {i} mask"
+        d = db.detections(i)
+        e = exp["result"].detections
+        assert len(d) == len(e)
+        assert np.array_equal(d["row"], e["row"]) and np.array_equal(d["col"], e["col"])
+        assert_bitwise(d["threshold"], e["threshold"], f"record {i} detection thresholds")
+
+
+def test_detect_batch_reports_nonfinite_record(uwb, cuda):
+    import torch
+    from paper_2012_11077_b200.batch import DetectBatch
+    recs = torch.randn((3, 64, 128), device="cuda", dtype=torch.float64)
+    recs[1, 5, 7] = float("nan")
+    config = uwb.PipelineConfig(fft_length=128, band_low_hz=0.3, band_high_hz=0.8, cfar=uwb.CfarParams(1, 2, 1e-3))
+    db = DetectBatch(3, 64, 128, config, prf=20.0, dtype=torch.float64)
+    db(recs)
+    torch.cuda.synchronize()
+    fb = db.first_bad.cpu().numpy().astype(np.uint64)
+    assert fb[1, 0] == 5 * 128 + 7
+    assert fb[0, 0] == np.uint64(0xFFFFFFFFFFFFFFFF) and fb[2, 0] == np.uint64(0xFFFFFFFFFFFFFFFF)
+    with pytest.raises(uwb.InputError):
+        db.check_inputs()
