@@ -33,6 +33,7 @@
 // a non-finite input makes every later S of its column non-finite, so each lane
 // checks its last S once per block and, the first time it is not finite,
 // rescans its own columns for the first offending row.
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 #include <type_traits>
@@ -373,6 +374,8 @@ static cudaError_t launch_sat_t(const SatLaunch& L, cudaStream_t stream) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sat_systolic_kernel<T>, kWarpsPerCta * kWarp, smem);
+    // leave room for a concurrent CFAR on another stream (UWB_SAT_CTAS_PER_SM)
+    if (const char* e = getenv("UWB_SAT_CTAS_PER_SM")) per_sm = std::min(per_sm, std::max(1, atoi(e)));
     const int64_t ctas = (n_tiles + kWarpsPerCta - 1) / kWarpsPerCta;
     const int64_t grid = imin(ctas, static_cast<int64_t>(sms) * (per_sm > 0 ? per_sm : 1));
     SatLaunch L2 = L;
