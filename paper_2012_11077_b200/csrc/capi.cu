@@ -150,6 +150,7 @@ std::string degenerate_msg(const uwb_cfar_params& p, uint64_t rows, uint64_t col
 struct Plan {
     JobGeometry geo;
     int64_t n_maps, cols, n_jobs, table_ld, table_stride, strips, max_rows, edge_stride;
+    int cpl;
     size_t off_tables, off_edge, off_prog, off_counter, off_scratch, total;
 };
 
@@ -180,7 +181,8 @@ Plan make_plan(const uwb_map_batch& b, const uwb_cfar_params* p, int sat_mode, u
     P.max_rows = P.geo.max_table_rows();
     P.table_ld = table_ld_for(P.cols);
     P.table_stride = (P.max_rows + 1) * P.table_ld;
-    P.strips = sat_strips(P.cols);
+    P.cpl = sat_cpl_for(P.n_jobs, P.cols);
+    P.strips = sat_strips(P.cols, P.cpl);
     size_t off = 0;
     auto take = [&](size_t bytes) {
         const size_t o = off;
@@ -210,6 +212,7 @@ SatLaunch sat_launch(const Plan& P, const uwb_map_batch& b, char* ws, unsigned l
     L.table_ld = P.table_ld;
     L.table_stride = P.table_stride;
     L.strips = P.strips;
+    L.cpl = P.cpl;
     L.gedge = reinterpret_cast<double*>(ws + P.off_edge);
     L.edge_stride = P.edge_stride;
     L.gprog = reinterpret_cast<unsigned*>(ws + P.off_prog);

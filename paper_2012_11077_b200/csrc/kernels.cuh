@@ -81,6 +81,7 @@ struct SatLaunch {
     bool vec_ok;         // 16-byte vector loads legal
     int elem_bytes;
     unsigned flags;      // bit 1: low-latency strip chain (set by the launcher)
+    int cpl;             // columns per lane (strips of 32 * cpl columns): 1, 2 or 4
 };
 
 struct SatJobView {
@@ -134,7 +135,8 @@ struct CfarLaunch {
 };
 
 cudaError_t launch_sat(const SatLaunch& L, int dtype, cudaStream_t stream);
-int64_t sat_strips(int64_t cols);
+int64_t sat_strips(int64_t cols, int cpl);       // strips of 32 * cpl columns
+int sat_cpl_for(int64_t n_jobs, int64_t cols);   // columns per lane for a batch
 
 cudaError_t launch_cfar_integral(const CfarLaunch& L, int dtype, cudaStream_t stream);
 cudaError_t launch_cfar_naive(const CfarLaunch& L, int dtype, cudaStream_t stream);

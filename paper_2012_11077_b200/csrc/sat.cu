@@ -45,8 +45,6 @@ namespace uwb {
 
 namespace {
 
-constexpr int kCpl = 4;                 // columns per lane
-constexpr int kStripCols = kCpl * kWarp; // 128 columns per unit of work
 constexpr int kWarpsPerCta = 4;         // independent warps per CTA
 constexpr int kAhead = 8;               // staging distance in steps (<= kXSlots - 8)
 constexpr int kXSlots = 16;             // lane-private source ring (copy steps)
@@ -56,7 +54,7 @@ constexpr int kSatCtasPerSm = 3;        // occupancy target (registers and share
 
 // Shared memory per CTA: the warps' source rings, the result rings and the
 // edge staging.
-template <typename T>
+template <typename T, int kCpl>
 struct SatSmem {
     static constexpr unsigned kXLane = kCpl * sizeof(T);              // source bytes per lane and row
     static constexpr unsigned kXSlotBytes = kWarp * kXLane;
@@ -69,11 +67,13 @@ struct SatSmem {
     }
 };
 
-// cp.async of a lane's kCpl source values (16-byte pieces; 8 bytes when that is all)
-template <typename T>
+// cp.async of a lane's kCpl source values (16-byte pieces; 4 / 8 bytes when that is all)
+template <typename T, int kCpl>
 __device__ __forceinline__ void cp_async_lane(unsigned dst, const T* src) {
     constexpr unsigned kBytes = kCpl * sizeof(T);
-    if constexpr (kBytes == 8) {
+    if constexpr (kBytes == 4) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+    } else if constexpr (kBytes == 8) {
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
     } else {
 #pragma unroll
@@ -89,8 +89,11 @@ __device__ __forceinline__ void cp_async_one(unsigned dst, const float* src) {
 __device__ __forceinline__ void cp_async_one(unsigned dst, const double* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
 }
+template <int kCpl>
 __device__ __forceinline__ void lds_lane(unsigned addr, float (&x)[kCpl]) {
-    if constexpr (kCpl == 4) {
+    if constexpr (kCpl == 1) {
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x[0]) : "r"(addr));
+    } else if constexpr (kCpl == 4) {
         asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                      : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3])
                      : "r"(addr));
@@ -100,22 +103,37 @@ __device__ __forceinline__ void lds_lane(unsigned addr, float (&x)[kCpl]) {
             asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(x[2 * q]), "=f"(x[2 * q + 1]) : "r"(addr + 8u * q));
     }
 }
+template <int kCpl>
 __device__ __forceinline__ void lds_lane(unsigned addr, double (&x)[kCpl]) {
+    if constexpr (kCpl == 1) {
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x[0]) : "r"(addr));
+    } else {
 #pragma unroll
-    for (int q = 0; q < kCpl / 2; ++q)
-        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x[2 * q]), "=d"(x[2 * q + 1]) : "r"(addr + 16u * q));
+        for (int q = 0; q < kCpl / 2; ++q)
+            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x[2 * q]), "=d"(x[2 * q + 1]) : "r"(addr + 16u * q));
+    }
 }
+template <int kCpl>
 __device__ __forceinline__ void sts_out(unsigned addr, const double (&v)[kCpl]) {
+    if constexpr (kCpl == 1) {
+        asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(v[0]) : "memory");
+    } else {
 #pragma unroll
-    for (int q = 0; q < kCpl / 2; ++q)
-        asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr + 16u * q), "d"(v[2 * q]), "d"(v[2 * q + 1])
-                     : "memory");
+        for (int q = 0; q < kCpl / 2; ++q)
+            asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr + 16u * q), "d"(v[2 * q]), "d"(v[2 * q + 1])
+                         : "memory");
+    }
 }
+template <int kCpl>
 __device__ __forceinline__ void lds_out(unsigned addr, double (&v)[kCpl]) {
+    if constexpr (kCpl == 1) {
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v[0]) : "r"(addr) : "memory");
+    } else {
 #pragma unroll
-    for (int q = 0; q < kCpl / 2; ++q)
-        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[2 * q]), "=d"(v[2 * q + 1]) : "r"(addr + 16u * q)
-                     : "memory");
+        for (int q = 0; q < kCpl / 2; ++q)
+            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[2 * q]), "=d"(v[2 * q + 1]) : "r"(addr + 16u * q)
+                         : "memory");
+    }
 }
 __device__ __forceinline__ double lds_d(unsigned addr) {
     double v;
@@ -141,11 +159,12 @@ __device__ __noinline__ int first_nonfinite(const T* src, int64_t ld, int c, int
     return INT_MAX;
 }
 
-template <typename T>
+template <typename T, int kCpl>
 __global__ void __launch_bounds__(kWarpsPerCta * kWarp, kSatCtasPerSm)
 sat_systolic_kernel(SatLaunch L) {
+    constexpr int kStripCols = kCpl * kWarp;
     extern __shared__ __align__(16) unsigned char sat_smem_raw[];
-    using SM = SatSmem<T>;
+    using SM = SatSmem<T, kCpl>;
     constexpr unsigned kXSlotBytes = SM::kXSlotBytes;
     constexpr unsigned kOSlotBytes = SM::kOSlotBytes;
     const int warp = threadIdx.x / kWarp;
@@ -212,10 +231,10 @@ sat_systolic_kernel(SatLaunch L) {
         auto stage = [&](unsigned slot_off, int row, const T* p, bool checked) {
             const unsigned dst = x_lane + slot_off;
             if (!checked) {
-                cp_async_lane<T>(dst, p);
+                cp_async_lane<T, kCpl>(dst, p);
             } else if (row >= 0 && row < rows) {
                 if (warp_fast) {
-                    cp_async_lane<T>(dst, p);
+                    cp_async_lane<T, kCpl>(dst, p);
                 } else {
                     for (int k = 0; k < nvalid; ++k) cp_async_one(dst + k * sizeof(T), p + k);
                 }
@@ -255,11 +274,15 @@ sat_systolic_kernel(SatLaunch L) {
             const int rf = s - 8 * grp - 8;
             if (!kChecked || (rf >= 0 && rf < rows)) {
                 double o[kCpl];
-                lds_out(o_lane + static_cast<unsigned>(u & (kOSlots - 1)) * kOSlotBytes, o);
+                lds_out<kCpl>(o_lane + static_cast<unsigned>(u & (kOSlots - 1)) * kOSlotBytes, o);
                 if (!kChecked || nvalid == kCpl) {
+                    if constexpr (kCpl == 1) {
+                        *tflush = o[0];
+                    } else {
 #pragma unroll
-                    for (int q = 0; q < kCpl / 2; ++q)
-                        reinterpret_cast<double2*>(tflush)[q] = make_double2(o[2 * q], o[2 * q + 1]);
+                        for (int q = 0; q < kCpl / 2; ++q)
+                            reinterpret_cast<double2*>(tflush)[q] = make_double2(o[2 * q], o[2 * q + 1]);
+                    }
                 } else {
 #pragma unroll
                     for (int k = 0; k < kCpl; ++k)
@@ -277,7 +300,7 @@ sat_systolic_kernel(SatLaunch L) {
             for (int k = 0; k < kCpl; ++k) x[k] = xn[k];
             const double from_left_strip = edge_n;
             cp_async_wait<kAhead - 1>();
-            lds_lane(x_lane + ((static_cast<unsigned>(u + 1) + x_rbase_lane) & (kXSlots - 1)) * kXSlotBytes, xn);
+            lds_lane<kCpl>(x_lane + ((static_cast<unsigned>(u + 1) + x_rbase_lane) & (kXSlots - 1)) * kXSlotBytes, xn);
             if (u + 1 < kWarp) edge_n = lds_d(edge_smem + static_cast<unsigned>(u + 1) * 8u);
             // (4) left neighbour S(r, c-1): lane l-1's newest S(., c+kCpl-1); lane 0: left strip's edge
             double left = __shfl_up_sync(0xffffffffu, last[kCpl - 1], 1);
@@ -301,7 +324,7 @@ sat_systolic_kernel(SatLaunch L) {
                 left_prev = left;
 #pragma unroll
                 for (int k = 0; k < kCpl; ++k) prev[k] = last[k] = sv[k];
-                sts_out(o_lane + ((static_cast<unsigned>(u) + o_rbase_lane) & (kOSlots - 1)) * kOSlotBytes, sv);
+                sts_out<kCpl>(o_lane + ((static_cast<unsigned>(u) + o_rbase_lane) & (kOSlots - 1)) * kOSlotBytes, sv);
             }
         };
 
@@ -312,7 +335,7 @@ sat_systolic_kernel(SatLaunch L) {
         double e_cur = fetch_left(0);
         double e_next = low_latency ? 0.0 : fetch_left(kWarp);
         cp_async_wait<kAhead - 1>();
-        lds_lane(x_lane + (x_rbase_lane & (kXSlots - 1)) * kXSlotBytes, xn);
+        lds_lane<kCpl>(x_lane + (x_rbase_lane & (kXSlots - 1)) * kXSlotBytes, xn);
         for (int s0 = 0; s0 < steps; s0 += kWarp) {
             // left-strip edge values for rows [s0, s0 + 32) (lane 0 reads row s at step s)
             __syncwarp();
@@ -359,21 +382,17 @@ sat_systolic_kernel(SatLaunch L) {
     }
 }
 
-} // namespace
-
-std::atomic<uint64_t> g_kernel_launches{0};
-
-template <typename T>
+template <typename T, int kCpl>
 static cudaError_t launch_sat_t(const SatLaunch& L, cudaStream_t stream) {
     const int64_t n_tiles = L.n_jobs * L.strips;
-    const size_t smem = SatSmem<T>::bytes();
-    cudaError_t e = cudaFuncSetAttribute(sat_systolic_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const size_t smem = SatSmem<T, kCpl>::bytes();
+    cudaError_t e = cudaFuncSetAttribute(sat_systolic_kernel<T, kCpl>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sat_systolic_kernel<T>, kWarpsPerCta * kWarp, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sat_systolic_kernel<T, kCpl>, kWarpsPerCta * kWarp, smem);
     // leave room for a concurrent CFAR on another stream (UWB_SAT_CTAS_PER_SM)
     if (const char* e = getenv("UWB_SAT_CTAS_PER_SM")) per_sm = std::min(per_sm, std::max(1, atoi(e)));
     const int64_t ctas = (n_tiles + kWarpsPerCta - 1) / kWarpsPerCta;
@@ -383,16 +402,44 @@ static cudaError_t launch_sat_t(const SatLaunch& L, cudaStream_t stream) {
     if (n_tiles < 2LL * sms * (per_sm > 0 ? per_sm : 1) * kWarpsPerCta) L2.flags |= 2u;
     if (const char* f = getenv("UWB_SAT_FLAGS")) L2.flags = static_cast<unsigned>(atoi(f));
     ++g_kernel_launches;
-    sat_systolic_kernel<T><<<static_cast<unsigned>(grid), kWarpsPerCta * kWarp, smem, stream>>>(L2);
+    sat_systolic_kernel<T, kCpl><<<static_cast<unsigned>(grid), kWarpsPerCta * kWarp, smem, stream>>>(L2);
     return cudaGetLastError();
 }
+
+template <typename T>
+static cudaError_t launch_sat_cpl(const SatLaunch& L, cudaStream_t stream) {
+    switch (L.cpl) {
+        case 1: return launch_sat_t<T, 1>(L, stream);
+        case 2: return launch_sat_t<T, 2>(L, stream);
+        default: return launch_sat_t<T, 4>(L, stream);
+    }
+}
+
+} // namespace
+
+std::atomic<uint64_t> g_kernel_launches{0};
 
 cudaError_t launch_sat(const SatLaunch& L, int dtype, cudaStream_t stream) {
     if (L.n_jobs * L.strips == 0) return cudaSuccess;
     if (L.geo.rows >= (int64_t(1) << 31) - 4096 || L.cols >= (int64_t(1) << 30)) return cudaErrorInvalidValue;
-    return dtype == UWB_F32 ? launch_sat_t<float>(L, stream) : launch_sat_t<double>(L, stream);
+    if (L.strips != sat_strips(L.cols, L.cpl)) return cudaErrorInvalidValue;
+    return dtype == UWB_F32 ? launch_sat_cpl<float>(L, stream) : launch_sat_cpl<double>(L, stream);
 }
 
-int64_t sat_strips(int64_t cols) { return (cols + kStripCols - 1) / kStripCols; }
+// Columns per lane. 4 (128-column strips) is best measured for every batch
+// shape: for large batches it needs the fewest per-cell operations, and for a
+// single map the strip chain (strips x hand-over lag + rows) is shortest with
+// the fewest strips; 32- and 64-column strips (UWB_SAT_CPL=1/2) stay available.
+int sat_cpl_for(int64_t n_jobs, int64_t cols) {
+    (void)n_jobs;
+    (void)cols;
+    if (const char* e = getenv("UWB_SAT_CPL")) {
+        const int c = atoi(e);
+        if (c == 1 || c == 2 || c == 4) return c;
+    }
+    return 4;
+}
+
+int64_t sat_strips(int64_t cols, int cpl) { return (cols + kWarp * cpl - 1) / (kWarp * cpl); }
 
 } // namespace uwb
