@@ -47,7 +47,8 @@ typedef enum uwb_status {
     UWB_CONFIGURATION_ERROR = 5, /* ConfigurationError */
     UWB_CUDA_ERROR = 6,          /* no device / launch failure */
     UWB_CAPACITY_ERROR = 7,      /* detection buffer too small (count still reported) */
-    UWB_INVALID_ARGUMENT = 8     /* null pointer / bad layout */
+    UWB_INVALID_ARGUMENT = 8,    /* null pointer / bad layout */
+    UWB_FORMAT_ERROR = 9         /* FormatError (frame files) */
 } uwb_status;
 
 typedef enum uwb_dtype { UWB_F32 = 0, UWB_F64 = 1 } uwb_dtype;
@@ -265,7 +266,29 @@ uwb_status uwb_dev_detect_batch(const void* records, int32_t dtype, uint64_t n_r
                                 uint64_t* kept_out, const uwb_cfar_outputs* out, void* workspace,
                                 uint64_t workspace_bytes, uint32_t flags, void* stream);
 
-/* Instrumentation./* Instrumentation. uwb_kernel_launches: number of kernels this library has
+/* ---- RFRM frame files (frame_io.hpp:10-23) ----
+ * uwb_rfrm_parse validates a whole file image exactly as read_frame does
+ * (frame_io.cpp:69-122: magic, version, header, 2x2 minimum, payload length,
+ * trailing bytes, RadarFrame rates; UWB_FORMAT_ERROR with the reference's
+ * message) and locates its payload. uwb_dev_rfrm_to_frames transposes n_rec
+ * payloads (each n_traces x m_samples f32, trace-major, packed back to back on
+ * the device) into range-major frames [n_rec][m][n] of out_dtype, and writes
+ * each record's first non-finite sample (row-major index, UINT64_MAX if none)
+ * to first_nonfinite[i] ("frame file: RadarFrame: non-finite sample"). */
+typedef struct uwb_rfrm_info {
+    uint32_t m_samples;
+    uint32_t n_traces;
+    double fast_rate;
+    double prf;
+    uint64_t payload_offset; /* bytes from the file start */
+    uint64_t payload_bytes;  /* m_samples * n_traces * 4 */
+} uwb_rfrm_info;
+
+uwb_status uwb_rfrm_parse(const void* file_bytes, uint64_t len, uwb_rfrm_info* info);
+uwb_status uwb_dev_rfrm_to_frames(const float* payload, uint64_t n_rec, uint64_t m_samples, uint64_t n_traces,
+                                  int32_t out_dtype, void* frames, uint64_t* first_nonfinite, void* stream);
+
+/* Instrumentation. uwb_kernel_launches: number of kernels this library has
  * launched in the process. With flags bit 1 set, uwb_dev_cfar2d records CUDA
  * events around its phases (SAT, CFAR, sort) into a 1024-slot ring without
  * synchronising; uwb_dev_phase_ms synchronises on them, writes up to max_calls

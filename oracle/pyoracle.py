@@ -27,6 +27,7 @@ KINDS = {
     3: "ParameterError",
     4: "BoundsError",
     5: "ConfigurationError",
+    7: "FormatError",
     9: "Error",
 }
 
@@ -250,6 +251,18 @@ class RefLib:
         c = _SceneConfig()
         self.lib.uwbref_default_scene_config(C.byref(c))
         return {name: getattr(c, name) for name, _ in _SceneConfig._fields_}
+
+    def read_frame(self, path: str):
+        """frame_io.cpp:69-122 read_frame_file -> (data m x n, fast_rate, prf)."""
+        m, n = C.c_uint32(), C.c_uint32()
+        fr, pr = C.c_double(), C.c_double()
+        # first call sizes the frame, second copies it
+        self._check(self.lib.uwbref_read_frame(path.encode(), None, C.c_uint64(0), C.byref(m), C.byref(n),
+                                               C.byref(fr), C.byref(pr), self.err, C.c_uint64(1024)))
+        data = np.zeros((m.value, n.value))
+        self._check(self.lib.uwbref_read_frame(path.encode(), _p(data), C.c_uint64(data.size), C.byref(m),
+                                               C.byref(n), C.byref(fr), C.byref(pr), self.err, C.c_uint64(1024)))
+        return data, fr.value, pr.value
 
     def generate_scene(self, **overrides):
         cfg = self.default_scene_config()

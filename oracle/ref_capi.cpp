@@ -22,6 +22,7 @@
 
 #include "uwbvital/cfar.hpp"
 #include "uwbvital/errors.hpp"
+#include "uwbvital/frame_io.hpp"
 #include "uwbvital/pipeline.hpp"
 #include "uwbvital/sat.hpp"
 #include "uwbvital/synth.hpp"
@@ -57,6 +58,9 @@ int guarded(char* errbuf, std::size_t errlen, F&& f) {
     } catch (const R::ConfigurationError& e) {
         put_msg(errbuf, errlen, e.what());
         return 5;
+    } catch (const R::FormatError& e) {
+        put_msg(errbuf, errlen, e.what());
+        return 7;
     } catch (const std::exception& e) {
         put_msg(errbuf, errlen, e.what());
         return 9;
@@ -355,6 +359,21 @@ int uwbref_generate_scene(const uwbref_scene_config* in, double* data, std::uint
         from_matrix(s.frame.data, data);
         *truth_bin = s.truth.target_range_bin;
         *truth_freq = s.truth.resp_freq_hz;
+    });
+}
+
+// ---- frame_io.cpp:69-122 read_frame (RFRM files) ----
+// data: m x n doubles (range-major, as RadarFrame::data) when capacity allows.
+int uwbref_read_frame(const char* path, double* data, std::uint64_t capacity, std::uint32_t* m, std::uint32_t* n,
+                      double* fast_rate, double* prf, char* errbuf, std::size_t errlen) {
+    return guarded(errbuf, errlen, [&] {
+        const R::RadarFrame f = R::read_frame_file(path);
+        *m = static_cast<std::uint32_t>(f.samples());
+        *n = static_cast<std::uint32_t>(f.traces());
+        *fast_rate = f.fast_rate;
+        *prf = f.prf;
+        if (data && capacity >= f.samples() * f.traces())
+            std::memcpy(data, f.data.values().data(), sizeof(double) * f.samples() * f.traces());
     });
 }
 

@@ -30,6 +30,7 @@ UWB_CONFIGURATION_ERROR = 5
 UWB_CUDA_ERROR = 6
 UWB_CAPACITY_ERROR = 7
 UWB_INVALID_ARGUMENT = 8
+UWB_FORMAT_ERROR = 9
 
 UWB_F32 = 0
 UWB_F64 = 1
@@ -66,6 +67,11 @@ class uwb_map_batch(C.Structure):
 class uwb_row_window(C.Structure):
     _fields_ = [("global_rows", C.c_uint64), ("buf_row0", C.c_uint64), ("row_begin", C.c_uint64),
                 ("row_end", C.c_uint64)]
+
+
+class uwb_rfrm_info(C.Structure):
+    _fields_ = [("m_samples", C.c_uint32), ("n_traces", C.c_uint32), ("fast_rate", C.c_double),
+                ("prf", C.c_double), ("payload_offset", C.c_uint64), ("payload_bytes", C.c_uint64)]
 
 
 class uwb_cfar_outputs(C.Structure):
@@ -107,6 +113,8 @@ SIGNATURES = {
     "uwb_dev_cfar2d_window": (_S, [_P, _P, _P, _P, _U64, _P, _P, _U64, C.c_uint32, _P]),
     "uwb_dev_detect_batch_workspace": (_U64, [_U64, _U64, _U64, _D, _P, _U64]),
     "uwb_dev_detect_batch": (_S, [_P, C.c_int32, _U64, _U64, _U64, _D, _D, _P, _P, _P, _P, _P, _U64, C.c_uint32, _P]),
+    "uwb_rfrm_parse": (_S, [_P, _U64, _P]),
+    "uwb_dev_rfrm_to_frames": (_S, [_P, _U64, _U64, _U64, C.c_int32, _P, _P, _P]),
     "uwb_dev_build_sat": (_S, [_P, _P, _U64, _U64, _P, _P, _U64, _P]),
     "uwb_dev_build_sat_workspace": (_U64, [_P]),
     "uwb_host_cfar2d_batch": (_S, [_P, _P, C.c_int32, _U64, _P, _P, _U64, _P, _U64]),

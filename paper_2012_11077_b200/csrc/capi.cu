@@ -1250,6 +1250,59 @@ uwb_status uwb_dev_detect_batch(const void* records, int32_t dtype, uint64_t n_r
     return ok();
 }
 
+// ---- RFRM frame files (frame_io.cpp:69-122) ---------------------------------
+
+uwb_status uwb_rfrm_parse(const void* file_bytes, uint64_t len, uwb_rfrm_info* info) {
+    if (!info || (!file_bytes && len)) return fail(UWB_INVALID_ARGUMENT, "uwb: null argument");
+    const unsigned char* b = static_cast<const unsigned char*>(file_bytes);
+    if (len < 4 || std::memcmp(b, "RFRM", 4) != 0) return fail(UWB_FORMAT_ERROR, "frame file: bad magic, expected \"RFRM\"");
+    uint64_t pos = 4;
+    auto get = [&](int bytes, uint64_t& v) { // little-endian field; false when the header is cut short
+        if (pos + static_cast<uint64_t>(bytes) > len) return false;
+        v = 0;
+        for (int i = 0; i < bytes; ++i) v |= static_cast<uint64_t>(b[pos + i]) << (8 * i);
+        pos += static_cast<uint64_t>(bytes);
+        return true;
+    };
+    uint64_t version = 0, m = 0, n = 0, fr = 0, pr = 0;
+    if (!get(2, version)) return fail(UWB_FORMAT_ERROR, "frame file: truncated header");
+    if (version != 1) return fail(UWB_FORMAT_ERROR, "frame file: unsupported version " + S(version));
+    if (!get(4, m) || !get(4, n) || !get(8, fr) || !get(8, pr))
+        return fail(UWB_FORMAT_ERROR, "frame file: truncated header");
+    if (m < 2 || n < 2)
+        return fail(UWB_FORMAT_ERROR, "frame file: header declares " + S(m) + "x" + S(n) + " frame, need at least 2x2");
+    double fast_rate, prf;
+    std::memcpy(&fast_rate, &fr, 8);
+    std::memcpy(&prf, &pr, 8);
+    const uint64_t payload = m * n * 4;
+    if (len - pos < payload)
+        return fail(UWB_FORMAT_ERROR, "frame file: truncated payload, expected " + S(payload) + " bytes");
+    if (len - pos > payload) return fail(UWB_FORMAT_ERROR, "frame file: trailing bytes after payload");
+    // RadarFrame::validate (pipeline.cpp:27-38); finiteness is checked on the device
+    if (!(fast_rate > 0.0) || !(prf > 0.0))
+        return fail(UWB_FORMAT_ERROR, "frame file: RadarFrame: fast_rate and prf must be positive");
+    info->m_samples = static_cast<uint32_t>(m);
+    info->n_traces = static_cast<uint32_t>(n);
+    info->fast_rate = fast_rate;
+    info->prf = prf;
+    info->payload_offset = pos;
+    info->payload_bytes = payload;
+    return ok();
+}
+
+uwb_status uwb_dev_rfrm_to_frames(const float* payload, uint64_t n_rec, uint64_t m, uint64_t n, int32_t out_dtype,
+                                  void* frames, uint64_t* first_nonfinite, void* stream) {
+    if ((!payload || !frames) && n_rec) return fail(UWB_INVALID_ARGUMENT, "uwb: null argument");
+    if (out_dtype != UWB_F32 && out_dtype != UWB_F64) return fail(UWB_INVALID_ARGUMENT, "uwb: bad dtype");
+    if (uwb_status st = need_device()) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (first_nonfinite && n_rec) UWB_CUDA_TRY(cudaMemsetAsync(first_nonfinite, 0xff, sizeof(uint64_t) * n_rec, s));
+    UWB_CUDA_TRY(launch_rfrm_transpose(payload, static_cast<int64_t>(n_rec), static_cast<int64_t>(m),
+                                       static_cast<int64_t>(n), out_dtype, frames,
+                                       reinterpret_cast<unsigned long long*>(first_nonfinite), s));
+    return ok();
+}
+
 uint64_t uwb_kernel_launches(void) { return g_kernel_launches.load(); }
 
 int32_t uwb_dev_phase_ms(float* out, int32_t max_calls) {

@@ -167,6 +167,9 @@ struct FrontendLaunch {
                          // non-finite report goes to first_nonfinite[i]
 };
 cudaError_t launch_frontend_columns(const FrontendLaunch& F, cudaStream_t stream);
+// RFRM payloads (trace-major f32) -> range-major frames (ingest.cu)
+cudaError_t launch_rfrm_transpose(const float* payload, int64_t n_rec, int64_t m, int64_t n, int out_dtype,
+                                  void* frames, unsigned long long* first_bad, cudaStream_t stream);
 cudaError_t launch_frontend_rows(const FrontendLaunch& F, cudaStream_t stream);
 
 } // namespace uwb

@@ -65,6 +65,7 @@ _CLASSES = {
     N.UWB_CONFIGURATION_ERROR: ConfigurationError,
     N.UWB_CUDA_ERROR: CudaError,
     N.UWB_INVALID_ARGUMENT: ValueError,
+    N.UWB_FORMAT_ERROR: FormatError,
 }
 
 
