@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(128) frontend_columns_kernel(FrontendLaunch F)
 
 __device__ __forceinline__ unsigned bitrev(unsigned i, int bits) { return __brev(i) >> (32 - bits); }
 
-__global__ void __launch_bounds__(512) frontend_rows_kernel(FrontendLaunch F) {
+__global__ void __launch_bounds__(256) frontend_rows_kernel(FrontendLaunch F) {
     extern __shared__ double sm[];
     const int64_t n = F.n, L = F.L;
     const int64_t r = static_cast<int64_t>(blockIdx.y) * F.m + blockIdx.x; // row across the batch
@@ -161,13 +161,16 @@ __global__ void __launch_bounds__(512) frontend_rows_kernel(FrontendLaunch F) {
         __syncthreads();
         for (int64_t i = threadIdx.x; i < L; i += blockDim.x) im[i] = 0.0;
         __syncthreads();
-        for (int64_t len = 2; len <= L; len <<= 1) {
-            const int64_t half = len >> 1, step = L / len;
-            for (int64_t b = threadIdx.x; b < L / 2; b += blockDim.x) {
-                const int64_t j = b % half;
-                const int64_t p = (b / half) * len + j;
-                const int64_t q = p + half;
-                const double w_r = F.wr[j * step], w_i = F.wi[j * step];
+        // stage with half-length 2^lh: butterfly b pairs p = (b >> lh) * 2^(lh+1) + j and
+        // p + 2^lh, j = b mod 2^lh, twiddle j * (L >> (lh + 1)) (powers of two: shifts)
+        for (int lh = 0; lh < bits; ++lh) {
+            const int half = 1 << lh;
+            const int tw_shift = bits - lh - 1;
+            for (int b = threadIdx.x; b < (1 << (bits - 1)); b += blockDim.x) {
+                const int j = b & (half - 1);
+                const int p = ((b >> lh) << (lh + 1)) + j;
+                const int q = p + half;
+                const double w_r = __ldg(F.wr + (j << tw_shift)), w_i = __ldg(F.wi + (j << tw_shift));
                 const double br = re[q], bi = im[q];
                 const double tr = dsub(dmul(w_r, br), dmul(w_i, bi));
                 const double ti = dadd(dmul(w_r, bi), dmul(w_i, br));
@@ -228,7 +231,7 @@ cudaError_t launch_frontend_rows(const FrontendLaunch& F, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
     ++g_kernel_launches;
     const dim3 grid(static_cast<unsigned>(F.m), static_cast<unsigned>(F.n_rec > 0 ? F.n_rec : 1));
-    frontend_rows_kernel<<<grid, 512, smem, stream>>>(F);
+    frontend_rows_kernel<<<grid, 256, smem, stream>>>(F);
     return cudaGetLastError();
 }
 
