@@ -579,8 +579,7 @@ cudaError_t go(const CfarLaunch& L0, cudaStream_t stream) {
 }
 
 template <typename T, int BOXC>
-cudaError_t go_ncw(const CfarLaunch& L, int ncw, cudaStream_t stream) {
-    (void)ncw;
+cudaError_t go_occ(const CfarLaunch& L, cudaStream_t stream) {
     // The most CTAs per SM whose rings fit with one group of look-ahead, then
     // the deepest look-ahead that still fits at that occupancy (measured: CTAs
     // per SM matter more than look-ahead). UWB_RING_OCC pins the occupancy.
@@ -609,12 +608,12 @@ cudaError_t go_ncw(const CfarLaunch& L, int ncw, cudaStream_t stream) {
 }
 
 template <typename T>
-cudaError_t go_cfg(const CfarLaunch& L, int ncw, int boxc, cudaStream_t stream) {
+cudaError_t go_cfg(const CfarLaunch& L, int boxc, cudaStream_t stream) {
     switch (boxc) {
-        case 152: return go_ncw<T, 152>(L, ncw, stream);
-        case 160: return go_ncw<T, 160>(L, ncw, stream);
-        case 204: return go_ncw<T, 204>(L, ncw, stream);
-        default: return go_ncw<T, 256>(L, ncw, stream);
+        case 152: return go_occ<T, 152>(L, stream);
+        case 160: return go_occ<T, 160>(L, stream);
+        case 204: return go_occ<T, 204>(L, stream);
+        default: return go_occ<T, 256>(L, stream);
     }
 }
 
@@ -635,9 +634,7 @@ cudaError_t launch_cfar_ring(const CfarLaunch& L, int dtype, cudaStream_t stream
     const int need = kW + 2 * L.hc + 4;
     const int boxc = need <= 152 ? 152 : need <= 160 ? 160 : need <= 204 ? 204 : need <= 256 ? 256 : 0;
     if (!boxc) return cudaErrorNotSupported;
-    int ncw = 4;
-    if (const char* a = getenv("UWB_RING_NCW")) ncw = atoi(a) == 2 ? 2 : 4;
-    return f32 ? go_cfg<float>(L, ncw, boxc, stream) : go_cfg<double>(L, ncw, boxc, stream);
+    return f32 ? go_cfg<float>(L, boxc, stream) : go_cfg<double>(L, boxc, stream);
 }
 
 } // namespace uwb
