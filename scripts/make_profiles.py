@@ -59,6 +59,14 @@ def main():
             n, ns = agg[k]
             share = f"{100 * ns / tot:.1f}%" if k in ours else "-"
             f.write(f"| `{k}` | {n} | {ns / 1e6:.3f} | {share} |\n")
+    # the raw launch list of the library's kernels (ncu CSV rows, unmodified)
+    src = os.path.join(ROOT, "gpurun_out", f"launches_{tag}.csv")
+    lines = [l for l in open(src) if l.startswith('"')]
+    with open(os.path.join(ROOT, "profiles", f"{tag}_launches.csv"), "w") as f:
+        f.write(lines[0])
+        for l in lines[1:]:
+            if OURS.search(l):
+                f.write(l)
     full = summarize(os.path.join(ROOT, "gpurun_out", f"prof_{tag}.ncu-rep"))
     js = {}
     with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_full.txt"), "w") as f:
