@@ -304,12 +304,32 @@ uwb_status dev_cfar(const uwb_map_batch& b, const uwb_cfar_params& p, const doub
     if (o.first_bad) UWB_CUDA_TRY(cudaMemsetAsync(o.first_bad, 0xff, sizeof(uint64_t) * 2 * b.n_maps, s));
     if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[0], s));
     if (backend == UWB_INTEGRAL) {
-        if (!(flags & 4u)) { // bit 2: the workspace already holds this batch's tables
+        bool fused = false;
+        if (!(flags & (4u | 16u))) {
+            // bit 2 clear and bit 4 clear: no table is kept, so SAT and CFAR run
+            // as one kernel with the table on chip (falls through when the
+            // geometry does not qualify)
             const SatLaunch SL = sat_launch(P, b, ws, reinterpret_cast<unsigned long long*>(o.first_bad));
-            UWB_CUDA_TRY(run_sat(P, SL, b.dtype, s));
+            UWB_CUDA_TRY(cudaMemsetAsync(SL.gprog, 0, sizeof(unsigned) * P.n_jobs * P.strips, s));
+            UWB_CUDA_TRY(cudaMemsetAsync(SL.tile_counter, 0, sizeof(unsigned), s));
+            if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[1], s));
+            const cudaError_t e = launch_cfar_fused(SL, cfar_launch(P, b, p, alpha, ws, o), b.dtype, s);
+            if (e == cudaSuccess) {
+                fused = true;
+            } else if (e != cudaErrorNotSupported) {
+                return set_cuda_error(e, "launch_cfar_fused");
+            } else {
+                cudaGetLastError();
+            }
         }
-        if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[1], s));
-        UWB_CUDA_TRY(launch_cfar_integral(cfar_launch(P, b, p, alpha, ws, o), b.dtype, s));
+        if (!fused) {
+            if (!(flags & 4u)) { // bit 2: the workspace already holds this batch's tables
+                const SatLaunch SL = sat_launch(P, b, ws, reinterpret_cast<unsigned long long*>(o.first_bad));
+                UWB_CUDA_TRY(run_sat(P, SL, b.dtype, s));
+            }
+            if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[1], s));
+            UWB_CUDA_TRY(launch_cfar_integral(cfar_launch(P, b, p, alpha, ws, o), b.dtype, s));
+        }
     } else {
         if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[1], s));
         UWB_CUDA_TRY(launch_cfar_naive(cfar_launch(P, b, p, alpha, nullptr, o), b.dtype, s));

@@ -6,6 +6,7 @@
 // association, and the library is compiled with --fmad=false as a second guard.
 #pragma once
 
+#include <climits>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -48,6 +49,18 @@ __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// First non-finite cell (row-major) of columns [c, c + n) in source rows [0, rows_end).
+template <typename T>
+__device__ __noinline__ int first_nonfinite(const T* src, int64_t ld, int c, int n, int rows_end, int* col) {
+    for (int r = 0; r < rows_end; ++r)
+        for (int k = 0; k < n; ++k)
+            if (!isfinite(widen(src[static_cast<int64_t>(r) * ld + c + k]))) {
+                *col = c + k;
+                return r;
+            }
+    return INT_MAX;
+}
+
 // ---- mbarrier + bulk async copy (TMA engine, 1-D form) ----
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -86,6 +99,35 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         : "memory");
 }
 
+// Blocking parity wait on a shared-window address; the thread may be suspended
+// in the barrier unit for up to kHintNs per try.
+template <unsigned kHintNs>
+__device__ __forceinline__ void mbar_wait_u(unsigned bar, unsigned parity) {
+    if constexpr (kHintNs == 0) {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "UWB_WAITZ_%=:\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+            "@!p bra UWB_WAITZ_%=;\n"
+            "}\n" ::"r"(bar),
+            "r"(parity)
+            : "memory");
+        return;
+    }
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "UWB_WAITU_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra UWB_WAITU_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity), "n"(kHintNs)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_u(unsigned bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
 // ---- cp.async (LDGSTS) small copies ----
 __device__ __forceinline__ void cp_async_4(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");

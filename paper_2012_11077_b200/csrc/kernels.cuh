@@ -139,6 +139,9 @@ int64_t sat_strips(int64_t cols, int cpl);       // strips of 32 * cpl columns
 int sat_cpl_for(int64_t n_jobs, int64_t cols);   // columns per lane for a batch
 
 cudaError_t launch_cfar_integral(const CfarLaunch& L, int dtype, cudaStream_t stream);
+// SAT + CFAR in one kernel, table kept on chip (cfar_fused.cu). Whole-map
+// batches only; cudaErrorNotSupported when the geometry does not qualify.
+cudaError_t launch_cfar_fused(const SatLaunch& S, const CfarLaunch& C, int dtype, cudaStream_t stream);
 cudaError_t launch_cfar_naive(const CfarLaunch& L, int dtype, cudaStream_t stream);
 // Sort each map's detection list: value desc, row asc, col asc (cfar.cpp:170-173).
 cudaError_t launch_sort_detections(uwb_detection* dets, int64_t cap,

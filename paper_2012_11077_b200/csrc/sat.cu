@@ -147,18 +147,6 @@ __device__ __noinline__ void publish_rows(unsigned* prog, int rows_done, int lan
     __syncwarp();
 }
 
-// First non-finite cell (row-major) of columns [c, c + n) in source rows [0, rows_end).
-template <typename T>
-__device__ __noinline__ int first_nonfinite(const T* src, int64_t ld, int c, int n, int rows_end, int* col) {
-    for (int r = 0; r < rows_end; ++r)
-        for (int k = 0; k < n; ++k)
-            if (!isfinite(widen(src[static_cast<int64_t>(r) * ld + c + k]))) {
-                *col = c + k;
-                return r;
-            }
-    return INT_MAX;
-}
-
 template <typename T, int kCpl>
 __global__ void __launch_bounds__(kWarpsPerCta * kWarp, kSatCtasPerSm)
 sat_systolic_kernel(SatLaunch L) {

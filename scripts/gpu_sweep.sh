@@ -1,2 +1,6 @@
-for c in 4 2; do echo "tests with UWB_SAT_CPL=$c"; UWB_SAT_CPL=$c timeout -s KILL 600 python -m pytest tests/test_gpu_sat_cfar.py tests/test_gpu_batch.py tests/test_gpu_frontend.py -x -q 2>&1 | tail -1; done
-for c in 3 4 5 1 6; do timeout -s KILL 600 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --e2e-steps 1 2>&1 | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print($c, round(d['value'],3), d['unit'], d.get('ms_per_step'), d.get('phases_ms'), [ (r['gpu_naive_ms'], r['gpu_integral_ms']) for r in d.get('table', [])])"; done
+# scratch sweep of the fused kernel (cfar phase = fused kernel)
+export PYTHONPATH=. MAPS=1024
+echo -n "base: "; python scripts/cfar_probe.py 2>&1 | tail -1
+echo -n "base consumers idle: "; UWB_FUSED_DEBUG=1 python scripts/cfar_probe.py 2>&1 | tail -1
+echo -n "occ1 ring 160: "; UWB_FUSED_OCC=1 UWB_FUSED_RING=160 python scripts/cfar_probe.py 2>&1 | tail -1
+echo -n "occ1 ring 160 consumers idle: "; UWB_FUSED_DEBUG=1 UWB_FUSED_OCC=1 UWB_FUSED_RING=160 python scripts/cfar_probe.py 2>&1 | tail -1

@@ -215,7 +215,7 @@ def test_reused_tables_match_fresh_call(uwb, oracle, cuda):
     a = BatchCfar(2, 600, 500, pa, torch.float32, det_capacity=8192, want_mask_u8=True, want_thresholds=True)
     b = BatchCfar(2, 600, 500, pb, torch.float32, det_capacity=8192, want_mask_u8=True, want_thresholds=True,
                   workspace=a.workspace)
-    a(maps)
+    a(maps, keep_tables=True)
     b(maps, reuse_tables=True)
     torch.cuda.synchronize()
     host = maps.double().cpu().numpy()
