@@ -45,8 +45,9 @@ namespace {
 constexpr int kBandOut = 128;   // output columns per band (unit)
 constexpr int kNcw = 4;         // CFAR warps (one column x 4 rows per thread per step)
 constexpr int kRs = 4;          // output rows per CFAR step (= ring group)
-constexpr int kFAhead = 8;      // SAT source staging distance (steps)
-constexpr int kFXSlots = 16;    // lane-private source ring (copy steps)
+constexpr int kFAhead = 6;      // SAT source staging distance (steps)
+constexpr int kFXSlots = 8;     // lane-private source ring (copy steps)
+constexpr int kMirror = kRs - 1; // ring slots mirrored past the end (4 consecutive slots stay contiguous)
 constexpr int kFPublish = 64;   // SAT steps between edge hand-overs
 constexpr int kFL2Ahead = 24;   // source rows are prefetched into L2 this many steps before staging
 #ifndef UWB_FUSED_HINT
@@ -73,9 +74,9 @@ struct FusedSmem {
     static constexpr unsigned kXLane = kCpl * sizeof(T);
     static constexpr unsigned kXSlotBytes = kWarp * kXLane;
     static constexpr unsigned kXRing = kFXSlots * kXSlotBytes;
-    // ring (+4 mirror rows), source ring, edge staging, unit queue, barriers
+    // ring (+ mirror rows), source ring, edge staging, unit queue, barriers
     static size_t bytes(int nr) {
-        return 128 + static_cast<size_t>(nr + kRs) * kRowBytes + kXRing + kWarp * 8 + 16 + 8 * 4 +
+        return 128 + static_cast<size_t>(nr + kMirror) * kRowBytes + kXRing + kWarp * 8 + 16 + 8 * 4 +
                2 * 8 * static_cast<size_t>(nr / kRs);
     }
 };
@@ -120,13 +121,14 @@ template <typename T, int kCpl, int OCC>
 __global__ void __launch_bounds__((kNcw + 1) * kWarp, OCC) cfar_fused_kernel(const __grid_constant__ FusedLaunch F) {
     using SM = FusedSmem<T, kCpl>;
     constexpr unsigned kRowBytes = SM::kRowBytes;
+    constexpr int kSlotElems = kWarp * kCpl; // doubles per ring slot
     static_assert(kWarp * kCpl >= kBandOut + 1, "band");
     extern __shared__ unsigned char fz_raw[];
     const unsigned raw = smem_u32(fz_raw);
     const unsigned base = (raw + 127u) & ~127u;
     const int nr = F.nr, nq = F.nr / kRs;
     const unsigned ring_u = base;
-    const unsigned xring_u = ring_u + static_cast<unsigned>(nr + kRs) * kRowBytes;
+    const unsigned xring_u = ring_u + static_cast<unsigned>(nr + kMirror) * kRowBytes;
     const unsigned edge_u = xring_u + SM::kXRing;
     const unsigned unitq_u = edge_u + kWarp * 8u;      // 2 unit ids (+ pad)
     const unsigned ubar_u = unitq_u + 16u;             // unit_full[2], unit_empty[2]
@@ -149,22 +151,20 @@ __global__ void __launch_bounds__((kNcw + 1) * kWarp, OCC) cfar_fused_kernel(con
     __syncthreads();
     const int rows = static_cast<int>(L.geo.rows), cols = static_cast<int>(L.cols);
     const int hr = L.hr, hc = L.hc, gr = L.gr, gc = L.gc;
-    const int groups = (rows + 1 + kRs - 1) / kRs; // ring groups per unit (padded rows 0..rows)
-    const int vstep = (kRs * groups) % nr;         // ring rows a unit advances the slot base by
+    // ring slots of a unit: SAT steps -1 .. rows + 30 write slots 0 .. rows + 31
+    const int groups = (rows + kWarp + kRs - 1) / kRs;
+    const int vstep = (kRs * groups) % nr;
 
     if (warp == kNcw) {
         // ============================== SAT warp ==============================
-        const int grp = lane >> 3;
-        const unsigned x_lane = xring_u + lane * SM::kXLane;
         // generic views for plain shared loads / stores (the compiler may schedule them)
         double* ring_w = reinterpret_cast<double*>(fz_raw + (base - raw)) + kCpl * lane; // my columns, slot 0
         const T* x_w = reinterpret_cast<const T*>(fz_raw + (xring_u - raw)) + kCpl * lane;
-        constexpr int kSlotElems = kWarp * kCpl;
-        const unsigned x_rbase_lane = static_cast<unsigned>(2 * kFXSlots - kFAhead - (lane & 7));
+        const unsigned x_lane = xring_u + lane * SM::kXLane;
         constexpr int kEdgeLane = (kBandOut - 1) / kCpl, kEdgeK = (kBandOut - 1) % kCpl;
         unsigned eslot = 0, epar = 1; // next "empty" group to wait for (first pass passes)
         unsigned fslot = 0;           // next "full" group to arrive on
-        int vb = 0;                   // ring slot of the unit's padded row 0
+        int vb = 0;                   // ring slot of the unit's slot 0
         for (int k = 0;; ++k) {
             // claim a unit and hand it to the CFAR warps (2-deep queue)
             long long unit = 0;
@@ -204,13 +204,15 @@ __global__ void __launch_bounds__((kNcw + 1) * kWarp, OCC) cfar_fused_kernel(con
                     for (int sl = 0; sl < kFXSlots; ++sl)
                         sts_zero(x_lane + sl * SM::kXSlotBytes + j * sizeof(T), static_cast<T*>(nullptr));
 
-            // padded row 0 is zero (first group of the unit)
+            // slot 0 (pre-step -1): lane 0's part of padded row 0
             mbar_wait_u<kFHint>(empty_u + 8u * eslot, epar);
             if (++eslot == static_cast<unsigned>(nq)) { eslot = 0; epar ^= 1; }
+            if (lane == 0) {
 #pragma unroll
-            for (int j = 0; j < kCpl; ++j) {
-                st_shared_f64(ring_u + vb * kRowBytes + (kCpl * lane + j) * 8u, 0.0);
-                if (vb == 0) st_shared_f64(ring_u + nr * kRowBytes + (kCpl * lane + j) * 8u, 0.0);
+                for (int j = 0; j < kCpl; ++j) {
+                    ring_w[vb * kSlotElems + j] = 0.0;
+                    if (vb < kMirror) ring_w[(nr + vb) * kSlotElems + j] = 0.0;
+                }
             }
 
             unsigned avail = 0;
@@ -227,14 +229,15 @@ __global__ void __launch_bounds__((kNcw + 1) * kWarp, OCC) cfar_fused_kernel(con
                 }
                 return v;
             };
-            // group g stages at step s source row s + kFAhead - 8g
-            const T* xrow = map0 + mc + static_cast<int64_t>(kFAhead - 8 * grp) * ld;
+            // lane l stages at step s its own columns of source row s + kFAhead - l
+            const T* xrow = map0 + mc + static_cast<int64_t>(kFAhead - lane) * ld;
             // the band's source row segment, 16-byte aligned inside the row, for the L2 prefetch
             const char* pf_row;
             unsigned pf_bytes;
             {
                 const int64_t lo = static_cast<int64_t>(max(0, jb - 1)) * static_cast<int64_t>(sizeof(T));
-                const int64_t hi = static_cast<int64_t>(min(cols, jb - 1 + kWarp * kCpl)) * static_cast<int64_t>(sizeof(T));
+                const int64_t hi =
+                    static_cast<int64_t>(min(cols, jb - 1 + kWarp * kCpl)) * static_cast<int64_t>(sizeof(T));
                 const char* row0 = reinterpret_cast<const char*>(map0);
                 const uintptr_t a0 = (reinterpret_cast<uintptr_t>(row0 + lo)) & ~static_cast<uintptr_t>(15);
                 const uintptr_t a1 = (reinterpret_cast<uintptr_t>(row0 + hi)) & ~static_cast<uintptr_t>(15);
@@ -254,8 +257,8 @@ __global__ void __launch_bounds__((kNcw + 1) * kWarp, OCC) cfar_fused_kernel(con
                     bulk_prefetch_l2(pf_row + (r - kFAhead - kFL2Ahead) * ld * static_cast<int64_t>(sizeof(T)), pf_bytes);
 #pragma unroll
             for (int v = -kFAhead; v < 0; ++v) {
-                stage(static_cast<unsigned>(((v + kFXSlots) & (kFXSlots - 1)) * SM::kXSlotBytes),
-                      v + kFAhead - 8 * grp, xrow + static_cast<int64_t>(v) * ld, true);
+                stage(static_cast<unsigned>(((v + kFXSlots) & (kFXSlots - 1)) * SM::kXSlotBytes), v + kFAhead - lane,
+                      xrow + static_cast<int64_t>(v) * ld, true);
                 cp_async_commit();
             }
 
@@ -265,8 +268,8 @@ __global__ void __launch_bounds__((kNcw + 1) * kWarp, OCC) cfar_fused_kernel(con
             double left_prev = 0.0;
             bool scanned = false;
             const int steps = rows + kWarp - 1;
-            // ring slot of the padded row I write at step s: vb + s - lane + 1
-            int wslot = ((vb + 1 - lane) % nr + nr) % nr;
+            // every lane writes slot vb + s + 1 at step s (its padded row s - lane + 1)
+            int wslot = vb + 1 >= nr ? vb + 1 - nr : vb + 1;
             T xn[kCpl];
             double edge_n = 0.0;
 
@@ -274,27 +277,27 @@ __global__ void __launch_bounds__((kNcw + 1) * kWarp, OCC) cfar_fused_kernel(con
                 constexpr bool kChecked = decltype(checked_tag)::value;
                 const int s = s0 + uu;
                 const int r = s - lane;
-                // (0) lane 0 starts padded row s + 1; a new ring group every 4 rows
-                if ((uu & 3) == 3 && (!kChecked || s + 1 <= rows)) {
+                // (0) slot vb + s + 1 opens a new ring group every 4 steps
+                if ((uu & 3) == 3) {
                     mbar_wait_u<kFHint>(empty_u + 8u * eslot, epar);
                     if (++eslot == static_cast<unsigned>(nq)) { eslot = 0; epar ^= 1; }
                 }
                 // (1a) L2 prefetch of source row s + kFAhead + kFL2Ahead (one lane)
                 if (pf_ok && s + kFAhead + kFL2Ahead < rows) bulk_prefetch_l2(pf_row, pf_bytes);
                 pf_row += ld * static_cast<int64_t>(sizeof(T));
-                // (1) stage source row s + kFAhead - 8g into slot s mod 16
-                stage(static_cast<unsigned>((uu & (kFXSlots - 1)) * SM::kXSlotBytes), s + kFAhead - 8 * grp, xrow,
+                // (1) stage my source row s + kFAhead - lane into slot s mod kFXSlots
+                stage(static_cast<unsigned>((uu & (kFXSlots - 1)) * SM::kXSlotBytes), s + kFAhead - lane, xrow,
                       kChecked);
                 cp_async_commit();
                 xrow += ld;
-                // (2) this step's inputs were loaded one step ahead
+                // (2) this step's inputs were loaded one step ahead (copied at step s - kFAhead)
                 T x[kCpl];
 #pragma unroll
                 for (int j = 0; j < kCpl; ++j) x[j] = xn[j];
                 const double from_left = edge_n;
                 cp_async_wait<kFAhead - 1>();
                 {
-                    const T* a = x_w + ((static_cast<unsigned>(uu + 1) + x_rbase_lane) & (kFXSlots - 1)) * kSlotElems;
+                    const T* a = x_w + ((uu + 1 - kFAhead + kFXSlots) & (kFXSlots - 1)) * kSlotElems;
 #pragma unroll
                     for (int j = 0; j < kCpl; ++j) xn[j] = a[j];
                 }
@@ -308,11 +311,11 @@ __global__ void __launch_bounds__((kNcw + 1) * kWarp, OCC) cfar_fused_kernel(con
 #pragma unroll
                 for (int j = 1; j < kCpl; ++j) sv[j] = dsub(dadd(dadd(widen(x[j]), prev[j]), sv[j - 1]), prev[j - 1]);
                 const bool act = !kChecked || (r >= 0 && r < rows);
+                double* dst = ring_w + wslot * kSlotElems;
                 if (act) {
-                    double* dst = ring_w + wslot * kSlotElems;
 #pragma unroll
                     for (int j = 0; j < kCpl; ++j) dst[j] = sv[j];
-                    if (wslot < kRs) {
+                    if (wslot < kMirror) {
 #pragma unroll
                         for (int j = 0; j < kCpl; ++j) dst[nr * kSlotElems + j] = sv[j];
                     }
@@ -320,12 +323,17 @@ __global__ void __launch_bounds__((kNcw + 1) * kWarp, OCC) cfar_fused_kernel(con
                     left_prev = left;
 #pragma unroll
                     for (int j = 0; j < kCpl; ++j) prev[j] = last[j] = sv[j];
+                } else if (kChecked && r == -1) { // my part of padded row 0
+#pragma unroll
+                    for (int j = 0; j < kCpl; ++j) dst[j] = 0.0;
+                    if (wslot < kMirror) {
+#pragma unroll
+                        for (int j = 0; j < kCpl; ++j) dst[nr * kSlotElems + j] = 0.0;
+                    }
                 }
                 if (++wslot == nr) wslot = 0;
-                // (5) lane 31 finished padded row s - 30: close its group
-                const int p31 = s - (kWarp - 2);
-                const bool close = kChecked ? (p31 >= 1 && p31 <= rows && ((p31 & 3) == 3 || p31 == rows))
-                                            : (uu & 3) == 1;
+                // (5) close the group of slot vb + s + 1
+                const bool close = kChecked ? ((uu & 3) == 2 || s == steps - 1) : (uu & 3) == 2;
                 if (close) {
                     mbar_arrive_u(full_u + 8u * fslot);
                     if (++fslot == static_cast<unsigned>(nq)) fslot = 0;
@@ -336,7 +344,7 @@ __global__ void __launch_bounds__((kNcw + 1) * kWarp, OCC) cfar_fused_kernel(con
             double e_next = fetch_left(kWarp);
             cp_async_wait<kFAhead - 1>();
             {
-                const T* a = x_w + (x_rbase_lane & (kFXSlots - 1)) * kSlotElems;
+                const T* a = x_w + ((kFXSlots - kFAhead) & (kFXSlots - 1)) * kSlotElems;
 #pragma unroll
                 for (int j = 0; j < kCpl; ++j) xn[j] = a[j];
             }
@@ -380,8 +388,11 @@ __global__ void __launch_bounds__((kNcw + 1) * kWarp, OCC) cfar_fused_kernel(con
     }
 
     // ============================== CFAR warps ==============================
+    // Ring slot of table entry (padded row i, band column t): vb + i + t / kCpl
+    // (the SAT lane owning column t wrote it at step i + t / kCpl - 1).
     const bool per_cell = L.thresholds != nullptr || L.mask_u8 != nullptr;
     const char* ring = reinterpret_cast<const char*>(fz_raw) + (base - raw); // generic view of the ring
+    const unsigned ring_bytes = static_cast<unsigned>(nr) * kRowBytes;
     unsigned wslot = 0, wpar = 0; // next "full" group to wait for
     unsigned rslot = 0;           // next "empty" group to hand back
     int vb = 0;
@@ -406,12 +417,17 @@ __global__ void __launch_bounds__((kNcw + 1) * kWarp, OCC) cfar_fused_kernel(con
         const int c = wc0 + lane;
         const ColConst K = col_const(c, cols, hc, gc, jb + kTabShift);
         const bool okc[1] = {K.ok};
-        // Rows with unclamped windows take the fast path in every column: the
-        // clamped column edges are in K, and n is constant down a column there
-        // (cfar.cpp:28-32 with full-height windows).
+        // SAT lanes of my four tap columns, and the warp's lane range
+        const int l_xa = static_cast<int>(K.xa / 8u) / kCpl, l_xb = static_cast<int>(K.xb / 8u) / kCpl;
+        const int l_ya = static_cast<int>(K.ya / 8u) / kCpl, l_yb = static_cast<int>(K.yb / 8u) / kCpl;
+        const int l_hi = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(l_xb));
+        const int l_lo = static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(l_xa)));
         // a warp right of the map only keeps the barrier protocol (so does every
         // warp under the UWB_FUSED_DEBUG=1 probe)
         const bool warp_live = wc0 < cols && !(L.debug & 1u);
+        // Rows with unclamped windows take the fast path in every column: the
+        // clamped column edges are in K, and n is constant down a column there
+        // (cfar.cpp:28-32 with full-height windows).
         const bool fast_cols = !per_cell;
         const int n_col = (2 * hr + 1) * K.ow - (2 * gr + 1) * K.gw;
         const double alpha_col = n_col > 0 ? __ldg(L.alpha + n_col) : 0.0;
@@ -420,7 +436,19 @@ __global__ void __launch_bounds__((kNcw + 1) * kWarp, OCC) cfar_fused_kernel(con
         const T* cp = static_cast<const T*>(L.maps) + map * L.map_stride + (K.ok ? c : 0); // CUT, row r0 + 4
         uint32_t* mrow = L.mask_bits ? L.mask_bits + map * L.mask_map_stride + (wc0 >> 5) : nullptr;
         auto slot_of = [&](int i) { return ((vb + i) % nr + nr) % nr; };
-        int sA = slot_of(-hr), sB = slot_of(hr + 1), sC = slot_of(-gr), sD = slot_of(gr + 1);
+        auto tap_at = [&](int i, unsigned xoff, int lt) {
+            return *reinterpret_cast<const double*>(ring + static_cast<unsigned>(slot_of(i + lt)) * kRowBytes + xoff);
+        };
+        // fast-path tap pointers: window rows A = r0 - hr, B = r0 + hr + 1, C = r0 - gr, D = r0 + gr + 1
+        auto wrap = [&](unsigned o) { return o >= ring_bytes ? o - ring_bytes : o; };
+        unsigned oAa = wrap(static_cast<unsigned>(slot_of(-hr + l_xa)) * kRowBytes);
+        unsigned oAb = wrap(static_cast<unsigned>(slot_of(-hr + l_xb)) * kRowBytes);
+        unsigned oBa = wrap(static_cast<unsigned>(slot_of(hr + 1 + l_xa)) * kRowBytes);
+        unsigned oBb = wrap(static_cast<unsigned>(slot_of(hr + 1 + l_xb)) * kRowBytes);
+        unsigned oCa = wrap(static_cast<unsigned>(slot_of(-gr + l_ya)) * kRowBytes);
+        unsigned oCb = wrap(static_cast<unsigned>(slot_of(-gr + l_yb)) * kRowBytes);
+        unsigned oDa = wrap(static_cast<unsigned>(slot_of(gr + 1 + l_ya)) * kRowBytes);
+        unsigned oDb = wrap(static_cast<unsigned>(slot_of(gr + 1 + l_yb)) * kRowBytes);
         int waited = -1, released = -1; // unit groups known full / handed back
         int ncache = -1;
         double kcache = 0.0;
@@ -434,7 +462,8 @@ __global__ void __launch_bounds__((kNcw + 1) * kWarp, OCC) cfar_fused_kernel(con
             const int r0 = step * kRs;
             const int r_last = min(r0 + kRs, rows) - 1;
             {
-                const int need = min(rows, r_last + hr + 1) / kRs;
+                // newest entry read: padded row min(rows, r_last + hr + 1) in SAT lane l_hi
+                const int need = (min(rows, r_last + hr + 1) + l_hi) / kRs;
                 while (waited < need) {
                     mbar_wait_u<kFHint>(full_u + 8u * wslot, wpar);
                     ++waited;
@@ -458,19 +487,21 @@ __global__ void __launch_bounds__((kNcw + 1) * kWarp, OCC) cfar_fused_kernel(con
             if (!warp_live) {
                 // nothing to evaluate
             } else if (fast_cols && step >= t_fast_lo && step < t_fast_hi) {
-                const char* pA = ring + static_cast<unsigned>(sA) * kRowBytes;
-                const char* pB = ring + static_cast<unsigned>(sB) * kRowBytes;
-                const char* pC = ring + static_cast<unsigned>(sC) * kRowBytes;
-                const char* pD = ring + static_cast<unsigned>(sD) * kRowBytes;
+                const char* pAa = ring + oAa + K.xa;
+                const char* pAb = ring + oAb + K.xb;
+                const char* pBa = ring + oBa + K.xa;
+                const char* pBb = ring + oBb + K.xb;
+                const char* pCa = ring + oCa + K.ya;
+                const char* pCb = ring + oCb + K.yb;
+                const char* pDa = ring + oDa + K.ya;
+                const char* pDb = ring + oDb + K.yb;
                 double sum[kRs];
                 bool need = false;
 #pragma unroll
                 for (int kk = 0; kk < kRs; ++kk) {
                     const unsigned o = kk * kRowBytes;
-                    const double rs_o = dsub(dadd(tap(pA, K.xa + o), tap(pB, K.xb + o)),
-                                             dadd(tap(pA, K.xb + o), tap(pB, K.xa + o)));
-                    const double rs_g = dsub(dadd(tap(pC, K.ya + o), tap(pD, K.yb + o)),
-                                             dadd(tap(pC, K.yb + o), tap(pD, K.ya + o)));
+                    const double rs_o = dsub(dadd(tap(pAa, o), tap(pBb, o)), dadd(tap(pAb, o), tap(pBa, o)));
+                    const double rs_g = dsub(dadd(tap(pCa, o), tap(pDb, o)), dadd(tap(pCb, o), tap(pDa, o)));
                     sum[kk] = dsub(rs_o, rs_g);
                     need |= !(v[kk][0] < dmul(sum[kk], fast_k)) || v[kk][0] < 0.0;
                 }
@@ -502,11 +533,11 @@ __global__ void __launch_bounds__((kNcw + 1) * kWarp, OCC) cfar_fused_kernel(con
                     const int r = min(r0 + kk, r_last);
                     const int iA = clamp_lo32(r, hr), iB = clamp_hi32(r, hr, rows) + 1;
                     const int iC = clamp_lo32(r, gr), iD = clamp_hi32(r, gr, rows) + 1;
-                    const char* rA = ring + static_cast<unsigned>(slot_of(iA)) * kRowBytes;
-                    const char* rB = ring + static_cast<unsigned>(slot_of(iB)) * kRowBytes;
-                    const char* rC = ring + static_cast<unsigned>(slot_of(iC)) * kRowBytes;
-                    const char* rD = ring + static_cast<unsigned>(slot_of(iD)) * kRowBytes;
-                    sum[kk] = train_sum(K, rA, rB, rC, rD);
+                    const double rs_o = dsub(dadd(tap_at(iA, K.xa, l_xa), tap_at(iB, K.xb, l_xb)),
+                                             dadd(tap_at(iA, K.xb, l_xb), tap_at(iB, K.xa, l_xa)));
+                    const double rs_g = dsub(dadd(tap_at(iC, K.ya, l_ya), tap_at(iD, K.yb, l_yb)),
+                                             dadd(tap_at(iC, K.yb, l_yb), tap_at(iD, K.ya, l_ya)));
+                    sum[kk] = dsub(rs_o, rs_g);
                     n[kk] = (iB - iA) * K.ow - (iD - iC) * K.gw;
                 }
 #pragma unroll
@@ -538,20 +569,26 @@ __global__ void __launch_bounds__((kNcw + 1) * kWarp, OCC) cfar_fused_kernel(con
                 }
                 emit_block<kRs, 1>(L, map, r0, r_last, wc0, c, okc, hit, v, thr, per_cell);
             }
-            // hand back the groups no later step of this unit reads
+            // hand back the groups no later step of this unit reads: entries of
+            // padded rows < keep_row in lanes >= l_lo, i.e. slots < keep_row + l_lo
             __syncwarp();
             if (step + 1 < n_steps) {
-                const int done = max(0, r_last + 1 - hr) / kRs - 1;
+                const int done = (max(0, r_last + 1 - hr) + l_lo) / kRs - 1;
                 while (released < done) {
                     ++released;
                     if (lane == 0) mbar_arrive_u(empty_u + 8u * rslot);
                     if (++rslot == static_cast<unsigned>(nq)) rslot = 0;
                 }
             }
-            sA += kRs; if (sA >= nr) sA -= nr;
-            sB += kRs; if (sB >= nr) sB -= nr;
-            sC += kRs; if (sC >= nr) sC -= nr;
-            sD += kRs; if (sD >= nr) sD -= nr;
+            constexpr unsigned kAdv = kRs * kRowBytes;
+            oAa = wrap(oAa + kAdv); oAb = wrap(oAb + kAdv); oBa = wrap(oBa + kAdv); oBb = wrap(oBb + kAdv);
+            oCa = wrap(oCa + kAdv); oCb = wrap(oCb + kAdv); oDa = wrap(oDa + kAdv); oDb = wrap(oDb + kAdv);
+        }
+        // every group of the unit is waited for and handed back once
+        while (waited < groups - 1) {
+            mbar_wait_u<kFHint>(full_u + 8u * wslot, wpar);
+            ++waited;
+            if (++wslot == static_cast<unsigned>(nq)) { wslot = 0; wpar ^= 1; }
         }
         __syncwarp();
         while (released < groups - 1) {
@@ -583,12 +620,19 @@ cudaError_t go_fused(const FusedLaunch& F, cudaStream_t stream) {
 
 template <typename T, int kCpl>
 cudaError_t go_fused_occ(FusedLaunch F, cudaStream_t stream) {
-    // the ring must hold the window (2 hr + 2 rows), the wavefront skew (31
-    // rows) and a step of slack on both sides; more rows only add look-ahead
-    const int need = ((2 * F.c.hr + kWarp + 2 * kRs + 2 + kRs - 1) / kRs + 2) * kRs;
+    // The ring must hold, for every CFAR warp, the window (2 hr + 1 rows) plus
+    // the SAT lanes its taps span (the wavefront skew between them), plus
+    // group alignment on both sides (see the deadlock bound in DESIGN.md);
+    // more slots only add look-ahead.
+    // Deadlock bound: the SAT opens slot group 4G' while the CFAR warps still
+    // need the group it replaces until they have passed rows 2 hr + (l_hi - l_lo)
+    // + 14 further on, so nr >= 2 hr + (l_hi - l_lo) + 14, with l_hi - l_lo the
+    // SAT lanes one CFAR warp's taps span; one group of margin on top.
+    const int span_lanes = (kWarp + 2 * F.c.hc + 1 + kCpl - 1) / kCpl + 2;
+    const int need = ((2 * F.c.hr + span_lanes + 14 + kRs - 1) / kRs + 1) * kRs;
     int pinned = 0;
     if (const char* e = getenv("UWB_FUSED_OCC")) pinned = atoi(e);
-    for (int occ : {2, 1}) {
+    for (int occ : {3, 2, 1}) {
         if (pinned && occ != pinned) continue;
         const size_t budget = static_cast<size_t>(233472 / occ - 1024);
         int nr = need;
@@ -596,7 +640,11 @@ cudaError_t go_fused_occ(FusedLaunch F, cudaStream_t stream) {
         while (FusedSmem<T, kCpl>::bytes(nr + kRs) <= budget && nr + kRs <= need + 64) nr += kRs;
         if (const char* e = getenv("UWB_FUSED_RING")) nr = std::max(need, atoi(e) / kRs * kRs);
         F.nr = nr;
-        return occ == 2 ? go_fused<T, kCpl, 2>(F, stream) : go_fused<T, kCpl, 1>(F, stream);
+        switch (occ) {
+            case 3: return go_fused<T, kCpl, 3>(F, stream);
+            case 2: return go_fused<T, kCpl, 2>(F, stream);
+            default: return go_fused<T, kCpl, 1>(F, stream);
+        }
     }
     return cudaErrorNotSupported;
 }
