@@ -45,15 +45,28 @@ namespace {
 constexpr int kBandOut = 128;   // output columns per band (unit)
 constexpr int kNcw = 4;         // CFAR warps (one column x 4 rows per thread per step)
 constexpr int kRs = 4;          // output rows per CFAR step (= ring group)
-constexpr int kFAhead = 6;      // SAT source staging distance (steps)
-constexpr int kFXSlots = 8;     // lane-private source ring (copy steps)
+#ifndef UWB_FUSED_XSLOTS
+#define UWB_FUSED_XSLOTS 8
+#endif
+constexpr int kFXSlots = UWB_FUSED_XSLOTS; // lane-private source ring (copy steps)
+constexpr int kFAhead = kFXSlots - 2;      // SAT source staging distance (steps; rows are L2-prefetched)
 constexpr int kMirror = kRs - 1; // ring slots mirrored past the end (4 consecutive slots stay contiguous)
 constexpr int kFPublish = 64;   // SAT steps between edge hand-overs
 constexpr int kFL2Ahead = 24;   // source rows are prefetched into L2 this many steps before staging
-#ifndef UWB_FUSED_HINT
-#define UWB_FUSED_HINT 0
+#ifndef UWB_FUSED_HINT_S
+#define UWB_FUSED_HINT_S 0
 #endif
-constexpr unsigned kFHint = UWB_FUSED_HINT; // barrier-wait suspend hint (ns); 0 = plain try_wait
+#ifndef UWB_FUSED_HINT_C
+#define UWB_FUSED_HINT_C 20000
+#endif
+// barrier-wait suspend hints (ns; 0 = plain try_wait): the SAT warp (the
+// critical path) / the CFAR warps (which would otherwise spin on issue slots)
+constexpr unsigned kFHint = UWB_FUSED_HINT_S;
+constexpr unsigned kCHint = UWB_FUSED_HINT_C;
+#ifndef UWB_FUSED_UNROLL
+#define UWB_FUSED_UNROLL 4
+#endif
+constexpr int kFUnroll = UWB_FUSED_UNROLL; // SAT steps per unrolled body (source slots stay compile-time)
 
 struct FusedLaunch {
     CfarLaunch c;
@@ -357,7 +370,7 @@ __global__ void __launch_bounds__((kNcw + 1) * kWarp, OCC) cfar_fused_kernel(con
                 e_next = fetch_left(s0 + 2 * kWarp);
                 const bool fast = s0 >= kWarp && s0 + kWarp + kFAhead <= rows;
                 if (fast) {
-#pragma unroll 16
+#pragma unroll kFUnroll
                     for (int uu = 0; uu < kWarp; ++uu) step(s0, uu, std::false_type{});
                 } else {
 #pragma unroll 1
@@ -404,7 +417,7 @@ __global__ void __launch_bounds__((kNcw + 1) * kWarp, OCC) cfar_fused_kernel(con
     const int64_t wpr = L.words_per_row;
     for (int k = 0;; ++k) {
         const int q = k & 1;
-        mbar_wait_u<kFHint>(ubar_u + 8u * q, static_cast<unsigned>((k >> 1) & 1));
+        mbar_wait_u<kCHint>(ubar_u + 8u * q, static_cast<unsigned>((k >> 1) & 1));
         const unsigned unit = ld_shared_u32(unitq_u + 4u * q);
         __syncwarp();
         if (lane == 0) mbar_arrive_u(ubar_u + 16u + 8u * q);
@@ -465,7 +478,7 @@ __global__ void __launch_bounds__((kNcw + 1) * kWarp, OCC) cfar_fused_kernel(con
                 // newest entry read: padded row min(rows, r_last + hr + 1) in SAT lane l_hi
                 const int need = (min(rows, r_last + hr + 1) + l_hi) / kRs;
                 while (waited < need) {
-                    mbar_wait_u<kFHint>(full_u + 8u * wslot, wpar);
+                    mbar_wait_u<kCHint>(full_u + 8u * wslot, wpar);
                     ++waited;
                     if (++wslot == static_cast<unsigned>(nq)) { wslot = 0; wpar ^= 1; }
                 }
@@ -586,7 +599,7 @@ __global__ void __launch_bounds__((kNcw + 1) * kWarp, OCC) cfar_fused_kernel(con
         }
         // every group of the unit is waited for and handed back once
         while (waited < groups - 1) {
-            mbar_wait_u<kFHint>(full_u + 8u * wslot, wpar);
+            mbar_wait_u<kCHint>(full_u + 8u * wslot, wpar);
             ++waited;
             if (++wslot == static_cast<unsigned>(nq)) { wslot = 0; wpar ^= 1; }
         }

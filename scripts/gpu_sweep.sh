@@ -1,6 +1,9 @@
 # scratch sweep of the fused kernel (cfar phase = fused kernel)
 export PYTHONPATH=. MAPS=1024
-for t in $(python -m pytest tests/test_gpu_fused.py --collect-only -q 2>/dev/null | grep "::"); do
-  timeout 60 python -m pytest "$t" -x -q 2>&1 | tail -1 | sed "s|^|$t: |"
+L=paper_2012_11077_b200/lib
+cp $L/libuwbvital_b200.so /tmp/base.so
+for v in x16; do
+[ $v = base ] || cp $L/variants/lib_$v.so $L/libuwbvital_b200.so
+echo "$v: $(timeout 120 python scripts/cfar_probe.py 2>&1 | tail -1) | idle $(UWB_FUSED_DEBUG=1 timeout 120 python scripts/cfar_probe.py 2>&1 | tail -1)"
 done
-echo -n "base: "; timeout 120 python scripts/cfar_probe.py 2>&1 | tail -1
+cp /tmp/base.so $L/libuwbvital_b200.so
