@@ -18,10 +18,11 @@
 // sum = RS(outer) - RS(guard), T = alpha[n] * (sum / n), mask = cut > T
 // (cfar.cpp:115-127).
 //
-// Interior fast path (all 4 rows and all of the warp's columns have unclamped
-// windows): the 4 tap rows of the step are consecutive ring slots (the first
-// group is mirrored past the ring's end), so every tap is one shared load at a
-// compile-time offset from one of 8 row pointers, and n = n_int. The IEEE
+// Fast path (all 4 rows have unclamped windows; columns may be clamped, their
+// edges and n are per-lane constants): the 4 tap rows of the step are
+// consecutive ring slots (the first group is mirrored past the ring's end), so
+// every tap is one shared load at a compile-time offset from one of 8 row
+// pointers, and n is the column's constant. The IEEE
 // division is skipped: a cell with 0 <= cut < sum * (alpha/n) * (1 - 1e-13) is
 // certainly below T; any other cell in the warp sends the warp through the
 // reference expression alpha[n] * (sum / n). Decisions, thresholds and
@@ -213,14 +214,19 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
         okc[j] = K[j].ok;
     }
     const bool per_cell = L.thresholds != nullptr || L.mask_u8 != nullptr;
-    // Interior fast path: the warp's columns have unclamped windows, so column
-    // j's taps sit exactly 32 j doubles after column 0's, and n = n_int
-    // (cfar.cpp:28-32).
-    const bool warp_cols_interior = !per_cell && wc0 - hc >= 0 && wc0 + kWarp * CPT - 1 + hc <= cols - 1;
-    const int n_int = (2 * hr + 1) * (2 * hc + 1) - (2 * gr + 1) * (2 * gc + 1);
-    const double alpha_int = n_int > 0 ? __ldg(L.alpha + n_int) : 0.0;
-    // 0 <= cut < sum * fast_k  implies  cut < alpha * (sum / n) (relative margin 1e-13)
-    const double fast_k = n_int > 0 ? dmul(ddiv(alpha_int, static_cast<double>(n_int)), 1.0 - 1e-13) : 0.0;
+    // Fast path: every row of the step has an unclamped window, so n is constant
+    // down each column (cfar.cpp:28-32 with full-height windows); clamped
+    // column edges are in K[j] and n_col[j].
+    const bool fast_cols = !per_cell && wc0 < cols;
+    int n_col[CPT];
+    double alpha_col[CPT], fast_k[CPT];
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+        n_col[j] = (2 * hr + 1) * K[j].ow - (2 * gr + 1) * K[j].gw;
+        alpha_col[j] = n_col[j] > 0 ? __ldg(L.alpha + n_col[j]) : 0.0;
+        // 0 <= cut < sum * fast_k  implies  cut < alpha * (sum / n) (relative margin 1e-13)
+        fast_k[j] = n_col[j] > 0 ? dmul(ddiv(alpha_col[j], static_cast<double>(n_col[j])), 1.0 - 1e-13) : 0.0;
+    }
 
     // ring slots of the (unclamped) tap rows of output row r0, advanced 4 rows per step
     auto slot0 = [&](int i) { return ((i - i_lo) % G.nr + G.nr) % G.nr; };
@@ -262,7 +268,7 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
         bool hit[RS][CPT];
         if (L.debug & 1u) goto release; // data-movement probe
         {
-            const bool fast = warp_cols_interior && r0 - hr >= 0 && r0 + RS - 1 == r_last && r_last + hr <= rows - 1;
+            const bool fast = fast_cols && r0 - hr >= 0 && r0 + RS - 1 == r_last && r_last + hr <= rows - 1;
             if (fast) {
                 // ---- interior step: 8 row pointers, compile-time tap offsets ----
                 const char* pA = ring + static_cast<unsigned>(sA) * kRowBytes;
@@ -275,14 +281,14 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
                 for (int k = 0; k < RS; ++k) {
 #pragma unroll
                     for (int j = 0; j < CPT; ++j) {
-                        const unsigned o = k * kRowBytes + j * kWarp * 8u;
-                        const double rs_o = dsub(dadd(tap(pA, K[0].xa + o), tap(pB, K[0].xb + o)),
-                                                 dadd(tap(pA, K[0].xb + o), tap(pB, K[0].xa + o)));
-                        const double rs_g = dsub(dadd(tap(pC, K[0].ya + o), tap(pD, K[0].yb + o)),
-                                                 dadd(tap(pC, K[0].yb + o), tap(pD, K[0].ya + o)));
+                        const unsigned o = k * kRowBytes;
+                        const double rs_o = dsub(dadd(tap(pA, K[j].xa + o), tap(pB, K[j].xb + o)),
+                                                 dadd(tap(pA, K[j].xb + o), tap(pB, K[j].xa + o)));
+                        const double rs_g = dsub(dadd(tap(pC, K[j].ya + o), tap(pD, K[j].yb + o)),
+                                                 dadd(tap(pC, K[j].yb + o), tap(pD, K[j].ya + o)));
                         sum[k][j] = dsub(rs_o, rs_g);
                         v[k][j] = static_cast<double>(cut_grp[k * kW + tc + j * kWarp]);
-                        need |= !(v[k][j] < dmul(sum[k][j], fast_k)) || v[k][j] < 0.0;
+                        need |= !(v[k][j] < dmul(sum[k][j], fast_k[j])) || v[k][j] < 0.0;
                     }
                 }
                 if (__any_sync(0xffffffffu, need)) {
@@ -292,8 +298,8 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
                         for (int j = 0; j < CPT; ++j) {
                             thr[k][j] = 0.0;
                             hit[k][j] = false;
-                            if (!(v[k][j] < dmul(sum[k][j], fast_k)) || v[k][j] < 0.0) {
-                                thr[k][j] = dmul(alpha_int, ddiv(sum[k][j], static_cast<double>(n_int)));
+                            if (!(v[k][j] < dmul(sum[k][j], fast_k[j])) || v[k][j] < 0.0) {
+                                thr[k][j] = dmul(alpha_col[j], ddiv(sum[k][j], static_cast<double>(n_col[j])));
                                 hit[k][j] = v[k][j] > thr[k][j];
                                 if (v[k][j] < 0.0)
                                     report_min(L.first_bad + 2 * map + 1,
@@ -305,8 +311,9 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
                     emit_block<RS, CPT>(L, map, r0, r_last, wc0, c0 + tc, okc, hit, v, thr, false);
                 } else if (lane < CPT * RS && L.mask_bits) { // no hit in the block: zero mask words
                     const int wk = lane / CPT, wc = wc0 + (lane % CPT) * kWarp;
-                    L.mask_bits[map * L.mask_map_stride + (r0 + wk - L.geo.row_lo) * L.words_per_row +
-                                (wc >> 5)] = 0u;
+                    if (wc < cols)
+                        L.mask_bits[map * L.mask_map_stride + (r0 + wk - L.geo.row_lo) * L.words_per_row +
+                                    (wc >> 5)] = 0u;
                 }
             } else {
                 // ---- general step: clamped windows, per-cell n ----
