@@ -263,7 +263,7 @@ def run_b200(args):
     total_count = torch.zeros(1, dtype=torch.int64, device=dev)
 
     def step(phase=False):
-        runner(maps, phase_events=phase)
+        runner(maps, phase_events=phase, fused=args.fused)
         total_count.copy_(runner.counts.sum().view(1))
         if world > 1:
             dist.all_reduce(total_count)  # final detection-count reduce (NCCL)
@@ -369,6 +369,8 @@ def run_b200(args):
             "data": "synthetic (seeded generator for BASELINE config 3, device-resident fp32 input)",
             "config": {"workload": WORKLOAD, "n_maps": N_MAPS, "rows": ROWS, "cols": COLS,
                        "input_dtype": "f32", "sat_mode": "global (bit-identical to the reference)",
+                       "kernels": ("fused SAT+CFAR (flags bit 4)" if args.fused else
+                                   "SAT (sat_systolic_kernel) + CFAR (cfar_ws_kernel) + sort"),
                        "l2": "inputs 16 GiB per pass >> 126 MB L2 (no flush needed)",
                        "parallelism": f"dp{world} (maps sharded in 64-map blocks)",
                        "detections_per_step": int(total_count.item()) if world > 1 else
@@ -407,6 +409,8 @@ def main():
     ap.add_argument("--e2e-chunk", type=int, default=64, help="maps per H2D chunk in the end-to-end call")
     ap.add_argument("--maps", type=int, default=N_MAPS, help="batch size (profiling runs only)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--fused", action="store_true",
+                    help="device path through the fused SAT+CFAR kernel (flags bit 4) instead of SAT + ring CFAR")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5, 6],
                     help="BASELINE.json configuration (3 = the headline line; 6 = the paper's Table I; "

@@ -206,7 +206,7 @@ def run_cfg5(args):
     def step(phase=False):
         count.zero_()
         for i, rn in enumerate(runners):
-            rn(maps, phase_events=phase, reuse_tables=i > 0, keep_tables=i == 0)
+            rn(maps, phase_events=phase, reuse_tables=i > 0)
             count.add_(rn.counts.sum())
         reduce_count(count)
 

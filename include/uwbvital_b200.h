@@ -198,13 +198,13 @@ uint64_t uwb_dev_cfar2d_workspace(const uwb_map_batch* batch, const uwb_cfar_par
  * flags bit 0: skip the detection sort (list left in unspecified order).
  * flags bit 2: reuse the summed-area tables already in `workspace` from the
  *   previous call on the same maps with the same table geometry (GLOBAL mode, or
- *   SLAB mode with the same slab_rows and g_r + b_r), which must have been made
- *   with bit 4: one table, several CFAR parameter sets (the integral image's
- *   point). Non-finite inputs are reported only by the call that built the tables.
- * flags bit 4: keep the summed-area tables in `workspace` (for later bit-2
- *   calls). Without bits 2 and 4, whole-map batches run SAT and CFAR as one
- *   kernel whose table never leaves shared memory (same results, a third of
- *   the memory traffic); other geometries always build the tables.
+ *   SLAB mode with the same slab_rows and g_r + b_r), made without bit 4: one
+ *   table, several CFAR parameter sets (the integral image's point). Non-finite
+ *   inputs are reported only by the call that built the tables.
+ * flags bit 4: fused SAT + CFAR for whole-map batches: one kernel whose table
+ *   never leaves shared memory (same results, about a third of the HBM traffic;
+ *   on an otherwise idle B200 the two-kernel default is measured slightly
+ *   faster). No table is left in `workspace`.
  * flags bit 3: the naive backend instead (cfar.cpp:200-216: explicit ring sums,
  *   no table; GLOBAL mode only) - the baseline of the paper's Table I. */
 uwb_status uwb_dev_cfar2d(const uwb_map_batch* batch, const uwb_cfar_params* params,

@@ -78,15 +78,14 @@ class BatchCfar:
             self.dets.data_ptr(), self.det_capacity, self.counts.data_ptr(), self.first_bad.data_ptr())
 
     def __call__(self, maps: torch.Tensor, sort: bool = True, stream=None, phase_events: bool = False,
-                 reuse_tables: bool = False, naive: bool = False, keep_tables: bool = False) -> None:
+                 reuse_tables: bool = False, naive: bool = False, fused: bool = False) -> None:
         """Launch SAT + CFAR (+ sort) for ``maps`` of shape (n_maps, rows, cols).
         ``phase_events`` records per-phase CUDA events (read with :func:`phase_ms`).
         ``reuse_tables`` skips the SAT: the (shared) workspace already holds the
         tables of these maps from the previous call (another parameter set).
         ``naive`` runs the naive backend (explicit window sums, no table).
-        ``keep_tables`` leaves the tables in the workspace for later
-        ``reuse_tables`` calls (otherwise whole-map batches run the fused
-        SAT+CFAR kernel and no table is written)."""
+        ``fused`` runs SAT and CFAR as one kernel with the table kept on chip
+        (whole-map batches; no table is left for ``reuse_tables``)."""
         if maps.dtype != self.dtype or tuple(maps.shape) != (self.n_maps, self.rows, self.cols):
             raise ValueError(f"expected {(self.n_maps, self.rows, self.cols)} {self.dtype}, got "
                              f"{tuple(maps.shape)} {maps.dtype}")
@@ -94,7 +93,7 @@ class BatchCfar:
             raise ValueError("maps must be a contiguous CUDA tensor")
         self._batch.maps = maps.data_ptr()
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
-        flags = (0 if sort else 1) | (2 if phase_events else 0) | (4 if reuse_tables else 0) | (8 if naive else 0) | (16 if keep_tables else 0)
+        flags = (0 if sort else 1) | (2 if phase_events else 0) | (4 if reuse_tables else 0) | (8 if naive else 0) | (16 if fused else 0)
         if self.window is None:
             st = N.lib.uwb_dev_cfar2d(C.byref(self._batch), C.byref(self._cparams), self.alpha.data_ptr(),
                                       self.sat_mode, C.c_uint64(self.slab_rows), C.byref(self._out),

@@ -305,10 +305,10 @@ uwb_status dev_cfar(const uwb_map_batch& b, const uwb_cfar_params& p, const doub
     if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[0], s));
     if (backend == UWB_INTEGRAL) {
         bool fused = false;
-        if (!(flags & (4u | 16u))) {
-            // bit 2 clear and bit 4 clear: no table is kept, so SAT and CFAR run
-            // as one kernel with the table on chip (falls through when the
-            // geometry does not qualify)
+        if ((flags & 16u) && !(flags & 4u)) {
+            // bit 4: SAT and CFAR as one kernel with the table on chip (no table
+            // is left in the workspace; falls through to the two kernels when
+            // the geometry does not qualify)
             const SatLaunch SL = sat_launch(P, b, ws, reinterpret_cast<unsigned long long*>(o.first_bad));
             UWB_CUDA_TRY(cudaMemsetAsync(SL.gprog, 0, sizeof(unsigned) * P.n_jobs * P.strips, s));
             UWB_CUDA_TRY(cudaMemsetAsync(SL.tile_counter, 0, sizeof(unsigned), s));

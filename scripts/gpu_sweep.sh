@@ -1,9 +1,6 @@
-# scratch sweep of the fused kernel (cfar phase = fused kernel)
-export PYTHONPATH=. MAPS=1024
-L=paper_2012_11077_b200/lib
-cp $L/libuwbvital_b200.so /tmp/base.so
-for v in x16; do
-[ $v = base ] || cp $L/variants/lib_$v.so $L/libuwbvital_b200.so
-echo "$v: $(timeout 120 python scripts/cfar_probe.py 2>&1 | tail -1) | idle $(UWB_FUSED_DEBUG=1 timeout 120 python scripts/cfar_probe.py 2>&1 | tail -1)"
+for f in 1 0; do
+  echo "== UWB_FUSED=$f"
+  UWB_FUSED=$f python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline 2>&1 | tail -1 | python3 -c "import json,sys; d=json.loads(sys.stdin.read()); print('cfg3', round(d['value'],1), round(d['ms_per_step'],2), d['phases_ms'])"
+  UWB_FUSED=$f python bench.py --config 1 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline 2>&1 | tail -1 | cut -c1-300
+  UWB_FUSED=$f python bench.py --config 2 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline 2>&1 | tail -1 | cut -c1-300
 done
-cp /tmp/base.so $L/libuwbvital_b200.so

@@ -24,17 +24,17 @@ def _check_map(batch, i, ref_res, what):
     assert_bitwise(d["threshold"], r["threshold"], f"{what}: det thresholds")
 
 
-@pytest.mark.parametrize("keep", [False, True], ids=["fused", "two_kernel"])
-def test_cfg3_maps_bit_identical_to_reference(uwb, ref, cuda, keep):
+@pytest.mark.parametrize("fused", [False, True], ids=["two_kernel", "fused"])
+def test_cfg3_maps_bit_identical_to_reference(uwb, ref, cuda, fused):
     """Config 3 maps (1024x1024 fp32, Exp(1) + 32 targets, g2 b8 pfa 1e-4), through
-    the fused kernel and through SAT + ring CFAR (tables kept, flags bit 4)."""
+    SAT + ring CFAR (the default) and through the fused kernel (flags bit 4)."""
     from paper_2012_11077_b200 import synth
     from paper_2012_11077_b200.batch import BatchCfar
     n = 6
     maps = synth.cfg3_maps(n, seed=3, device=cuda)
     p = uwb.CfarParams(2, 8, 1e-4)
     b = BatchCfar(n, 1024, 1024, p, torch.float32, det_capacity=1024, want_mask_u8=True, want_thresholds=True)
-    b(maps, keep_tables=keep)
+    b(maps, fused=fused)
     torch.cuda.synchronize()
     b.check_inputs()
     host = maps.double().cpu().numpy()
@@ -42,7 +42,7 @@ def test_cfg3_maps_bit_identical_to_reference(uwb, ref, cuda, keep):
         _check_map(b, i, ref.cfar2d(host[i], 2, 8, 1e-4, "integral"), f"cfg3 map {i}")
     # mask bits only (the fast paths), compared with the reference masks
     b2 = BatchCfar(n, 1024, 1024, p, torch.float32, det_capacity=1024)
-    b2(maps, keep_tables=keep)
+    b2(maps, fused=fused)
     torch.cuda.synchronize()
     for i in range(n):
         assert np.array_equal(b2.mask(i), b.mask_u8[i].cpu().numpy()), f"cfg3 map {i} bits-only mask"
@@ -62,10 +62,10 @@ def test_cfg1_map_and_sat(uwb, ref, cuda):
     assert len(got.detections) >= 5
 
 
-@pytest.mark.parametrize("keep", [False, True], ids=["fused", "two_kernel"])
+@pytest.mark.parametrize("fused", [False, True], ids=["two_kernel", "fused"])
 @pytest.mark.parametrize("win", [((1, 3), (4, 16)), ((3, 1), (16, 4))])
 @pytest.mark.parametrize("pfa", [1e-3, 1e-5])
-def test_cfg5_per_axis_windows_vs_restatement(uwb, oracle, cuda, win, pfa, keep):
+def test_cfg5_per_axis_windows_vs_restatement(uwb, oracle, cuda, win, pfa, fused):
     """Config 5 (K-clutter, non-square windows), scaled to 3 maps of 1024x512;
     per-cell outputs, then mask bits only (the fast paths)."""
     from paper_2012_11077_b200 import synth
@@ -74,9 +74,9 @@ def test_cfg5_per_axis_windows_vs_restatement(uwb, oracle, cuda, win, pfa, keep)
     maps = synth.cfg5_maps(3, seed=5, device=cuda, rows=1024, cols=512)
     p = uwb.CfarParams(guard_radius=gr, background_radius=br, pfa=pfa, guard_cols=gc, background_cols=bc)
     b = BatchCfar(3, 1024, 512, p, torch.float32, det_capacity=4096, want_mask_u8=True, want_thresholds=True)
-    b(maps, keep_tables=keep)
+    b(maps, fused=fused)
     b2 = BatchCfar(3, 1024, 512, p, torch.float32, det_capacity=4096)
-    b2(maps, keep_tables=keep)
+    b2(maps, fused=fused)
     torch.cuda.synchronize()
     host = maps.double().cpu().numpy()
     for i in range(3):
@@ -231,7 +231,7 @@ def test_reused_tables_match_fresh_call(uwb, oracle, cuda):
     a = BatchCfar(2, 600, 500, pa, torch.float32, det_capacity=8192, want_mask_u8=True, want_thresholds=True)
     b = BatchCfar(2, 600, 500, pb, torch.float32, det_capacity=8192, want_mask_u8=True, want_thresholds=True,
                   workspace=a.workspace)
-    a(maps, keep_tables=True)
+    a(maps)
     b(maps, reuse_tables=True)
     torch.cuda.synchronize()
     host = maps.double().cpu().numpy()

@@ -1,5 +1,5 @@
 """The fused SAT+CFAR kernel (csrc/cfar_fused.cu): bit-identical to the
-two-kernel path (table in HBM, flags bit 4) and to the reference / restatement
+two-kernel path (table in HBM; the fused kernel is flags bit 4) and to the reference / restatement
 over band edges, partial bands, every columns-per-lane variant, both ring
 occupancies, f32/f64, per-cell outputs, the unit queue wrapping many times,
 a single wide map (band chain), and non-finite / negative input reports."""
@@ -12,12 +12,12 @@ from tests.helpers import assert_bitwise
 pytestmark = pytest.mark.gpu
 
 
-def _run(uwb, maps, p, per_cell, keep, cap=1 << 14):
+def _run(uwb, maps, p, per_cell, fused, cap=1 << 14):
     from paper_2012_11077_b200.batch import BatchCfar, kernel_launches
     n, R, C = maps.shape
     b = BatchCfar(n, R, C, p, maps.dtype, det_capacity=cap, want_mask_u8=per_cell, want_thresholds=per_cell)
     k0 = kernel_launches()
-    b(maps, keep_tables=keep)
+    b(maps, fused=fused)
     torch.cuda.synchronize()
     return b, kernel_launches() - k0
 
@@ -55,8 +55,8 @@ def test_fused_matches_two_kernel_path(uwb, cuda, case, per_cell):
     maps = torch.empty((n, R, C), device=cuda, dtype=dt).exponential_(1.0, generator=gen)
     maps[:, ::7, ::5] *= 40.0  # targets
     p = uwb.CfarParams(guard_radius=gr, background_radius=br, pfa=pfa, guard_cols=gc, background_cols=bc)
-    fused, k_f = _run(uwb, maps, p, per_cell, keep=False)
-    two, k_t = _run(uwb, maps, p, per_cell, keep=True)
+    fused, k_f = _run(uwb, maps, p, per_cell, fused=True)
+    two, k_t = _run(uwb, maps, p, per_cell, fused=False)
     assert k_f == k_t - 1, "the fused call launches one kernel fewer (SAT + CFAR -> one)"
     _same(fused, two, f"case {case}")
     assert int(fused.counts.sum()) > 0
@@ -68,7 +68,7 @@ def test_fused_vs_restatement(uwb, oracle, cuda, case):
     gen = torch.Generator(device="cuda").manual_seed(7 + case)
     maps = torch.empty((min(n, 2), R, C), device=cuda, dtype=dt).exponential_(1.0, generator=gen)
     p = uwb.CfarParams(guard_radius=gr, background_radius=br, pfa=pfa, guard_cols=gc, background_cols=bc)
-    b, _ = _run(uwb, maps, p, True, keep=False)
+    b, _ = _run(uwb, maps, p, True, fused=True)
     host = maps.double().cpu().numpy()
     for i in range(maps.shape[0]):
         r = oracle.cfar(host[i], gr, gc, br, bc, pfa)
@@ -82,7 +82,7 @@ def test_fused_cfg3_maps_vs_reference(uwb, ref, cuda):
     from paper_2012_11077_b200 import synth
     maps = synth.cfg3_maps(4, seed=33, device=cuda)
     p = uwb.CfarParams(2, 8, 1e-4)
-    b, _ = _run(uwb, maps, p, False, keep=False, cap=1024)
+    b, _ = _run(uwb, maps, p, False, fused=True, cap=1024)
     host = maps.double().cpu().numpy()
     for i in range(4):
         r = ref.cfar2d(host[i], 2, 8, 1e-4, "integral")
@@ -104,8 +104,8 @@ def test_fused_reports_bad_inputs(uwb, cuda):
     maps[1, 64, 7] = -2.0
     maps[2, 129, 599] = float("-inf")
     p = uwb.CfarParams(2, 8, 1e-3)
-    fused, _ = _run(uwb, maps, p, False, keep=False)
-    two, _ = _run(uwb, maps, p, False, keep=True)
+    fused, _ = _run(uwb, maps, p, False, fused=True)
+    two, _ = _run(uwb, maps, p, False, fused=False)
     fb = fused.first_bad.cpu().numpy().astype(np.uint64)
     assert int(fb[0, 0]) == 100 * 600 + 590
     assert int(fb[1, 1]) == 5 * 600 + 200
