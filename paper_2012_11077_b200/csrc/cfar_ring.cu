@@ -248,7 +248,96 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
         kcache[j] = 0.0;
     }
 
+    // Steady run: consecutive fast steps (every row of the step has an unclamped
+    // window and the step is full). There each step needs exactly one more table
+    // group and one CUT group, and frees one of each, so the bookkeeping is a few
+    // increments; the step body is the fast path below.
+    const int steady_lo = max(0, (hr - ra + RS - 1) / RS);
+    const int steady_hi = min(n_steps, min((rb - RS - ra) / RS, (rows - RS - hr - ra) / RS) + 1);
+    const bool steady = SG == 1 && fast_cols && !(L.debug & 1u) && steady_lo < steady_hi;
+    const char* cut_lane = reinterpret_cast<const char*>(cuts + tc);
+    constexpr unsigned kCutBytes = kG * kW * sizeof(T);
+
     for (int step = 0; step < n_steps; ++step) {
+        if (steady && step == steady_lo) {
+            int need = min(last_grp_c, (ra + step * RS + RS + hr - i_lo) / kG);
+            int done = (ra + step * RS + RS - hr - i_lo) / kG - 1;
+            for (; step < steady_hi; ++step) {
+                const int r0 = ra + step * RS;
+                while (waited < need) {
+                    mbar_wait_u<kHint>(full_t_u + 8u * wslot, static_cast<unsigned>(wphase));
+                    ++waited;
+                    if (++wslot == G.ng) { wslot = 0; wphase ^= 1; }
+                }
+                need = min(last_grp_c, need + 1);
+                mbar_wait_u<kHint>(full_c_u + 8u * cslot, static_cast<unsigned>(cphase));
+                const char* cg = cut_lane + cslot * kCutBytes;
+                const char* pA = ring + static_cast<unsigned>(sA) * kRowBytes;
+                const char* pB = ring + static_cast<unsigned>(sB) * kRowBytes;
+                const char* pC = ring + static_cast<unsigned>(sC) * kRowBytes;
+                const char* pD = ring + static_cast<unsigned>(sD) * kRowBytes;
+                double v[RS][CPT], thr[RS][CPT], sum[RS][CPT];
+                bool hit[RS][CPT];
+                bool any = false;
+#pragma unroll
+                for (int k = 0; k < RS; ++k) {
+#pragma unroll
+                    for (int j = 0; j < CPT; ++j) {
+                        const unsigned o = k * kRowBytes;
+                        const double rs_o = dsub(dadd(tap(pA, K[j].xa + o), tap(pB, K[j].xb + o)),
+                                                 dadd(tap(pA, K[j].xb + o), tap(pB, K[j].xa + o)));
+                        const double rs_g = dsub(dadd(tap(pC, K[j].ya + o), tap(pD, K[j].yb + o)),
+                                                 dadd(tap(pC, K[j].yb + o), tap(pD, K[j].ya + o)));
+                        sum[k][j] = dsub(rs_o, rs_g);
+                        v[k][j] = static_cast<double>(
+                            *reinterpret_cast<const T*>(cg + (k * kW + j * kWarp) * sizeof(T)));
+                        any |= !(v[k][j] < dmul(sum[k][j], fast_k[j])) || v[k][j] < 0.0;
+                    }
+                }
+                if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+                    for (int k = 0; k < RS; ++k) {
+#pragma unroll
+                        for (int j = 0; j < CPT; ++j) {
+                            thr[k][j] = 0.0;
+                            hit[k][j] = false;
+                            if (!(v[k][j] < dmul(sum[k][j], fast_k[j])) || v[k][j] < 0.0) {
+                                thr[k][j] = dmul(alpha_col[j], ddiv(sum[k][j], static_cast<double>(n_col[j])));
+                                hit[k][j] = v[k][j] > thr[k][j];
+                                if (v[k][j] < 0.0)
+                                    report_min(L.first_bad + 2 * map + 1,
+                                               static_cast<unsigned long long>(static_cast<int64_t>(r0 + k) * cols +
+                                                                               c0 + tc + j * kWarp));
+                            }
+                        }
+                    }
+                    emit_block<RS, CPT>(L, map, r0, r0 + RS - 1, wc0, c0 + tc, okc, hit, v, thr, false);
+                } else if (lane < CPT * RS && L.mask_bits) { // no hit in the block: zero mask words
+                    const int wk = lane / CPT, wc = wc0 + (lane % CPT) * kWarp;
+                    if (wc < cols)
+                        L.mask_bits[map * L.mask_map_stride + (r0 + wk - L.geo.row_lo) * L.words_per_row +
+                                    (wc >> 5)] = 0u;
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive_u(empty_c_u + 8u * cslot);
+                    if (step + 1 < n_steps) {
+                        while (released < done) {
+                            ++released;
+                            mbar_arrive_u(empty_t_u + 8u * rslot);
+                            if (++rslot == G.ng) rslot = 0;
+                        }
+                    }
+                }
+                ++done;
+                if (++cslot == kCutGroups) { cslot = 0; cphase ^= 1; }
+                sA += RS; if (sA >= G.nr) sA -= G.nr;
+                sB += RS; if (sB >= G.nr) sB -= G.nr;
+                sC += RS; if (sC >= G.nr) sC -= G.nr;
+                sD += RS; if (sD >= G.nr) sD -= G.nr;
+            }
+            if (step >= n_steps) break;
+        }
         const int r0 = ra + step * RS;
         const int r_last = min(r0 + RS, rb) - 1;
         {
