@@ -81,6 +81,26 @@ __device__ __forceinline__ void mbar_wait_susp(uint64_t* bar, unsigned parity, u
         "r"(parity), "r"(hint_ns)
         : "memory");
 }
+// Shared loads on 32-bit shared-window addresses. Volatile keeps them after the
+// (volatile) mbarrier waits; no memory clobber, so other work schedules around them.
+__device__ __forceinline__ double lds_f64(unsigned a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+template <typename T>
+__device__ __forceinline__ double lds_widen(unsigned a);
+template <>
+__device__ __forceinline__ double lds_widen<float>(unsigned a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return static_cast<double>(v);
+}
+template <>
+__device__ __forceinline__ double lds_widen<double>(unsigned a) {
+    return lds_f64(a);
+}
+
 // 3-D tensor box -> L2 (no shared memory, no completion tracking).
 __device__ __forceinline__ void tma_prefetch3(const CUtensorMap* map, int x, int y, int z) {
     asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
@@ -255,27 +275,55 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
     const int steady_lo = max(0, (hr - ra + RS - 1) / RS);
     const int steady_hi = min(n_steps, min((rb - RS - ra) / RS, (rows - RS - hr - ra) / RS) + 1);
     const bool steady = SG == 1 && fast_cols && !(L.debug & 1u) && steady_lo < steady_hi;
-    const char* cut_lane = reinterpret_cast<const char*>(cuts + tc);
     constexpr unsigned kCutBytes = kG * kW * sizeof(T);
 
     for (int step = 0; step < n_steps; ++step) {
         if (steady && step == steady_lo) {
             int need = min(last_grp_c, (ra + step * RS + RS + hr - i_lo) / kG);
             int done = (ra + step * RS + RS - hr - i_lo) / kG - 1;
+            while (waited < need - 1) { // catch up; then one group per step
+                mbar_wait_u<kHint>(full_t_u + 8u * wslot, static_cast<unsigned>(wphase));
+                ++waited;
+                if (++wslot == G.ng) { wslot = 0; wphase ^= 1; }
+            }
+            // 32-bit shared addresses (no generic-to-shared conversions in the loop)
+            const unsigned ring_s = smem_u32(ring);
+            const unsigned ring_end = static_cast<unsigned>(G.nr) * kRowBytes;
+            unsigned oA = static_cast<unsigned>(sA) * kRowBytes, oB = static_cast<unsigned>(sB) * kRowBytes;
+            unsigned oC = static_cast<unsigned>(sC) * kRowBytes, oD = static_cast<unsigned>(sD) * kRowBytes;
+            unsigned xa[CPT], xb[CPT], ya[CPT], yb[CPT];
+#pragma unroll
+            for (int j = 0; j < CPT; ++j) {
+                xa[j] = ring_s + K[j].xa;
+                xb[j] = ring_s + K[j].xb;
+                ya[j] = ring_s + K[j].ya;
+                yb[j] = ring_s + K[j].yb;
+            }
+            const unsigned cut_s = smem_u32(cuts + tc);
+            // lane k*CPT+j owns mask word (row r0 + k, column word of wc0 + 32 j)
+            uint32_t* mword = nullptr;
+            if (L.mask_bits && lane < CPT * RS && wc0 + (lane % CPT) * kWarp < cols)
+                mword = L.mask_bits + map * L.mask_map_stride +
+                        (ra + step * RS + lane / CPT - L.geo.row_lo) * L.words_per_row +
+                        ((wc0 + (lane % CPT) * kWarp) >> 5);
+            const int64_t mstep = RS * L.words_per_row;
+            if (lane == 0 && step + 1 < n_steps) { // catch up the hand-backs; then one per step
+                while (released < done - 1) {
+                    ++released;
+                    mbar_arrive_u(empty_t_u + 8u * rslot);
+                    if (++rslot == G.ng) rslot = 0;
+                }
+            }
             for (; step < steady_hi; ++step) {
                 const int r0 = ra + step * RS;
-                while (waited < need) {
+                if (waited < need) {
                     mbar_wait_u<kHint>(full_t_u + 8u * wslot, static_cast<unsigned>(wphase));
                     ++waited;
                     if (++wslot == G.ng) { wslot = 0; wphase ^= 1; }
                 }
                 need = min(last_grp_c, need + 1);
                 mbar_wait_u<kHint>(full_c_u + 8u * cslot, static_cast<unsigned>(cphase));
-                const char* cg = cut_lane + cslot * kCutBytes;
-                const char* pA = ring + static_cast<unsigned>(sA) * kRowBytes;
-                const char* pB = ring + static_cast<unsigned>(sB) * kRowBytes;
-                const char* pC = ring + static_cast<unsigned>(sC) * kRowBytes;
-                const char* pD = ring + static_cast<unsigned>(sD) * kRowBytes;
+                const unsigned cg = cut_s + cslot * kCutBytes;
                 double v[RS][CPT], thr[RS][CPT], sum[RS][CPT];
                 bool hit[RS][CPT];
                 bool any = false;
@@ -284,13 +332,12 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
 #pragma unroll
                     for (int j = 0; j < CPT; ++j) {
                         const unsigned o = k * kRowBytes;
-                        const double rs_o = dsub(dadd(tap(pA, K[j].xa + o), tap(pB, K[j].xb + o)),
-                                                 dadd(tap(pA, K[j].xb + o), tap(pB, K[j].xa + o)));
-                        const double rs_g = dsub(dadd(tap(pC, K[j].ya + o), tap(pD, K[j].yb + o)),
-                                                 dadd(tap(pC, K[j].yb + o), tap(pD, K[j].ya + o)));
+                        const double rs_o = dsub(dadd(lds_f64(xa[j] + oA + o), lds_f64(xb[j] + oB + o)),
+                                                 dadd(lds_f64(xb[j] + oA + o), lds_f64(xa[j] + oB + o)));
+                        const double rs_g = dsub(dadd(lds_f64(ya[j] + oC + o), lds_f64(yb[j] + oD + o)),
+                                                 dadd(lds_f64(yb[j] + oC + o), lds_f64(ya[j] + oD + o)));
                         sum[k][j] = dsub(rs_o, rs_g);
-                        v[k][j] = static_cast<double>(
-                            *reinterpret_cast<const T*>(cg + (k * kW + j * kWarp) * sizeof(T)));
+                        v[k][j] = lds_widen<T>(cg + (k * kW + j * kWarp) * sizeof(T));
                         any |= !(v[k][j] < dmul(sum[k][j], fast_k[j])) || v[k][j] < 0.0;
                     }
                 }
@@ -312,30 +359,31 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
                         }
                     }
                     emit_block<RS, CPT>(L, map, r0, r0 + RS - 1, wc0, c0 + tc, okc, hit, v, thr, false);
-                } else if (lane < CPT * RS && L.mask_bits) { // no hit in the block: zero mask words
-                    const int wk = lane / CPT, wc = wc0 + (lane % CPT) * kWarp;
-                    if (wc < cols)
-                        L.mask_bits[map * L.mask_map_stride + (r0 + wk - L.geo.row_lo) * L.words_per_row +
-                                    (wc >> 5)] = 0u;
+                } else if (mword) { // no hit in the block: zero mask words
+                    *mword = 0u;
                 }
+                if (mword) mword += mstep;
                 __syncwarp();
                 if (lane == 0) {
                     mbar_arrive_u(empty_c_u + 8u * cslot);
-                    if (step + 1 < n_steps) {
-                        while (released < done) {
-                            ++released;
-                            mbar_arrive_u(empty_t_u + 8u * rslot);
-                            if (++rslot == G.ng) rslot = 0;
-                        }
+                    if (step + 1 < n_steps && released < done) {
+                        ++released;
+                        mbar_arrive_u(empty_t_u + 8u * rslot);
+                        if (++rslot == G.ng) rslot = 0;
                     }
                 }
                 ++done;
                 if (++cslot == kCutGroups) { cslot = 0; cphase ^= 1; }
-                sA += RS; if (sA >= G.nr) sA -= G.nr;
-                sB += RS; if (sB >= G.nr) sB -= G.nr;
-                sC += RS; if (sC >= G.nr) sC -= G.nr;
-                sD += RS; if (sD >= G.nr) sD -= G.nr;
+                constexpr unsigned kAdv = RS * kRowBytes;
+                oA += kAdv; if (oA >= ring_end) oA -= ring_end;
+                oB += kAdv; if (oB >= ring_end) oB -= ring_end;
+                oC += kAdv; if (oC >= ring_end) oC -= ring_end;
+                oD += kAdv; if (oD >= ring_end) oD -= ring_end;
             }
+            sA = static_cast<int>(oA / kRowBytes);
+            sB = static_cast<int>(oB / kRowBytes);
+            sC = static_cast<int>(oC / kRowBytes);
+            sD = static_cast<int>(oD / kRowBytes);
             if (step >= n_steps) break;
         }
         const int r0 = ra + step * RS;
