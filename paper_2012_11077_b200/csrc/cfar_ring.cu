@@ -299,7 +299,13 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
                 ya[j] = ring_s + K[j].ya;
                 yb[j] = ring_s + K[j].yb;
             }
-            const unsigned cut_s = smem_u32(cuts + tc);
+            unsigned cut_s = smem_u32(cuts + tc);
+            // opaque: keep these shared-window addresses in registers instead of
+            // re-deriving the window base every step
+            unsigned ft_u = full_t_u, fc_u = full_c_u, ec_u = empty_c_u, et_u = empty_t_u;
+            asm volatile("" : "+r"(cut_s), "+r"(ft_u), "+r"(fc_u), "+r"(ec_u), "+r"(et_u));
+#pragma unroll
+            for (int j = 0; j < CPT; ++j) asm volatile("" : "+r"(xa[j]), "+r"(xb[j]), "+r"(ya[j]), "+r"(yb[j]));
             // lane k*CPT+j owns mask word (row r0 + k, column word of wc0 + 32 j)
             uint32_t* mword = nullptr;
             if (L.mask_bits && lane < CPT * RS && wc0 + (lane % CPT) * kWarp < cols)
@@ -317,12 +323,12 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
             for (; step < steady_hi; ++step) {
                 const int r0 = ra + step * RS;
                 if (waited < need) {
-                    mbar_wait_u<kHint>(full_t_u + 8u * wslot, static_cast<unsigned>(wphase));
+                    mbar_wait_u<kHint>(ft_u + 8u * wslot, static_cast<unsigned>(wphase));
                     ++waited;
                     if (++wslot == G.ng) { wslot = 0; wphase ^= 1; }
                 }
                 need = min(last_grp_c, need + 1);
-                mbar_wait_u<kHint>(full_c_u + 8u * cslot, static_cast<unsigned>(cphase));
+                mbar_wait_u<kHint>(fc_u + 8u * cslot, static_cast<unsigned>(cphase));
                 const unsigned cg = cut_s + cslot * kCutBytes;
                 double v[RS][CPT], thr[RS][CPT], sum[RS][CPT];
                 bool hit[RS][CPT];
@@ -365,10 +371,10 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
                 if (mword) mword += mstep;
                 __syncwarp();
                 if (lane == 0) {
-                    mbar_arrive_u(empty_c_u + 8u * cslot);
+                    mbar_arrive_u(ec_u + 8u * cslot);
                     if (step + 1 < n_steps && released < done) {
                         ++released;
-                        mbar_arrive_u(empty_t_u + 8u * rslot);
+                        mbar_arrive_u(et_u + 8u * rslot);
                         if (++rslot == G.ng) rslot = 0;
                     }
                 }
