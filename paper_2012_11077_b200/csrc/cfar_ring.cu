@@ -307,12 +307,12 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
 #pragma unroll
             for (int j = 0; j < CPT; ++j) asm volatile("" : "+r"(xa[j]), "+r"(xb[j]), "+r"(ya[j]), "+r"(yb[j]));
             // lane k*CPT+j owns mask word (row r0 + k, column word of wc0 + 32 j)
-            uint32_t* mword = nullptr;
-            if (L.mask_bits && lane < CPT * RS && wc0 + (lane % CPT) * kWarp < cols)
-                mword = L.mask_bits + map * L.mask_map_stride +
-                        (ra + step * RS + lane / CPT - L.geo.row_lo) * L.words_per_row +
-                        ((wc0 + (lane % CPT) * kWarp) >> 5);
-            const int64_t mstep = RS * L.words_per_row;
+            const bool has_word = L.mask_bits && lane < CPT * RS && wc0 + (lane % CPT) * kWarp < cols;
+            uint32_t* mword = has_word ? L.mask_bits + map * L.mask_map_stride +
+                                             (ra + step * RS + lane / CPT - L.geo.row_lo) * L.words_per_row +
+                                             ((wc0 + (lane % CPT) * kWarp) >> 5)
+                                       : nullptr;
+            const int64_t mstep = has_word ? RS * L.words_per_row : 0;
             if (lane == 0 && step + 1 < n_steps) { // catch up the hand-backs; then one per step
                 while (released < done - 1) {
                     ++released;
@@ -365,10 +365,10 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
                         }
                     }
                     emit_block<RS, CPT>(L, map, r0, r0 + RS - 1, wc0, c0 + tc, okc, hit, v, thr, false);
-                } else if (mword) { // no hit in the block: zero mask words
+                } else if (has_word) { // no hit in the block: zero mask words
                     *mword = 0u;
                 }
-                if (mword) mword += mstep;
+                mword += mstep;
                 __syncwarp();
                 if (lane == 0) {
                     mbar_arrive_u(ec_u + 8u * cslot);
