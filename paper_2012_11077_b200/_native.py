@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(HERE, "lib", "libuwbvital_b200.so")
 DROPIN_PATH = os.path.join(HERE, "lib", "libuwbvital.so")
 
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"{LIB_PATH} is missing; build it with `python -m paper_2012_11077_b200.build` "
+    raise ImportError(f"{LIB_PATH} is missing; build it with `python __graft_entry__.py` "
                       "(the package has no CPU fallback)")
 
 lib = C.CDLL(LIB_PATH)
