@@ -68,7 +68,9 @@ def main():
             if OURS.search(l):
                 f.write(l)
     full = summarize(os.path.join(ROOT, "gpurun_out", f"prof_{tag}.ncu-rep"))
-    js = {}
+    # merge: kernels captured by other runs keep their entries
+    summ = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    js = json.load(open(summ)) if os.path.exists(summ) else {}
     with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_full.txt"), "w") as f:
         f.write(f"# {tag}: ncu --set full --clock-control none, bench.py --maps {maps} (one launch each, cfg3 maps)\n")
         for d in full:
@@ -85,7 +87,7 @@ def main():
             js[name] = {"tag": tag, "maps": maps, "dram_read_bytes": rd, "dram_write_bytes": wr,
                         "dram_bytes_per_launch_per_map": (rd + wr) / maps,
                         "duration": d["gpu__time_duration.sum"]}
-    with open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w") as f:
+    with open(summ, "w") as f:
         json.dump(js, f, indent=1)
     print(json.dumps(js, indent=1))
 
