@@ -235,7 +235,7 @@ __global__ void __launch_bounds__((kNcw + 1) * kWarp, OCC) cfar_fused_kernel(con
                     const unsigned need = static_cast<unsigned>(min(rows, b0 + kWarp));
                     if (avail < need) {
                         if (lane == 0)
-                            while (avail < need) avail = ld_acquire_u32(prog_in);
+                            avail = wait_count_geq(prog_in, need);
                         avail = __shfl_sync(0xffffffffu, avail, 0);
                     }
                     if (b0 + lane < rows) v = ge_in[b0 + lane];

@@ -45,6 +45,17 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+// Spin until *p >= need: relaxed polls (an acquire load per poll invalidates the
+// SM's whole L1 each time, which stalls the other warps on the SM), then one
+// acquire fence. Returns the value seen.
+__device__ __forceinline__ unsigned wait_count_geq(const unsigned* p, unsigned need) {
+    unsigned v;
+    do {
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    } while (v < need);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    return v;
+}
 __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }

@@ -201,7 +201,7 @@ sat_systolic_kernel(SatLaunch L) {
                 const unsigned need = static_cast<unsigned>(min(rows, base + kWarp));
                 if (avail < need) { // lane 0 acquires; the warp barrier extends the ordering
                     if (lane == 0)
-                        while (avail < need) avail = ld_acquire_u32(prog_in);
+                        avail = wait_count_geq(prog_in, need);
                     avail = __shfl_sync(0xffffffffu, avail, 0);
                 }
                 if (base + lane < rows) v = ge_in[base + lane];
