@@ -951,9 +951,8 @@ uwb_status uwb_detect(const double* frame, uint64_t m, uint64_t n, double fast_r
     F.L = static_cast<int64_t>(L);
     F.first_bin = static_cast<int64_t>(first);
     F.kept = static_cast<int64_t>(kept);
-    F.stage_mask = 3;
-    UWB_CUDA_TRY(launch_frontend_columns(F, s));
     std::vector<double> wr, wi;
+    cudaError_t fused = cudaErrorNotSupported;
     if (run_all) {
         twiddles(F.L, wr, wi);
         UWB_CUDA_TRY(d_wr.alloc(sizeof(double) * L, s));
@@ -964,8 +963,17 @@ uwb_status uwb_detect(const double* frame, uint64_t m, uint64_t n, double fast_r
         F.wr = d_wr.as<double>();
         F.wi = d_wi.as<double>();
         F.band = d_band.as<double>();
-        F.stage_mask = 4 | 8 | 16;
-        UWB_CUDA_TRY(launch_frontend_rows(F, s));
+        fused = launch_frontend_fused(F, s); // whole front end in two kernels when it applies
+        if (fused != cudaErrorNotSupported) UWB_CUDA_TRY(fused);
+    }
+    if (fused == cudaErrorNotSupported) {
+        // the columns stage also runs on its own: it reports non-finite samples
+        F.stage_mask = 3;
+        UWB_CUDA_TRY(launch_frontend_columns(F, s));
+        if (run_all) {
+            F.stage_mask = 4 | 8 | 16;
+            UWB_CUDA_TRY(launch_frontend_rows(F, s));
+        }
     }
     uint64_t bad = ~0ull;
     UWB_CUDA_TRY(cudaMemcpyAsync(&bad, d_bad.p, sizeof(bad), cudaMemcpyDeviceToHost, s));
@@ -1253,10 +1261,15 @@ uwb_status uwb_dev_detect_batch(const void* records, int32_t dtype, uint64_t n_r
     F.first_bin = static_cast<int64_t>(D.first);
     F.kept = static_cast<int64_t>(D.kept);
     F.band = band;
-    F.stage_mask = 3;
-    UWB_CUDA_TRY(launch_frontend_columns(F, s));
-    F.stage_mask = 4 | 8 | 16;
-    UWB_CUDA_TRY(launch_frontend_rows(F, s));
+    const cudaError_t fused = launch_frontend_fused(F, s);
+    if (fused == cudaErrorNotSupported) {
+        F.stage_mask = 3;
+        UWB_CUDA_TRY(launch_frontend_columns(F, s));
+        F.stage_mask = 4 | 8 | 16;
+        UWB_CUDA_TRY(launch_frontend_rows(F, s));
+    } else {
+        UWB_CUDA_TRY(fused);
+    }
     // CFAR over the band maps (pipeline.cpp:269-273)
     const int backend = cfg->backend == UWB_NAIVE ? UWB_NAIVE : UWB_INTEGRAL;
     if (uwb_status st = dev_cfar(b, cfg->cfar, d_alpha.as<double>(), backend, UWB_SAT_GLOBAL, 0, *out,

@@ -17,6 +17,7 @@
 //      for non-power-of-two lengths, so the band map reproduces the oracle bit for
 //      bit and FFTW within the reference tests' 1e-9.
 #include <cfloat>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -208,6 +209,285 @@ __global__ void __launch_bounds__(256) frontend_rows_kernel(FrontendLaunch F) {
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Fused detect() front end for L = 1024 (the batched device detect() path):
+// two kernels and no fp64 work frame in HBM.
+//
+// (f1) frontend_stats_kernel — one warp per 32 traces (columns) of one record:
+//      the 32 x m input block is staged in shared memory once, then each lane
+//      runs remove_dc's mean (pipeline.cpp:58-69) and detrend_linear's moment
+//      sums (:71-98) over its column, serially in the reference's order, and
+//      stores (mean, slope, intercept) per column. Non-finite samples are
+//      reported here (RadarFrame::validate, pipeline.cpp:27-38).
+// (f2) frontend_fft1024_kernel — one warp per range row: the row is read once
+//      (coalesced), detrended from the column statistics with the reference's
+//      expression, mean-filtered (:100-122) and normalised (:139-155) in
+//      registers / shared memory, then transformed by the radix-2 DIT of the
+//      FFT provider with the same twiddles and per-element operation order:
+//      stages 1..5 as 32-point FFTs in registers (lane t holds bit-reversed
+//      elements 32t..32t+31, which are the stride-32 samples starting at
+//      rev5(t)), a padded shared-memory transpose, stages 6..10 in registers
+//      with lane t holding elements 32a + t, pruned to the butterflies whose
+//      outputs reach the band bins (band select, :192-223). Every value that
+//      reaches the band map is produced by the same IEEE operations on the same
+//      operands as in frontend_rows_kernel, so the band map is bit-identical.
+template <typename T, bool kStage>
+__global__ void __launch_bounds__(32) frontend_stats_kernel(FrontendLaunch F) {
+    extern __shared__ __align__(16) unsigned char fs_raw[];
+    T* blk = reinterpret_cast<T*>(fs_raw);
+    const int lane = threadIdx.x;
+    const int64_t m = F.m, n = F.n, rec = blockIdx.y;
+    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * kWarp;
+    const int64_t c = c0 + lane;
+    const bool ok = c < n;
+    const T* x = static_cast<const T*>(F.frame) + rec * m * n + (ok ? c : 0);
+    if (kStage) {
+        // the 32-column block, every copy in flight at once (cp.async)
+        const T* base = static_cast<const T*>(F.frame) + rec * m * n + c0;
+        const unsigned sb = static_cast<unsigned>(__cvta_generic_to_shared(blk));
+        constexpr int kVec = 16 / sizeof(T); // elements per 16-byte copy
+        const bool vec = c0 + kWarp <= n && (reinterpret_cast<uintptr_t>(base) % 16) == 0 && (n * sizeof(T)) % 16 == 0;
+        if (vec) {
+            // lane: row (lane / 8) + 4 k, 16-byte piece lane % 8 (rows of 32 elements = 8 pieces for f32)
+            constexpr int kPieces = kWarp / kVec, kRowsPer = kWarp / kPieces;
+            const int pr = lane / kPieces, pc = lane % kPieces;
+            for (int64_t r = pr; r < m; r += kRowsPer)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + static_cast<unsigned>((r * kWarp + pc * kVec) * sizeof(T))),
+                             "l"(base + r * n + pc * kVec)
+                             : "memory");
+        } else if (ok) {
+            for (int64_t r = 0; r < m; ++r)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(sb + static_cast<unsigned>((r * kWarp + lane) * sizeof(T))),
+                             "l"(x + r * n), "n"(sizeof(T))
+                             : "memory");
+        }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+    }
+    if (!ok) return;
+    auto X = [&](int64_t r) -> double { return widen(kStage ? blk[r * kWarp + lane] : x[r * n]); };
+    const double dm = static_cast<double>(m);
+    // remove_dc: serial sum over fast time, then the mean (pipeline.cpp:62-66)
+    double sum = 0.0;
+    int64_t bad = -1;
+#pragma unroll 8
+    for (int64_t r = 0; r < m; ++r) {
+        const double v = X(r);
+        if (!isfinite(v) && bad < 0) bad = r;
+        sum = dadd(sum, v);
+    }
+    if (bad >= 0 && F.first_nonfinite)
+        report_min(F.first_nonfinite + rec, static_cast<unsigned long long>(bad * n + c));
+    const double mean = ddiv(sum, dm);
+    // detrend_linear on the DC-removed trace (pipeline.cpp:78-93)
+    const double sum_r = ddiv(dmul(dm, dsub(dm, 1.0)), 2.0);
+    const double sum_rr = ddiv(dmul(dmul(dsub(dm, 1.0), dm), dsub(dmul(2.0, dm), 1.0)), 6.0);
+    const double det = dsub(dmul(dm, sum_rr), dmul(sum_r, sum_r));
+    double sum_x = 0.0, sum_rx = 0.0;
+#pragma unroll 8
+    for (int64_t r = 0; r < m; ++r) {
+        const double v = dsub(X(r), mean);
+        sum_x = dadd(sum_x, v);
+        sum_rx = dadd(sum_rx, dmul(static_cast<double>(r), v));
+    }
+    const double slope = ddiv(dsub(dmul(dm, sum_rx), dmul(sum_r, sum_x)), det);
+    const double intercept = ddiv(dsub(sum_x, dmul(slope, sum_r)), dm);
+    double* st = F.work + rec * 3 * n;
+    st[c] = mean;
+    st[n + c] = slope;
+    st[2 * n + c] = intercept;
+}
+
+__host__ __device__ constexpr int rev5(int a) {
+    return ((a & 1) << 4) | ((a & 2) << 2) | (a & 4) | ((a & 8) >> 2) | ((a & 16) >> 4);
+}
+
+constexpr int kFftWarps = 4;                        // rows per CTA
+constexpr int kTw2 = 31 * kWarp;                    // stage 6..10 twiddles, [stage group][lane]
+constexpr int kTw1 = 32;                            // stage 1..5 twiddles (31 used)
+constexpr int kXpPitch = 33;                        // padded transpose pitch (doubles)
+constexpr int kWarpBuf = kXpPitch * kWarp;          // transpose buffer per warp (doubles; re, then im)
+constexpr size_t kFftSmem = sizeof(double) * (2 * kTw2 + 2 * kTw1 + kFftWarps * kWarpBuf);
+
+__device__ __forceinline__ void butterfly(double& ur, double& ui, double& br, double& bi, double w_r, double w_i) {
+    const double tr = dsub(dmul(w_r, br), dmul(w_i, bi));
+    const double ti = dadd(dmul(w_r, bi), dmul(w_i, br));
+    br = dsub(ur, tr);
+    bi = dsub(ui, ti);
+    ur = dadd(ur, tr);
+    ui = dadd(ui, ti);
+}
+
+// HALF = mean-filter half width (window / 2), or -1: any window (runtime loop)
+template <typename T, int HALF>
+__global__ void __launch_bounds__(kFftWarps * kWarp, 3) frontend_fft1024_kernel(FrontendLaunch F) {
+    extern __shared__ __align__(16) double fz[];
+    double* t2r = fz;              // [g * 32 + t]: stage 6 + s, group g = 2^s - 1 + b, element 32 b + t
+    double* t2i = t2r + kTw2;
+    double* t1r = t2i + kTw2;      // [2^lh - 1 + j]: stage lh + 1, butterfly offset j
+    double* t1i = t1r + kTw1;
+    const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+    // twiddle index of butterfly offset j at stage lh: j << (bits - lh - 1), bits = 10
+    for (int e = threadIdx.x; e < kTw2; e += blockDim.x) {
+        const int g = e / kWarp, t = e % kWarp;
+        const int sft = 31 - __clz(g + 1);          // stage lh = 5 + sft
+        const int b = g + 1 - (1 << sft);
+        const int idx = (kWarp * b + t) << (4 - sft);
+        t2r[e] = F.wr[idx];
+        t2i[e] = F.wi[idx];
+    }
+    for (int e = threadIdx.x; e < 31; e += blockDim.x) {
+        const int lh = 31 - __clz(e + 1);
+        const int j = e + 1 - (1 << lh);
+        const int idx = j << (9 - lh);
+        t1r[e] = F.wr[idx];
+        t1i[e] = F.wi[idx];
+    }
+    __syncthreads();
+    const int64_t m = F.m, n = F.n;
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * kFftWarps + warp; // across the batch
+    if (row >= m * (F.n_rec > 0 ? F.n_rec : 1)) return;
+    const int64_t rec = row / m, r = row % m;
+    double* xbuf = fz + 2 * kTw2 + 2 * kTw1 + warp * kWarpBuf;
+    double* zb = xbuf; // the detrended / normalised row (n <= 1024 < 33 * 32) before the transform
+
+    // ---- detrend from the column statistics: dsub(v, dadd(intercept, dmul(slope, r))) with
+    //      v = dsub(x, mean) (pipeline.cpp:66, :93)
+    const double* st = F.work + rec * 3 * n;
+    const T* xr = static_cast<const T*>(F.frame) + row * n;
+    const double rd = static_cast<double>(r);
+#pragma unroll 8
+    for (int j = 0; j < kWarp; ++j) {
+        const int c = kWarp * j + lane;
+        if (c < n) {
+            const double v = dsub(widen(xr[c]), __ldg(st + c));
+            zb[c] = dsub(v, dadd(__ldg(st + 2 * n + c), dmul(__ldg(st + n + c), rd)));
+        }
+    }
+    __syncwarp();
+    // ---- mean_filter_slow (pipeline.cpp:100-122): centred window, shrunk at the edges;
+    //      sum = ((0 + x[c-h]) + ...) + x[c+h], then / (2h + 1)
+    double f[kWarp];
+    const int nn = static_cast<int>(n);
+    const int half = HALF >= 0 ? HALF : static_cast<int>(F.window / 2);
+    auto edge_cell = [&](int c) {
+        int h = half;
+        if (c < h) h = c;
+        if (nn - 1 - c < h) h = nn - 1 - c;
+        double sum = 0.0;
+        for (int k = c - h; k <= c + h; ++k) sum = dadd(sum, zb[k]);
+        return ddiv(sum, static_cast<double>(2 * h + 1));
+    };
+#pragma unroll
+    for (int j = 0; j < kWarp; ++j) {
+        const int c = kWarp * j + lane;
+        f[j] = 0.0;
+        if (HALF == 0) {
+            if (c < nn) f[j] = zb[c];
+        } else if (HALF > 0) {
+            // interior cells (full window) with compile-time taps; the first and
+            // last HALF cells of the row take the shrinking window
+            const bool interior = c >= HALF && c + HALF < nn;
+            if (interior) {
+                double sum = 0.0;
+#pragma unroll
+                for (int k = -HALF; k <= HALF; ++k) sum = dadd(sum, zb[c + k]);
+                f[j] = ddiv(sum, static_cast<double>(2 * HALF + 1));
+            } else if (c < nn) {
+                f[j] = edge_cell(c);
+            }
+        } else if (c < nn) {
+            f[j] = F.window > 1 ? edge_cell(c) : zb[c];
+        }
+    }
+    // ---- normalize_slow (pipeline.cpp:139-155): divide by max(max |x|, eps)
+    double peak = 0.0;
+#pragma unroll
+    for (int j = 0; j < kWarp; ++j)
+        if (kWarp * j + lane < n) peak = fmax(peak, fabs(f[j]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) peak = fmax(peak, __shfl_xor_sync(0xffffffffu, peak, o));
+    const double scale = peak < F.epsilon ? F.epsilon : peak;
+    __syncwarp(); // every lane has read zb
+#pragma unroll
+    for (int j = 0; j < kWarp; ++j) {
+        const int c = kWarp * j + lane;
+        if (c < n) zb[c] = ddiv(f[j], scale);
+    }
+    __syncwarp();
+    // ---- bit-reversed load: element 32 t + a = sample 32 rev5(a) + rev5(t) (zero past n)
+    double yr[kWarp], yi[kWarp];
+    const int rt = rev5(lane);
+#pragma unroll
+    for (int a = 0; a < kWarp; ++a) {
+        const int src = kWarp * rev5(a) + rt;
+        yr[a] = src < n ? zb[src] : 0.0;
+        yi[a] = 0.0;
+    }
+    // ---- stages 1..5: butterflies (p, p + 2^lh) inside the lane's 32 elements
+    //      (offset j = 0 has the twiddle (1, -0): w * b is b itself for every
+    //      nonzero b, and zeros stay zeros, so those butterflies skip the product)
+#pragma unroll
+    for (int lh = 0; lh < 5; ++lh) {
+        const int hf = 1 << lh;
+#pragma unroll
+        for (int b = 0; b < 16; ++b) {
+            const int j = b & (hf - 1);
+            const int p = ((b >> lh) << (lh + 1)) + j;
+            const int q = p + hf;
+            if (j == 0) {
+                const double ur = yr[p], ui = yi[p];
+                yr[p] = dadd(ur, yr[q]);
+                yi[p] = dadd(ui, yi[q]);
+                yr[q] = dsub(ur, yr[q]);
+                yi[q] = dsub(ui, yi[q]);
+            } else {
+                butterfly(yr[p], yi[p], yr[q], yi[q], t1r[hf - 1 + j], t1i[hf - 1 + j]);
+            }
+        }
+    }
+    // ---- transpose (padded pitch: conflict-free both ways): lane t then holds elements 32 a + t
+    __syncwarp();
+#pragma unroll
+    for (int a = 0; a < kWarp; ++a) xbuf[kXpPitch * lane + a] = yr[a];
+    __syncwarp();
+#pragma unroll
+    for (int a = 0; a < kWarp; ++a) yr[a] = xbuf[kXpPitch * a + lane];
+    __syncwarp();
+#pragma unroll
+    for (int a = 0; a < kWarp; ++a) xbuf[kXpPitch * lane + a] = yi[a];
+    __syncwarp();
+#pragma unroll
+    for (int a = 0; a < kWarp; ++a) yi[a] = xbuf[kXpPitch * a + lane];
+    // ---- stages 6..10 (pairs a, a + 2^s in registers); the last stage only forms
+    //      the outputs at or below L/2 (registers 0..16)
+#pragma unroll
+    for (int sft = 0; sft < 5; ++sft) {
+        const int sb = 1 << sft;
+#pragma unroll
+        for (int a0 = 0; a0 < kWarp; ++a0) {
+            if (a0 & sb) continue;
+            const int a1 = a0 + sb;
+            const int g = sb - 1 + (a0 & (sb - 1));
+            const double w_r = t2r[g * kWarp + lane], w_i = t2i[g * kWarp + lane];
+            if (sft < 4 || a1 == 16) {
+                butterfly(yr[a0], yi[a0], yr[a1], yi[a1], w_r, w_i);
+            } else {
+                const double br = yr[a1], bi = yi[a1];
+                yr[a0] = dadd(yr[a0], dsub(dmul(w_r, br), dmul(w_i, bi)));
+                yi[a0] = dadd(yi[a0], dadd(dmul(w_r, bi), dmul(w_i, br)));
+            }
+        }
+    }
+    // ---- |X|^2 of the band bins (pipeline.cpp:183-188, :211-219)
+    const int k_lo = static_cast<int>(F.first_bin), k_hi = static_cast<int>(F.first_bin + F.kept); // bins [k_lo, k_hi)
+#pragma unroll
+    for (int a = 0; a <= 16; ++a) {
+        const int k = kWarp * a + lane;
+        if (k >= k_lo && k < k_hi) F.band[row * F.kept + (k - k_lo)] = dadd(dmul(yr[a], yr[a]), dmul(yi[a], yi[a]));
+    }
+}
 } // namespace
 
 cudaError_t launch_frontend_columns(const FrontendLaunch& F, cudaStream_t stream) {
@@ -232,6 +512,72 @@ cudaError_t launch_frontend_rows(const FrontendLaunch& F, cudaStream_t stream) {
     ++g_kernel_launches;
     const dim3 grid(static_cast<unsigned>(F.m), static_cast<unsigned>(F.n_rec > 0 ? F.n_rec : 1));
     frontend_rows_kernel<<<grid, 256, smem, stream>>>(F);
+    return cudaGetLastError();
+}
+
+} // namespace uwb
+
+namespace uwb {
+
+namespace {
+template <typename T, int HALF>
+cudaError_t launch_fft(const FrontendLaunch& F, dim3 grid, cudaStream_t stream) {
+    cudaError_t e = cudaFuncSetAttribute(frontend_fft1024_kernel<T, HALF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kFftSmem));
+    if (e != cudaSuccess) return e;
+    frontend_fft1024_kernel<T, HALF><<<grid, kFftWarps * kWarp, kFftSmem, stream>>>(F);
+    return cudaSuccess;
+}
+template <typename T>
+cudaError_t launch_fft_half(const FrontendLaunch& F, int half, dim3 grid, cudaStream_t stream) {
+    switch (half) {
+        case 0: return launch_fft<T, 0>(F, grid, stream);
+        case 1: return launch_fft<T, 1>(F, grid, stream);
+        case 2: return launch_fft<T, 2>(F, grid, stream);
+        case 3: return launch_fft<T, 3>(F, grid, stream);
+        case 4: return launch_fft<T, 4>(F, grid, stream);
+        default: return launch_fft<T, -1>(F, grid, stream);
+    }
+}
+} // namespace
+
+// The fused front end (stats + fft1024) for the whole detect() front end;
+// cudaErrorNotSupported when the configuration needs the general kernels.
+cudaError_t launch_frontend_fused(const FrontendLaunch& F, cudaStream_t stream) {
+    if (const char* e = getenv("UWB_FE_FUSED"))
+        if (atoi(e) == 0) return cudaErrorNotSupported;
+    if (F.L != 1024 || F.n < 2 || F.n > 1024 || F.m < 3 || F.mode != 0 || F.full_power || !F.band || F.kept < 1 ||
+        F.first_bin < 0 || F.first_bin + F.kept > F.L / 2 + 1 || F.window < 1 || (F.window & 1) == 0)
+        return cudaErrorNotSupported;
+    const int64_t n_rec = F.n_rec > 0 ? F.n_rec : 1;
+    // (f1) column statistics into the work buffer (3 n doubles per record <= m n)
+    const size_t esz = F.dtype == UWB_F32 ? 4 : 8;
+    const size_t blk = static_cast<size_t>(F.m) * kWarp * esz;
+    const dim3 g1(static_cast<unsigned>((F.n + kWarp - 1) / kWarp), static_cast<unsigned>(n_rec));
+    cudaError_t e = cudaSuccess;
+    ++g_kernel_launches;
+    if (blk <= 112 * 1024) {
+        if (F.dtype == UWB_F32) {
+            e = cudaFuncSetAttribute(frontend_stats_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(blk));
+            if (e == cudaSuccess) frontend_stats_kernel<float, true><<<g1, kWarp, blk, stream>>>(F);
+        } else {
+            e = cudaFuncSetAttribute(frontend_stats_kernel<double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(blk));
+            if (e == cudaSuccess) frontend_stats_kernel<double, true><<<g1, kWarp, blk, stream>>>(F);
+        }
+    } else {
+        if (F.dtype == UWB_F32) frontend_stats_kernel<float, false><<<g1, kWarp, 0, stream>>>(F);
+        else frontend_stats_kernel<double, false><<<g1, kWarp, 0, stream>>>(F);
+    }
+    if (e != cudaSuccess) return e;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    // (f2) rows: detrend, filter, normalise, FFT, band power
+    const dim3 g2(static_cast<unsigned>((F.m * n_rec + kFftWarps - 1) / kFftWarps));
+    const int half = F.window <= 9 ? static_cast<int>(F.window / 2) : -1;
+    e = F.dtype == UWB_F32 ? launch_fft_half<float>(F, half, g2, stream) : launch_fft_half<double>(F, half, g2, stream);
+    ++g_kernel_launches;
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

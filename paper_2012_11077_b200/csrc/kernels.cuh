@@ -174,5 +174,8 @@ cudaError_t launch_frontend_columns(const FrontendLaunch& F, cudaStream_t stream
 cudaError_t launch_rfrm_transpose(const float* payload, int64_t n_rec, int64_t m, int64_t n, int out_dtype,
                                   void* frames, unsigned long long* first_bad, cudaStream_t stream);
 cudaError_t launch_frontend_rows(const FrontendLaunch& F, cudaStream_t stream);
+// stats + fft1024 kernels for the whole front end (detect paths); cudaErrorNotSupported
+// when the configuration needs launch_frontend_columns + launch_frontend_rows
+cudaError_t launch_frontend_fused(const FrontendLaunch& F, cudaStream_t stream);
 
 } // namespace uwb

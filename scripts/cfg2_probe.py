@@ -4,7 +4,8 @@ import paper_2012_11077_b200 as uwb
 from paper_2012_11077_b200 import synth
 from paper_2012_11077_b200.batch import DetectBatch
 
-n = 256
+import os
+n = int(os.environ.get("RECS", "1024"))
 recs = torch.stack([synth.cfg2_record(seed=2 + i, device="cuda") for i in range(n)]).contiguous()
 cfg = uwb.PipelineConfig(mean_filter_window=5, fft_length=1024, cfar=uwb.CfarParams(1, 4, 1e-3))
 db = DetectBatch(n, 512, 1024, cfg, prf=20.0, dtype=torch.float32, det_capacity=2048)

@@ -248,3 +248,63 @@ def test_detect_batch_reports_nonfinite_record(uwb, cuda):
     assert fb[0, 0] == np.uint64(0xFFFFFFFFFFFFFFFF) and fb[2, 0] == np.uint64(0xFFFFFFFFFFFFFFFF)
     with pytest.raises(uwb.InputError):
         db.check_inputs()
+
+
+@pytest.mark.parametrize("m,n,window,band,dtype", [
+    (512, 1024, 5, (0.3, 0.8), "float32"),     # config 2
+    (3, 1024, 5, (0.3, 0.8), "float64"),       # fewest rows the fused path takes
+    (40, 600, 7, (0.3, 0.8), "float32"),       # zero padding to L = 1024
+    (37, 1000, 1, (0.3, 0.8), "float64"),      # window 1 = identity
+    (64, 1024, 3, (2.0, 9.9), "float32"),      # wide band: bins 102..506 (most butterflies needed)
+    (16, 1024, 9, (9.95, 9.99), "float64"),    # band at the top of the spectrum (bins 509..511)
+])
+def test_fused_front_end_matches_reference(uwb, ref, cuda, m, n, window, band, dtype):
+    """The fused L = 1024 front end (column statistics + one-warp-per-row FFT,
+    csrc/frontend.cu) against the reference detect() per record, bit for bit,
+    and against the general kernels (UWB_FE_FUSED=0)."""
+    import os
+    import torch
+    from paper_2012_11077_b200.batch import DetectBatch
+    g = torch.Generator(device="cuda").manual_seed(m * 1000 + n)
+    recs = torch.randn((3, m, n), device="cuda", dtype=torch.float64, generator=g)
+    recs += torch.linspace(-1, 1, n, device="cuda", dtype=torch.float64)[None, None, :] * 0.3
+    recs += torch.sin(torch.arange(n, device="cuda", dtype=torch.float64) * 0.13)[None, None, :]
+    recs = recs.to(getattr(torch, dtype)).contiguous()
+    cfar = uwb.CfarParams(1, 1, 1e-2)
+    config = uwb.PipelineConfig(mean_filter_window=window, fft_length=1024, band_low_hz=band[0],
+                                band_high_hz=band[1], cfar=cfar)
+    outs = []
+    for fused in ("1", "0"):
+        os.environ["UWB_FE_FUSED"] = fused
+        try:
+            db = DetectBatch(3, m, n, config, prf=20.0, dtype=recs.dtype, det_capacity=1 << 14)
+            db(recs)
+            torch.cuda.synchronize()
+            db.check_inputs()
+            outs.append((db.band.cpu().numpy().copy(), [db.mask(i) for i in range(3)]))
+        finally:
+            os.environ.pop("UWB_FE_FUSED", None)
+    assert_bitwise(outs[0][0], outs[1][0], "fused vs general band maps")
+    host = recs.double().cpu().numpy()
+    for i in range(3):
+        exp = ref.detect(host[i], prf=20.0, mean_filter_window=window, fft_length=1024, band_low_hz=band[0],
+                         band_high_hz=band[1], guard_radius=1, background_radius=1, pfa=1e-2)
+        assert_bitwise(outs[0][0][i], exp["band_power"], f"record {i} band map")
+        assert np.array_equal(outs[0][1][i], exp["result"].mask), f"record {i} mask"
+
+
+def test_fused_front_end_reports_nonfinite(uwb, cuda):
+    import torch
+    from paper_2012_11077_b200.batch import DetectBatch
+    recs = torch.randn((3, 64, 1024), device="cuda", dtype=torch.float32)
+    recs[2, 9, 1000] = float("inf")
+    recs[2, 30, 3] = float("nan")
+    config = uwb.PipelineConfig(fft_length=1024, band_low_hz=0.3, band_high_hz=0.8, cfar=uwb.CfarParams(1, 2, 1e-3))
+    db = DetectBatch(3, 64, 1024, config, prf=20.0, dtype=torch.float32)
+    db(recs)
+    torch.cuda.synchronize()
+    fb = db.first_bad.cpu().numpy().astype(np.uint64)
+    assert fb[2, 0] == 9 * 1024 + 1000
+    assert fb[0, 0] == np.uint64(0xFFFFFFFFFFFFFFFF) and fb[1, 0] == np.uint64(0xFFFFFFFFFFFFFFFF)
+    with pytest.raises(uwb.InputError):
+        db.check_inputs()
