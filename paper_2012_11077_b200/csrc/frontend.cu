@@ -17,6 +17,7 @@
 //      for non-power-of-two lengths, so the band map reproduces the oracle bit for
 //      bit and FFTW within the reference tests' 1e-9.
 #include <cfloat>
+#include <cmath>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -232,65 +233,95 @@ __global__ void __launch_bounds__(256) frontend_rows_kernel(FrontendLaunch F) {
 //      outputs reach the band bins (band select, :192-223). Every value that
 //      reaches the band map is produced by the same IEEE operations on the same
 //      operands as in frontend_rows_kernel, so the band map is bit-identical.
-template <typename T, bool kStage>
+constexpr int kStatGroup = 16;        // rows per cp.async group of the stats kernel's ring
+constexpr int kStatRingBytes = 8192;  // ring size (measured: more CTAs per SM beat L2 reuse of the second pass)
+
+// Streams the 32-column block of rows [0, m) through a shared-memory ring
+// (cp.async, stat_slots<T>() - 1 groups in flight) and calls use(r, value) in row order.
+template <typename T>
+__host__ __device__ constexpr int stat_slots() { return kStatRingBytes / (kStatGroup * kWarp * static_cast<int>(sizeof(T))); }
+
+template <typename T, typename Use>
+__device__ __forceinline__ void stream_block(const T* base, int64_t n, int64_t m, bool vec, bool ok, T* ring, Use use) {
+    const int lane = threadIdx.x;
+    const unsigned sb = static_cast<unsigned>(__cvta_generic_to_shared(ring));
+    constexpr int kVec = 16 / sizeof(T);         // elements per 16-byte piece
+    constexpr int kPieces = kWarp / kVec;        // pieces per 32-element row
+    constexpr int kRowsPer = kWarp / kPieces;    // rows per warp-wide copy
+    const int64_t ngroups = (m + kStatGroup - 1) / kStatGroup;
+    auto issue = [&](int64_t g) {
+        if (g < ngroups) {
+            const unsigned slot = sb + static_cast<unsigned>((g % stat_slots<T>()) * kStatGroup * kWarp * sizeof(T));
+            const int64_t r0 = g * kStatGroup;
+            if (vec) {
+                const int pr = lane / kPieces, pc = lane % kPieces;
+                for (int rr = pr; rr < kStatGroup && r0 + rr < m; rr += kRowsPer)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                                     slot + static_cast<unsigned>((rr * kWarp + pc * kVec) * sizeof(T))),
+                                 "l"(base + (r0 + rr) * n + pc * kVec)
+                                 : "memory");
+            } else if (ok) {
+                for (int rr = 0; rr < kStatGroup && r0 + rr < m; ++rr)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(
+                                     slot + static_cast<unsigned>((rr * kWarp + lane) * sizeof(T))),
+                                 "l"(base + (r0 + rr) * n + lane), "n"(sizeof(T))
+                                 : "memory");
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    for (int g = 0; g < stat_slots<T>() - 1; ++g) issue(g);
+    for (int64_t g = 0; g < ngroups; ++g) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(stat_slots<T>() - 2) : "memory");
+        __syncwarp();
+        const T* slot = ring + (g % stat_slots<T>()) * kStatGroup * kWarp;
+        const int64_t r0 = g * kStatGroup;
+        if (r0 + kStatGroup <= m) {
+#pragma unroll
+            for (int rr = 0; rr < kStatGroup; ++rr) use(r0 + rr, widen(slot[rr * kWarp + lane]));
+        } else {
+            for (int rr = 0; r0 + rr < m; ++rr) use(r0 + rr, widen(slot[rr * kWarp + lane]));
+        }
+        __syncwarp(); // the slot is consumed before it is refilled
+        issue(g + stat_slots<T>() - 1);
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+template <typename T>
 __global__ void __launch_bounds__(32) frontend_stats_kernel(FrontendLaunch F) {
-    extern __shared__ __align__(16) unsigned char fs_raw[];
-    T* blk = reinterpret_cast<T*>(fs_raw);
+    __shared__ __align__(16) T ring[kStatRingBytes / sizeof(T)];
     const int lane = threadIdx.x;
     const int64_t m = F.m, n = F.n, rec = blockIdx.y;
     const int64_t c0 = static_cast<int64_t>(blockIdx.x) * kWarp;
     const int64_t c = c0 + lane;
     const bool ok = c < n;
-    const T* x = static_cast<const T*>(F.frame) + rec * m * n + (ok ? c : 0);
-    if (kStage) {
-        // the 32-column block, every copy in flight at once (cp.async)
-        const T* base = static_cast<const T*>(F.frame) + rec * m * n + c0;
-        const unsigned sb = static_cast<unsigned>(__cvta_generic_to_shared(blk));
-        constexpr int kVec = 16 / sizeof(T); // elements per 16-byte copy
-        const bool vec = c0 + kWarp <= n && (reinterpret_cast<uintptr_t>(base) % 16) == 0 && (n * sizeof(T)) % 16 == 0;
-        if (vec) {
-            // lane: row (lane / 8) + 4 k, 16-byte piece lane % 8 (rows of 32 elements = 8 pieces for f32)
-            constexpr int kPieces = kWarp / kVec, kRowsPer = kWarp / kPieces;
-            const int pr = lane / kPieces, pc = lane % kPieces;
-            for (int64_t r = pr; r < m; r += kRowsPer)
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + static_cast<unsigned>((r * kWarp + pc * kVec) * sizeof(T))),
-                             "l"(base + r * n + pc * kVec)
-                             : "memory");
-        } else if (ok) {
-            for (int64_t r = 0; r < m; ++r)
-                asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(sb + static_cast<unsigned>((r * kWarp + lane) * sizeof(T))),
-                             "l"(x + r * n), "n"(sizeof(T))
-                             : "memory");
-        }
-        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-        __syncwarp();
-    }
-    if (!ok) return;
-    auto X = [&](int64_t r) -> double { return widen(kStage ? blk[r * kWarp + lane] : x[r * n]); };
+    const T* base = static_cast<const T*>(F.frame) + rec * m * n + c0;
+    const bool vec = c0 + kWarp <= n && (reinterpret_cast<uintptr_t>(base) % 16) == 0 && (n * sizeof(T)) % 16 == 0;
     const double dm = static_cast<double>(m);
     // remove_dc: serial sum over fast time, then the mean (pipeline.cpp:62-66)
     double sum = 0.0;
     int64_t bad = -1;
-#pragma unroll 8
-    for (int64_t r = 0; r < m; ++r) {
-        const double v = X(r);
+    stream_block<T>(base, n, m, vec, ok, ring, [&](int64_t r, double v) {
         if (!isfinite(v) && bad < 0) bad = r;
         sum = dadd(sum, v);
-    }
-    if (bad >= 0 && F.first_nonfinite)
+    });
+    if (ok && bad >= 0 && F.first_nonfinite)
         report_min(F.first_nonfinite + rec, static_cast<unsigned long long>(bad * n + c));
     const double mean = ddiv(sum, dm);
-    // detrend_linear on the DC-removed trace (pipeline.cpp:78-93)
+    // detrend_linear on the DC-removed trace (pipeline.cpp:78-93); the second
+    // pass over the block is served by L2
     const double sum_r = ddiv(dmul(dm, dsub(dm, 1.0)), 2.0);
     const double sum_rr = ddiv(dmul(dmul(dsub(dm, 1.0), dm), dsub(dmul(2.0, dm), 1.0)), 6.0);
     const double det = dsub(dmul(dm, sum_rr), dmul(sum_r, sum_r));
     double sum_x = 0.0, sum_rx = 0.0;
-#pragma unroll 8
-    for (int64_t r = 0; r < m; ++r) {
-        const double v = dsub(X(r), mean);
+    __syncwarp();
+    stream_block<T>(base, n, m, vec, ok, ring, [&](int64_t r, double x) {
+        const double v = dsub(x, mean);
         sum_x = dadd(sum_x, v);
         sum_rx = dadd(sum_rx, dmul(static_cast<double>(r), v));
-    }
+    });
+    if (!ok) return;
     const double slope = ddiv(dsub(dmul(dm, sum_rx), dmul(sum_r, sum_x)), det);
     const double intercept = ddiv(dsub(sum_x, dmul(slope, sum_r)), dm);
     double* st = F.work + rec * 3 * n;
@@ -345,16 +376,17 @@ __global__ void __launch_bounds__(kFftWarps * kWarp, 3) frontend_fft1024_kernel(
         t1i[e] = F.wi[idx];
     }
     __syncthreads();
-    const int64_t m = F.m, n = F.n;
+    const int64_t m = F.m;
+    const int n = static_cast<int>(F.n), nn = n;
     const int64_t row = static_cast<int64_t>(blockIdx.x) * kFftWarps + warp; // across the batch
     if (row >= m * (F.n_rec > 0 ? F.n_rec : 1)) return;
     const int64_t rec = row / m, r = row % m;
     double* xbuf = fz + 2 * kTw2 + 2 * kTw1 + warp * kWarpBuf;
-    double* zb = xbuf; // the detrended / normalised row (n <= 1024 < 33 * 32) before the transform
+    double* zb = xbuf; // the row before the transform (n <= 1024 < 33 * 32)
+    const double* st = F.work + rec * 3 * n;                 // mean[n], slope[n], intercept[n] of this record
 
     // ---- detrend from the column statistics: dsub(v, dadd(intercept, dmul(slope, r))) with
     //      v = dsub(x, mean) (pipeline.cpp:66, :93)
-    const double* st = F.work + rec * 3 * n;
     const T* xr = static_cast<const T*>(F.frame) + row * n;
     const double rd = static_cast<double>(r);
 #pragma unroll 8
@@ -367,11 +399,19 @@ __global__ void __launch_bounds__(kFftWarps * kWarp, 3) frontend_fft1024_kernel(
     }
     __syncwarp();
     // ---- mean_filter_slow (pipeline.cpp:100-122): centred window, shrunk at the edges;
-    //      sum = ((0 + x[c-h]) + ...) + x[c+h], then / (2h + 1)
-    double f[kWarp];
-    const int nn = static_cast<int>(n);
+    //      sum = ((0 + x[c-h]) + ...) + x[c+h], then / (2h + 1). In place, one
+    //      32-cell block behind the reads (half <= 15, so block j reads no cell
+    //      of block j - 2); a small loop body keeps the kernel's code compact.
     const int half = HALF >= 0 ? HALF : static_cast<int>(F.window / 2);
-    auto edge_cell = [&](int c) {
+    auto filt = [&](int c) -> double {
+        if (HALF == 0) return zb[c];
+        if (HALF > 0 && c >= HALF && c + HALF < nn) { // interior: compile-time taps
+            double sum = 0.0;
+#pragma unroll
+            for (int k = -HALF; k <= HALF; ++k) sum = dadd(sum, zb[c + k]);
+            return ddiv(sum, static_cast<double>(2 * HALF + 1));
+        }
+        if (HALF < 0 && half == 0) return zb[c];
         int h = half;
         if (c < h) h = c;
         if (nn - 1 - c < h) h = nn - 1 - c;
@@ -379,41 +419,26 @@ __global__ void __launch_bounds__(kFftWarps * kWarp, 3) frontend_fft1024_kernel(
         for (int k = c - h; k <= c + h; ++k) sum = dadd(sum, zb[k]);
         return ddiv(sum, static_cast<double>(2 * h + 1));
     };
-#pragma unroll
-    for (int j = 0; j < kWarp; ++j) {
+    const int nblk = (nn + kWarp - 1) / kWarp;
+    double peak = 0.0, prev = 0.0;
+#pragma unroll 2
+    for (int j = 0; j < nblk; ++j) {
         const int c = kWarp * j + lane;
-        f[j] = 0.0;
-        if (HALF == 0) {
-            if (c < nn) f[j] = zb[c];
-        } else if (HALF > 0) {
-            // interior cells (full window) with compile-time taps; the first and
-            // last HALF cells of the row take the shrinking window
-            const bool interior = c >= HALF && c + HALF < nn;
-            if (interior) {
-                double sum = 0.0;
-#pragma unroll
-                for (int k = -HALF; k <= HALF; ++k) sum = dadd(sum, zb[c + k]);
-                f[j] = ddiv(sum, static_cast<double>(2 * HALF + 1));
-            } else if (c < nn) {
-                f[j] = edge_cell(c);
-            }
-        } else if (c < nn) {
-            f[j] = F.window > 1 ? edge_cell(c) : zb[c];
-        }
+        const double v = c < nn ? filt(c) : 0.0;
+        __syncwarp(); // block j's reads are done: block j - 1 may be overwritten
+        if (j > 0) zb[c - kWarp] = prev;
+        if (c < nn) peak = fmax(peak, fabs(v)); // normalize_slow's max |x| (pipeline.cpp:143-147)
+        prev = v;
     }
+    if (kWarp * (nblk - 1) + lane < nn) zb[kWarp * (nblk - 1) + lane] = prev;
     // ---- normalize_slow (pipeline.cpp:139-155): divide by max(max |x|, eps)
-    double peak = 0.0;
-#pragma unroll
-    for (int j = 0; j < kWarp; ++j)
-        if (kWarp * j + lane < n) peak = fmax(peak, fabs(f[j]));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) peak = fmax(peak, __shfl_xor_sync(0xffffffffu, peak, o));
     const double scale = peak < F.epsilon ? F.epsilon : peak;
-    __syncwarp(); // every lane has read zb
-#pragma unroll
-    for (int j = 0; j < kWarp; ++j) {
+#pragma unroll 4
+    for (int j = 0; j < nblk; ++j) {
         const int c = kWarp * j + lane;
-        if (c < n) zb[c] = ddiv(f[j], scale);
+        if (c < nn) zb[c] = ddiv(zb[c], scale);
     }
     __syncwarp();
     // ---- bit-reversed load: element 32 t + a = sample 32 rev5(a) + rev5(t) (zero past n)
@@ -547,29 +572,16 @@ cudaError_t launch_frontend_fused(const FrontendLaunch& F, cudaStream_t stream) 
     if (const char* e = getenv("UWB_FE_FUSED"))
         if (atoi(e) == 0) return cudaErrorNotSupported;
     if (F.L != 1024 || F.n < 2 || F.n > 1024 || F.m < 3 || F.mode != 0 || F.full_power || !F.band || F.kept < 1 ||
-        F.first_bin < 0 || F.first_bin + F.kept > F.L / 2 + 1 || F.window < 1 || (F.window & 1) == 0)
+        F.first_bin < 0 || F.first_bin + F.kept > F.L / 2 + 1 || F.window < 1 || (F.window & 1) == 0 ||
+        F.window > 31)
         return cudaErrorNotSupported;
     const int64_t n_rec = F.n_rec > 0 ? F.n_rec : 1;
     // (f1) column statistics into the work buffer (3 n doubles per record <= m n)
-    const size_t esz = F.dtype == UWB_F32 ? 4 : 8;
-    const size_t blk = static_cast<size_t>(F.m) * kWarp * esz;
     const dim3 g1(static_cast<unsigned>((F.n + kWarp - 1) / kWarp), static_cast<unsigned>(n_rec));
     cudaError_t e = cudaSuccess;
     ++g_kernel_launches;
-    if (blk <= 112 * 1024) {
-        if (F.dtype == UWB_F32) {
-            e = cudaFuncSetAttribute(frontend_stats_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(blk));
-            if (e == cudaSuccess) frontend_stats_kernel<float, true><<<g1, kWarp, blk, stream>>>(F);
-        } else {
-            e = cudaFuncSetAttribute(frontend_stats_kernel<double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(blk));
-            if (e == cudaSuccess) frontend_stats_kernel<double, true><<<g1, kWarp, blk, stream>>>(F);
-        }
-    } else {
-        if (F.dtype == UWB_F32) frontend_stats_kernel<float, false><<<g1, kWarp, 0, stream>>>(F);
-        else frontend_stats_kernel<double, false><<<g1, kWarp, 0, stream>>>(F);
-    }
+    if (F.dtype == UWB_F32) frontend_stats_kernel<float><<<g1, kWarp, 0, stream>>>(F);
+    else frontend_stats_kernel<double><<<g1, kWarp, 0, stream>>>(F);
     if (e != cudaSuccess) return e;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     // (f2) rows: detrend, filter, normalise, FFT, band power
