@@ -50,9 +50,11 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
 // acquire fence. Returns the value seen.
 __device__ __forceinline__ unsigned wait_count_geq(const unsigned* p, unsigned need) {
     unsigned v;
-    do {
+    for (;;) {
         asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    } while (v < need);
+        if (v >= need) break;
+        __nanosleep(100);
+    }
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
     return v;
 }

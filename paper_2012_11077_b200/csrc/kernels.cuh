@@ -82,6 +82,7 @@ struct SatLaunch {
     int elem_bytes;
     unsigned flags;      // bit 1: low-latency strip chain (set by the launcher)
     int cpl;             // columns per lane (strips of 32 * cpl columns): 1, 2 or 4
+    unsigned long long* trace; // debug (UWB_SAT_TRACE): 8 timestamps per tile, else null
 };
 
 struct SatJobView {

@@ -37,6 +37,8 @@
 #include <climits>
 #include <cstdlib>
 #include <type_traits>
+#include <vector>
+#include <cstdio>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -51,6 +53,10 @@ constexpr int kXSlots = 16;             // lane-private source ring (copy steps)
 constexpr int kOSlots = 8;              // lane-private result delay ring (rows)
 constexpr int kPublishEvery = 64;       // steps between edge hand-overs
 constexpr int kSatCtasPerSm = 3;        // occupancy target (registers and shared memory)
+#ifndef UWB_POLL_SLEEP_NS
+#define UWB_POLL_SLEEP_NS 200
+#endif
+constexpr unsigned kPollSleepNs = UWB_POLL_SLEEP_NS; // back-off between edge polls
 
 // Shared memory per CTA: the warps' source rings, the result rings and the
 // edge staging.
@@ -141,6 +147,16 @@ __device__ __forceinline__ double lds_d(unsigned addr) {
     return v;
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ double canon_edge(double v) {
+    return __double_as_longlong(v) == -1LL ? __longlong_as_double(0x7ff8000000000000LL) : v;
+}
+
 // Lane 31 (which produced the strip's edge column) releases the row count.
 __device__ __noinline__ void publish_rows(unsigned* prog, int rows_done, int lane) {
     if (lane == kWarp - 1 && rows_done > 0) st_release_u32(prog, static_cast<unsigned>(rows_done));
@@ -165,6 +181,9 @@ sat_systolic_kernel(SatLaunch L) {
     const unsigned edge_smem = base + kWarpsPerCta * (SM::kXRing + SM::kORing) + warp * kWarp * sizeof(double);
     const int64_t n_tiles = L.n_jobs * L.strips;
     const int cols = static_cast<int>(L.cols);
+    // flags bit 3: one strip warp per SM (a batch of at most one strip per SM is
+    // latency-bound on its dependent chain, which co-resident warps slow down)
+    if ((L.flags & 8u) && warp != 0) return;
 
     for (;;) {
         long long tile = 0;
@@ -172,6 +191,8 @@ sat_systolic_kernel(SatLaunch L) {
         tile = __shfl_sync(0xffffffffu, tile, 0);
         if (tile >= n_tiles) return;
 
+        unsigned long long* tr = L.trace ? L.trace + 8 * tile : nullptr;
+        if (tr && lane == 0) tr[0] = gtimer();
         // strip-major claim order: every job's strip k precedes any job's strip k+1
         const int strip = static_cast<int>(tile / L.n_jobs);
         const int64_t job = tile % L.n_jobs;
@@ -194,9 +215,24 @@ sat_systolic_kernel(SatLaunch L) {
         const double* ge_in = prog_in ? L.gedge + (job * L.strips + strip - 1) * L.edge_stride : nullptr;
         double* ge_out = prog_out ? L.gedge + (job * L.strips + strip) * L.edge_stride : nullptr;
         unsigned avail = 0;
+        // flags bit 4: the edge buffer holds a sentinel (all-ones NaN) until a
+        // row's value is stored, so a lane polls its own row's value and no row
+        // counter, fence or release is needed (low-latency chains)
+        const bool sentinel = (L.flags & 16u) != 0;
         // left-strip edge for rows [base, base+32) (lane k: row base + k)
         auto fetch_left = [&](int base) {
             double v = 0.0;
+            if (sentinel) {
+                if (prog_in && base + lane < rows) {
+                    const double* p = ge_in + base + lane;
+                    for (;;) { // back off between polls: spinning warps would load L2
+                        asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+                        if (__double_as_longlong(v) != -1LL) break;
+                        __nanosleep(kPollSleepNs);
+                    }
+                }
+                return v;
+            }
             if (prog_in && base < rows) { // warp-uniform
                 const unsigned need = static_cast<unsigned>(min(rows, base + kWarp));
                 if (avail < need) { // lane 0 acquires; the warp barrier extends the ordering
@@ -215,6 +251,7 @@ sat_systolic_kernel(SatLaunch L) {
                             ((ld * sizeof(T)) % kVecAlign) == 0;
         const bool warp_fast = __all_sync(0xffffffffu, vec_ok);
         const T* xrow = src + c + static_cast<int64_t>(kAhead - 8 * grp) * ld; // row staged at step 0
+        const bool solo = (L.flags & 8u) != 0;
         // a copy issued at step s lands in slot s mod 16
         auto stage = [&](unsigned slot_off, int row, const T* p, bool checked) {
             const unsigned dst = x_lane + slot_off;
@@ -302,11 +339,14 @@ sat_systolic_kernel(SatLaunch L) {
             if (act) {
                 // (6) edge column for the strip to the right (two rows per 16-byte store)
                 if (edge_lane) {
+                    // the all-ones NaN is the sentinel of flags bit 4; any NaN marks
+                    // a non-finite input, which the call reports as an error
+                    const double e_new = canon_edge(sv[kCpl - 1]), e_prev = canon_edge(prev[kCpl - 1]);
                     if (kChecked) {
-                        ge_out[r] = sv[kCpl - 1];
-                        if (u == 0 && r >= 1) ge_out[r - 1] = prev[kCpl - 1]; // row a fast block left unstored
+                        ge_out[r] = e_new;
+                        if (u == 0 && r >= 1) ge_out[r - 1] = e_prev; // row a fast block left unstored
                     } else if ((u & 1) == 0) { // r = s - 31 is odd
-                        *reinterpret_cast<double2*>(ge_out + r - 1) = make_double2(prev[kCpl - 1], sv[kCpl - 1]);
+                        *reinterpret_cast<double2*>(ge_out + r - 1) = make_double2(e_prev, e_new);
                     }
                 }
                 left_prev = left;
@@ -320,18 +360,23 @@ sat_systolic_kernel(SatLaunch L) {
         // (low-latency mode, for batches too small to fill the GPU: one block
         // ahead and hand-overs every 32 steps, which shortens the strip chain)
         const bool low_latency = (L.flags & 2u) != 0;
+        // flags bit 5: fetch the next block's edge at the end of the block (shorter
+        // chain lag, the fetch latency exposed once per block)
+        const bool late_fetch = low_latency && (L.flags & 32u) != 0;
         double e_cur = fetch_left(0);
         double e_next = low_latency ? 0.0 : fetch_left(kWarp);
         cp_async_wait<kAhead - 1>();
         lds_lane<kCpl>(x_lane + (x_rbase_lane & (kXSlots - 1)) * kXSlotBytes, xn);
+        if (tr && lane == 0) tr[1] = gtimer();
         for (int s0 = 0; s0 < steps; s0 += kWarp) {
+            if (tr && lane == 0 && s0 / kWarp < 5) tr[2 + s0 / kWarp] = gtimer(); // blocks 0..4
             // left-strip edge values for rows [s0, s0 + 32) (lane 0 reads row s at step s)
             __syncwarp();
             asm volatile("st.shared.f64 [%0], %1;" ::"r"(edge_smem + 8u * lane), "d"(e_cur) : "memory");
             __syncwarp();
             edge_n = lds_d(edge_smem);
             if (low_latency) {
-                e_cur = fetch_left(s0 + kWarp);
+                if (!late_fetch) e_cur = fetch_left(s0 + kWarp);
             } else {
                 e_cur = e_next;
                 e_next = fetch_left(s0 + 2 * kWarp);
@@ -343,6 +388,11 @@ sat_systolic_kernel(SatLaunch L) {
             if (fast) {
 #pragma unroll 16
                 for (int u = 0; u < kWarp; ++u) step(s0, u, std::false_type{});
+            } else if (solo && s0 + kWarp <= steps) {
+                // a chain-critical strip (one warp per SM): its first block is on
+                // every later strip's critical path, so it runs unrolled too
+#pragma unroll 16
+                for (int u = 0; u < kWarp; ++u) step(s0, u, std::true_type{});
             } else {
 #pragma unroll 1
                 for (int u = 0; u < kWarp && s0 + u < steps; ++u) step(s0, u, std::true_type{});
@@ -358,15 +408,17 @@ sat_systolic_kernel(SatLaunch L) {
                 if (bad != INT_MAX)
                     report_min(J.nonfinite, static_cast<unsigned long long>((J.row0 + bad) * L.cols + col));
             }
+            if (late_fetch) e_cur = fetch_left(s0 + kWarp);
             // hand over the edge rows stored so far (warp-uniform); a fast block
             // leaves its last row for the next block's paired store
             const int s_end = min(s0 + kWarp, steps);
             const int every = low_latency ? kWarp : kPublishEvery;
-            if (prog_out && ((s_end & (every - 1)) == 0 || s_end == steps))
+            if (!sentinel && prog_out && ((s_end & (every - 1)) == 0 || s_end == steps))
                 publish_rows(prog_out, min(rows, s_end - (kWarp - 1) - (fast ? 1 : 0)), lane);
         }
         cp_async_wait<0>();
         __syncwarp();
+        if (tr && lane == 0) tr[7] = gtimer();
     }
 }
 
@@ -384,13 +436,43 @@ static cudaError_t launch_sat_t(const SatLaunch& L, cudaStream_t stream) {
     // leave room for a concurrent CFAR on another stream (UWB_SAT_CTAS_PER_SM)
     if (const char* e = getenv("UWB_SAT_CTAS_PER_SM")) per_sm = std::min(per_sm, std::max(1, atoi(e)));
     const int64_t ctas = (n_tiles + kWarpsPerCta - 1) / kWarpsPerCta;
-    const int64_t grid = imin(ctas, static_cast<int64_t>(sms) * (per_sm > 0 ? per_sm : 1));
+    int64_t grid = imin(ctas, static_cast<int64_t>(sms) * (per_sm > 0 ? per_sm : 1));
     SatLaunch L2 = L;
     // batches that cannot fill the resident warps are latency-bound on the strip chain
     if (n_tiles < 2LL * sms * (per_sm > 0 ? per_sm : 1) * kWarpsPerCta) L2.flags |= 2u;
+    // at most one strip per SM: each strip gets an SM to itself
+    if (n_tiles <= sms) L2.flags |= 8u;
     if (const char* f = getenv("UWB_SAT_FLAGS")) L2.flags = static_cast<unsigned>(atoi(f));
+    // low-latency chains hand edges over through sentinel-initialised values
+    // (and, one strip per SM, fetch each block's left edge at the end of the
+    // previous block: 32 steps less lag per strip, measured 6% faster on 128 strips)
+    if ((L2.flags & 2u) && L.strips > 1 && !getenv("UWB_SAT_FLAGS")) L2.flags |= (L2.flags & 8u) ? 48u : 16u;
+    if (L2.flags & 8u) grid = imin(n_tiles, sms);
+    if ((L2.flags & 16u) && L.strips > 1) {
+        const cudaError_t me = cudaMemsetAsync(L.gedge, 0xff, sizeof(double) * L.n_jobs * L.strips * L.edge_stride, stream);
+        if (me != cudaSuccess) return me;
+    }
+    static unsigned long long* trace = nullptr;
+    const char* trace_file = getenv("UWB_SAT_TRACE");
+    if (trace_file) {
+        if (!trace) cudaMalloc(&trace, sizeof(unsigned long long) * 8 * 65536);
+        if (n_tiles <= 65536) L2.trace = trace;
+    }
     ++g_kernel_launches;
     sat_systolic_kernel<T, kCpl><<<static_cast<unsigned>(grid), kWarpsPerCta * kWarp, smem, stream>>>(L2);
+    if (L2.trace) { // debug dump: tile, 8 timestamps (ns)
+        std::vector<unsigned long long> h(8 * n_tiles);
+        cudaMemcpyAsync(h.data(), trace, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, stream);
+        cudaStreamSynchronize(stream);
+        if (FILE* f = fopen(trace_file, "w")) {
+            for (int64_t t = 0; t < n_tiles; ++t) {
+                fprintf(f, "%lld", static_cast<long long>(t));
+                for (int k = 0; k < 8; ++k) fprintf(f, " %llu", h[8 * t + k]);
+                fprintf(f, "\n");
+            }
+            fclose(f);
+        }
+    }
     return cudaGetLastError();
 }
 

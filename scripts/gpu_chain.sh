@@ -1,6 +1,6 @@
 export PYTHONPATH=.
-for c in 128 256 512 1024 4096 16384; do
-  echo "cols=$c $(COLS=$c timeout 120 python scripts/cfg4_probe.py 2>&1 | tail -1)"
-done
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+echo "16k $(timeout 120 python scripts/cfg4_probe.py 2>&1 | tail -1)"
 echo "cfg3 $(timeout 120 python scripts/cfar_probe.py | tail -1)"
-timeout 900 python -m pytest tests -m gpu -x -q ${TESTS:-tests/test_gpu_sat_cfar.py tests/test_gpu_fused.py} 2>&1 | tail -2
+for c in 4 1 6; do timeout -s KILL 900 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/cfg${c}_r01z3.log 2>&1; tail -1 gpurun_out/cfg${c}_r01z3.log | cut -c1-250; done
