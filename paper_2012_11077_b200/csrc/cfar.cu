@@ -180,18 +180,39 @@ __device__ int merge_path(const uwb_detection* a, int na, const uwb_detection* b
     return lo;
 }
 
+// Phase 1 of the detection sort: CTA (map, y) sorts run y of the map's list
+// (kSortRun entries) in shared memory, so the runs of one long list sort in parallel.
 __global__ void __launch_bounds__(kSortThreads)
-sort_detections_kernel(uwb_detection* dets, int64_t cap, const unsigned long long* counts,
-                       uwb_detection* scratch) {
+sort_runs_kernel(uwb_detection* dets, int64_t cap, const unsigned long long* counts) {
     extern __shared__ uwb_detection smem_det[];
     const int64_t map = blockIdx.x;
     const int64_t count = imin(static_cast<int64_t>(counts[map]), cap);
-    if (count <= 1) return;
+    const int64_t base = static_cast<int64_t>(blockIdx.y) * kSortRun;
+    if (count <= 1 || base >= count) return;
+    uwb_detection* src = dets + map * cap;
+    const int n = static_cast<int>(imin(kSortRun, count - base));
+    int p2 = 1;
+    while (p2 < n) p2 <<= 1;
+    for (int i = threadIdx.x; i < p2; i += blockDim.x) smem_det[i] = i < n ? src[base + i] : sentinel();
+    __syncthreads();
+    smem_bitonic(smem_det, p2);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) src[base + i] = smem_det[i];
+}
+
+// Phase 2: merge passes (merge path) over the sorted runs, one CTA per map
+// (runs_sorted = false: the CTA also sorts the runs itself, one after another).
+__global__ void __launch_bounds__(kSortThreads)
+sort_detections_kernel(uwb_detection* dets, int64_t cap, const unsigned long long* counts,
+                       uwb_detection* scratch, bool runs_sorted) {
+    extern __shared__ uwb_detection smem_det[];
+    const int64_t map = blockIdx.x;
+    const int64_t count = imin(static_cast<int64_t>(counts[map]), cap);
+    if (count <= 1 || (runs_sorted && count <= kSortRun)) return;
     uwb_detection* src = dets + map * cap;
     uwb_detection* alt = scratch ? scratch + map * cap : nullptr;
 
     // 1. sort runs of kSortRun in shared memory
-    for (int64_t base = 0; base < count; base += kSortRun) {
+    for (int64_t base = 0; !runs_sorted && base < count; base += kSortRun) {
         const int n = static_cast<int>(imin(kSortRun, count - base));
         int p2 = 1;
         while (p2 < n) p2 <<= 1;
@@ -271,8 +292,24 @@ cudaError_t launch_sort_detections(uwb_detection* dets, int64_t cap, const unsig
     cudaError_t e = cudaFuncSetAttribute(sort_detections_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
+    const int64_t runs = (cap + kSortRun - 1) / kSortRun;
+    if (runs > 1 && runs <= 65535 && n_maps <= 8) {
+        // few long lists (single large maps): the runs of a list sort in parallel
+        e = cudaFuncSetAttribute(sort_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        ++g_kernel_launches;
+        sort_runs_kernel<<<dim3(static_cast<unsigned>(n_maps), static_cast<unsigned>(runs)), kSortThreads, smem,
+                           stream>>>(dets, cap, counts);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        if (!scratch) return cudaSuccess;
+        ++g_kernel_launches;
+        sort_detections_kernel<<<static_cast<unsigned>(n_maps), kSortThreads, smem, stream>>>(dets, cap, counts, scratch,
+                                                                                            true);
+        return cudaGetLastError();
+    }
     ++g_kernel_launches;
-    sort_detections_kernel<<<static_cast<unsigned>(n_maps), kSortThreads, smem, stream>>>(dets, cap, counts, scratch);
+    sort_detections_kernel<<<static_cast<unsigned>(n_maps), kSortThreads, smem, stream>>>(dets, cap, counts, scratch,
+                                                                                        false);
     return cudaGetLastError();
 }
 
