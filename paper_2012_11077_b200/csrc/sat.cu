@@ -191,7 +191,7 @@ sat_systolic_kernel(SatLaunch L) {
         tile = __shfl_sync(0xffffffffu, tile, 0);
         if (tile >= n_tiles) return;
 
-        unsigned long long* tr = L.trace ? L.trace + 8 * tile : nullptr;
+        unsigned long long* tr = L.trace ? L.trace + 40 * tile : nullptr;
         if (tr && lane == 0) tr[0] = gtimer();
         // strip-major claim order: every job's strip k precedes any job's strip k+1
         const int strip = static_cast<int>(tile / L.n_jobs);
@@ -231,6 +231,7 @@ sat_systolic_kernel(SatLaunch L) {
                         __nanosleep(kPollSleepNs);
                     }
                 }
+                __syncwarp(); // reconverge: lanes whose rows came early must not run ahead alone
                 return v;
             }
             if (prog_in && base < rows) { // warp-uniform
@@ -392,7 +393,10 @@ sat_systolic_kernel(SatLaunch L) {
                 // a chain-critical strip (one warp per SM): its first block is on
                 // every later strip's critical path, so it runs unrolled too
 #pragma unroll 16
-                for (int u = 0; u < kWarp; ++u) step(s0, u, std::true_type{});
+                for (int u = 0; u < kWarp; ++u) {
+                    step(s0, u, std::true_type{});
+                    if (tr && lane == 0 && s0 == 0) tr[8 + u] = clock64();
+                }
             } else {
 #pragma unroll 1
                 for (int u = 0; u < kWarp && s0 + u < steps; ++u) step(s0, u, std::true_type{});
@@ -455,19 +459,19 @@ static cudaError_t launch_sat_t(const SatLaunch& L, cudaStream_t stream) {
     static unsigned long long* trace = nullptr;
     const char* trace_file = getenv("UWB_SAT_TRACE");
     if (trace_file) {
-        if (!trace) cudaMalloc(&trace, sizeof(unsigned long long) * 8 * 65536);
+        if (!trace) cudaMalloc(&trace, sizeof(unsigned long long) * 40 * 65536);
         if (n_tiles <= 65536) L2.trace = trace;
     }
     ++g_kernel_launches;
     sat_systolic_kernel<T, kCpl><<<static_cast<unsigned>(grid), kWarpsPerCta * kWarp, smem, stream>>>(L2);
     if (L2.trace) { // debug dump: tile, 8 timestamps (ns)
-        std::vector<unsigned long long> h(8 * n_tiles);
+        std::vector<unsigned long long> h(40 * n_tiles);
         cudaMemcpyAsync(h.data(), trace, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, stream);
         cudaStreamSynchronize(stream);
         if (FILE* f = fopen(trace_file, "w")) {
             for (int64_t t = 0; t < n_tiles; ++t) {
                 fprintf(f, "%lld", static_cast<long long>(t));
-                for (int k = 0; k < 8; ++k) fprintf(f, " %llu", h[8 * t + k]);
+                for (int k = 0; k < 40; ++k) fprintf(f, " %llu", h[40 * t + k]);
                 fprintf(f, "\n");
             }
             fclose(f);
