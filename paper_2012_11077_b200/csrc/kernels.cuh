@@ -82,7 +82,8 @@ struct SatLaunch {
     int elem_bytes;
     unsigned flags;      // bit 1: low-latency strip chain (set by the launcher)
     int cpl;             // columns per lane (strips of 32 * cpl columns): 1, 2 or 4
-    unsigned long long* trace; // debug (UWB_SAT_TRACE): 8 timestamps per tile, else null
+    unsigned long long* trace; // debug (UWB_SAT_TRACE): per tile: SM id, globaltimer at the first
+                               // fetch, blocks 0..4 and the end, clock64 after each first-block step
 };
 
 struct SatJobView {

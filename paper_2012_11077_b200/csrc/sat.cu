@@ -147,6 +147,9 @@ __device__ __forceinline__ double lds_d(unsigned addr) {
     return v;
 }
 
+// Zero source for the virtual rows r < 0 of a strip's first block (see step()).
+__device__ __align__(16) double g_sat_zero[4];
+
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -192,7 +195,11 @@ sat_systolic_kernel(SatLaunch L) {
         if (tile >= n_tiles) return;
 
         unsigned long long* tr = L.trace ? L.trace + 40 * tile : nullptr;
-        if (tr && lane == 0) tr[0] = gtimer();
+        if (tr && lane == 0) {
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            tr[0] = smid;
+        }
         // strip-major claim order: every job's strip k precedes any job's strip k+1
         const int strip = static_cast<int>(tile / L.n_jobs);
         const int64_t job = tile % L.n_jobs;
@@ -252,8 +259,8 @@ sat_systolic_kernel(SatLaunch L) {
                             ((ld * sizeof(T)) % kVecAlign) == 0;
         const bool warp_fast = __all_sync(0xffffffffu, vec_ok);
         const T* xrow = src + c + static_cast<int64_t>(kAhead - 8 * grp) * ld; // row staged at step 0
-        const bool solo = (L.flags & 8u) != 0;
         // a copy issued at step s lands in slot s mod 16
+        const T* zero_src = reinterpret_cast<const T*>(g_sat_zero);
         auto stage = [&](unsigned slot_off, int row, const T* p, bool checked) {
             const unsigned dst = x_lane + slot_off;
             if (!checked) {
@@ -266,6 +273,14 @@ sat_systolic_kernel(SatLaunch L) {
                 }
             }
         };
+        // mode-2 first block: every source slot starts as zero (virtual rows of
+        // lanes whose first slot is read before any copy lands in it)
+        const bool first_fast = kWarp + kAhead <= rows && warp_fast && !(L.flags & 64u);
+        if (first_fast) {
+            for (int sl = 0; sl < kXSlots; ++sl)
+                for (unsigned q = 0; q < SM::kXLane; q += 4)
+                    asm volatile("st.shared.u32 [%0], 0;" ::"r"(x_lane + sl * kXSlotBytes + q) : "memory");
+        }
         // prologue: virtual steps -kAhead..-1 stage rows -8g .. kAhead-1-8g
 #pragma unroll
         for (int v = -kAhead; v < 0; ++v) {
@@ -291,14 +306,21 @@ sat_systolic_kernel(SatLaunch L) {
         T xn[kCpl];          // source values of the next step (loaded one step ahead)
         double edge_n = 0.0; // lane 0: left strip's edge for the next step
 
-        // One systolic step. kChecked: range checks on rows (prologue/epilogue blocks).
-        auto step = [&](const int s0, const int u, auto checked_tag) {
-            constexpr bool kChecked = decltype(checked_tag)::value;
+        // One systolic step. Mode 0: interior block, no checks. Mode 1: range
+        // checks on rows (last block, short maps). Mode 2: the first block as
+        // straight-line code: a lane whose row r = s - lane is still negative
+        // computes a virtual row of zeros (its source slots read zero: the ring
+        // is zeroed at the tile start and rows < 0 copy from a zero buffer; its
+        // state is zero, so S stays 0), and only the table and edge stores are
+        // predicated.
+        auto step = [&](const int s0, const int u, auto mode_tag) {
+            constexpr int kMode = decltype(mode_tag)::value;
+            constexpr bool kChecked = kMode == 1, kFirst = kMode == 2;
             const int s = s0 + u;
             const int r = s - lane;
             // (1) group g writes back row s - 8g - 8 (slot u mod 8, stored >= 1 step ago)
             const int rf = s - 8 * grp - 8;
-            if (!kChecked || (rf >= 0 && rf < rows)) {
+            if (kFirst ? rf >= 0 : (!kChecked || (rf >= 0 && rf < rows))) {
                 double o[kCpl];
                 lds_out<kCpl>(o_lane + static_cast<unsigned>(u & (kOSlots - 1)) * kOSlotBytes, o);
                 if (!kChecked || nvalid == kCpl) {
@@ -317,7 +339,13 @@ sat_systolic_kernel(SatLaunch L) {
             }
             tflush += tld;
             // (2) stage source row s + kAhead - 8g into slot u (s0 is a multiple of 32)
-            stage(static_cast<unsigned>((u & (kXSlots - 1)) * kXSlotBytes), s + kAhead - 8 * grp, xrow, kChecked);
+            if (kFirst) {
+                const int row = s + kAhead - 8 * grp;
+                cp_async_lane<T, kCpl>(x_lane + static_cast<unsigned>((u & (kXSlots - 1)) * kXSlotBytes),
+                                       row >= 0 ? xrow : zero_src);
+            } else {
+                stage(static_cast<unsigned>((u & (kXSlots - 1)) * kXSlotBytes), s + kAhead - 8 * grp, xrow, kChecked);
+            }
             cp_async_commit();
             xrow += ld;
             // (3) this step's inputs were loaded one step ahead; load the next step's
@@ -346,7 +374,7 @@ sat_systolic_kernel(SatLaunch L) {
                     if (kChecked) {
                         ge_out[r] = e_new;
                         if (u == 0 && r >= 1) ge_out[r - 1] = e_prev; // row a fast block left unstored
-                    } else if ((u & 1) == 0) { // r = s - 31 is odd
+                    } else if ((u & 1) == 0 && (!kFirst || r >= 1)) { // r = s - 31 is odd
                         *reinterpret_cast<double2*>(ge_out + r - 1) = make_double2(e_prev, e_new);
                     }
                 }
@@ -388,18 +416,18 @@ sat_systolic_kernel(SatLaunch L) {
             const bool fast = s0 >= kWarp && s0 + kWarp + kAhead <= rows && warp_fast;
             if (fast) {
 #pragma unroll 16
-                for (int u = 0; u < kWarp; ++u) step(s0, u, std::false_type{});
-            } else if (solo && s0 + kWarp <= steps) {
-                // a chain-critical strip (one warp per SM): its first block is on
-                // every later strip's critical path, so it runs unrolled too
+                for (int u = 0; u < kWarp; ++u) step(s0, u, std::integral_constant<int, 0>{});
+            } else if (first_fast && s0 == 0) {
+                // the first block at interior speed (it is on every later strip's
+                // critical path in a chain)
 #pragma unroll 16
                 for (int u = 0; u < kWarp; ++u) {
-                    step(s0, u, std::true_type{});
-                    if (tr && lane == 0 && s0 == 0) tr[8 + u] = clock64();
+                    step(s0, u, std::integral_constant<int, 2>{});
+                    if (tr && lane == 0) tr[8 + u] = clock64();
                 }
             } else {
 #pragma unroll 1
-                for (int u = 0; u < kWarp && s0 + u < steps; ++u) step(s0, u, std::true_type{});
+                for (int u = 0; u < kWarp && s0 + u < steps; ++u) step(s0, u, std::integral_constant<int, 1>{});
             }
             // non-finite inputs poison every later S of their column (see header)
             bool finite = true;
