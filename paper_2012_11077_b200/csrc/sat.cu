@@ -119,6 +119,11 @@ __device__ __forceinline__ void lds_lane(unsigned addr, double (&x)[kCpl]) {
             asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x[2 * q]), "=d"(x[2 * q + 1]) : "r"(addr + 16u * q));
     }
 }
+// Result delay ring: a lane's kCpl doubles of one row are split into 16-byte
+// halves stored kOHalf apart, so each 16-byte access of the warp is one
+// contiguous 512-byte run (no bank conflicts; a 32-byte lane stride conflicts 2-way).
+constexpr unsigned kOHalf = kWarp * 16u;
+
 template <int kCpl>
 __device__ __forceinline__ void sts_out(unsigned addr, const double (&v)[kCpl]) {
     if constexpr (kCpl == 1) {
@@ -126,7 +131,7 @@ __device__ __forceinline__ void sts_out(unsigned addr, const double (&v)[kCpl]) 
     } else {
 #pragma unroll
         for (int q = 0; q < kCpl / 2; ++q)
-            asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr + 16u * q), "d"(v[2 * q]), "d"(v[2 * q + 1])
+            asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr + kOHalf * q), "d"(v[2 * q]), "d"(v[2 * q + 1])
                          : "memory");
     }
 }
@@ -137,7 +142,7 @@ __device__ __forceinline__ void lds_out(unsigned addr, double (&v)[kCpl]) {
     } else {
 #pragma unroll
         for (int q = 0; q < kCpl / 2; ++q)
-            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[2 * q]), "=d"(v[2 * q + 1]) : "r"(addr + 16u * q)
+            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[2 * q]), "=d"(v[2 * q + 1]) : "r"(addr + kOHalf * q)
                          : "memory");
     }
 }
@@ -180,7 +185,7 @@ sat_systolic_kernel(SatLaunch L) {
     const unsigned raw = smem_u32(sat_smem_raw);
     const unsigned base = (raw + 15u) & ~15u;
     const unsigned x_lane = base + warp * SM::kXRing + lane * SM::kXLane; // slot 0, my columns
-    const unsigned o_lane = base + kWarpsPerCta * SM::kXRing + warp * SM::kORing + lane * SM::kOLane;
+    const unsigned o_lane = base + kWarpsPerCta * SM::kXRing + warp * SM::kORing + lane * (kCpl == 1 ? 8u : 16u);
     const unsigned edge_smem = base + kWarpsPerCta * (SM::kXRing + SM::kORing) + warp * kWarp * sizeof(double);
     const int64_t n_tiles = L.n_jobs * L.strips;
     const int cols = static_cast<int>(L.cols);
