@@ -231,6 +231,7 @@ sat_systolic_kernel(SatLaunch L) {
         // row's value is stored, so a lane polls its own row's value and no row
         // counter, fence or release is needed (low-latency chains)
         const bool sentinel = (L.flags & 16u) != 0;
+        const bool poll_sleep = (L.flags & 128u) == 0; // flags bit 7: spin without back-off
         // left-strip edge for rows [base, base+32) (lane k: row base + k)
         auto fetch_left = [&](int base) {
             double v = 0.0;
@@ -240,7 +241,7 @@ sat_systolic_kernel(SatLaunch L) {
                     for (;;) { // back off between polls: spinning warps would load L2
                         asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
                         if (__double_as_longlong(v) != -1LL) break;
-                        __nanosleep(kPollSleepNs);
+                        if (poll_sleep) __nanosleep(kPollSleepNs);
                     }
                 }
                 __syncwarp(); // reconverge: lanes whose rows came early must not run ahead alone
