@@ -293,8 +293,8 @@ cudaError_t launch_sort_detections(uwb_detection* dets, int64_t cap, const unsig
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     const int64_t runs = (cap + kSortRun - 1) / kSortRun;
-    if (runs > 1 && runs <= 65535 && n_maps <= 8) {
-        // few long lists (single large maps): the runs of a list sort in parallel
+    if (runs > 1 && runs <= 65535) {
+        // long lists: the runs of every list sort in parallel CTAs
         e = cudaFuncSetAttribute(sort_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (e != cudaSuccess) return e;
         ++g_kernel_launches;

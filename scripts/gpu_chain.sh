@@ -1,6 +1,4 @@
 export PYTHONPATH=.
-mkdir -p gpurun_out
-echo "16k sleep $(timeout 120 python scripts/cfg4_probe.py 2>&1 | tail -1)"
-echo "16k spin $(UWB_SAT_FLAGS=186 timeout 120 python scripts/cfg4_probe.py 2>&1 | tail -1)"
-echo "16k sleep-expl $(UWB_SAT_FLAGS=58 timeout 120 python scripts/cfg4_probe.py 2>&1 | tail -1)"
-UWB_SAT_FLAGS=186 UWB_SAT_TRACE=gpurun_out/trace_spin.txt REPS=1 timeout 120 python scripts/cfg4_probe.py 2>&1 | tail -1
+timeout 900 python -m pytest tests/test_gpu_batch.py tests/test_gpu_fullsize.py tests/test_gpu_sat_cfar.py -m gpu -x -q 2>&1 | tail -2
+timeout -s KILL 900 python bench.py --config 5 --steps 5 --warmup 3 > gpurun_out/cfg5_r01z6.log 2>&1; tail -1 gpurun_out/cfg5_r01z6.log | cut -c1-200
+timeout -s KILL 900 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/cfg3_r01z6.log 2>&1; tail -1 gpurun_out/cfg3_r01z6.log | cut -c1-200
