@@ -149,8 +149,8 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
     const int rows = static_cast<int>(L.geo.rows), cols = static_cast<int>(L.cols);
     const int hr = L.hr, hc = L.hc, gr = L.gr, gc = L.gc;
     const int c0 = col_tile * kW;
-    const int ra = static_cast<int>(L.geo.owned_begin(slab)) + chunk * kRingRows;
-    const int rb = min(ra + kRingRows, static_cast<int>(L.geo.owned_end(slab)));
+    const int ra = static_cast<int>(L.geo.owned_begin(slab)) + chunk * static_cast<int>(L.ring_rows);
+    const int rb = min(ra + static_cast<int>(L.ring_rows), static_cast<int>(L.geo.owned_end(slab)));
     if (ra >= rb) return;
     const int trow0 = static_cast<int>(L.geo.table_begin(slab));
 
@@ -273,7 +273,10 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
     // group and one CUT group, and frees one of each, so the bookkeeping is a few
     // increments; the step body is the fast path below.
     const int steady_lo = max(0, (hr - ra + RS - 1) / RS);
-    const int steady_hi = min(n_steps, min((rb - RS - ra) / RS, (rows - RS - hr - ra) / RS) + 1);
+    // last steady step: floor division (a negative numerator means no steady step;
+    // C++ division would truncate it to 0)
+    auto fdiv = [](int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); };
+    const int steady_hi = min(n_steps, min(fdiv(rb - RS - ra, RS), fdiv(rows - RS - hr - ra, RS)) + 1);
     const bool steady = SG == 1 && fast_cols && !(L.debug & 1u) && steady_lo < steady_hi;
     constexpr unsigned kCutBytes = kG * kW * sizeof(T);
 
@@ -592,7 +595,16 @@ cudaError_t go(const CfarLaunch& L0, cudaStream_t stream) {
     L.debug = 0;
     if (const char* e = getenv("UWB_RING_DEBUG")) L.debug = static_cast<unsigned>(atoi(e));
     L.col_tiles = (L.cols + kW - 1) / kW;
-    L.row_chunks = (L.geo.slab_rows + kRingRows - 1) / kRingRows;
+    // row chunks of kRingRows; a batch too small to give every SM two CTAs
+    // (single small maps) takes shorter chunks (each re-reads its window's
+    // 2 hr + 1 halo rows, but the chunks' serial steps run in parallel)
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    L.ring_rows = kRingRows;
+    auto ctas = [&](int64_t rr) { return L.col_tiles * ((L.geo.slab_rows + rr - 1) / rr) * L.n_jobs; };
+    while (L.ring_rows > 32 && ctas(L.ring_rows) < 2 * sms && !getenv("UWB_RING_FIXED_ROWS")) L.ring_rows /= 2;
+    L.row_chunks = (L.geo.slab_rows + L.ring_rows - 1) / L.ring_rows;
     const int64_t n_maps = L.n_jobs / L.geo.n_slabs;
     CUtensorMap tmap_tab, tmap_cut;
     const uint64_t tab_rows = static_cast<uint64_t>(L.table_stride / L.table_ld);

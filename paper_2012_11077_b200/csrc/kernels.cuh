@@ -130,6 +130,7 @@ struct CfarLaunch {
     unsigned long long* det_counts;
     unsigned long long* first_bad;
     int64_t row_chunks;  // row chunks per job
+    int64_t ring_rows;   // CFAR ring kernel: output rows per CTA (row chunk height)
     unsigned sleep_ns;   // barrier-wait suspend hint of the CFAR ring kernel (ns)
     unsigned debug;      // bit 0: consumers skip the cell arithmetic (data-movement probe)
     int ring_ahead;      // CFAR ring: table groups of look-ahead beyond the window
