@@ -59,7 +59,13 @@ typedef enum uwb_backend { UWB_NAIVE = 0, UWB_INTEGRAL = 1 } uwb_backend;
 /* Table scope for the integral backend. */
 typedef enum uwb_sat_mode {
     UWB_SAT_GLOBAL = 0, /* one (M+1)x(N+1) table per map: reference-exact */
-    UWB_SAT_SLAB = 1    /* row slabs, each with its own table over slab + halo */
+    UWB_SAT_SLAB = 1,   /* row slabs, each with its own table over slab + halo */
+    UWB_SAT_TILE = 2    /* row slabs (slab_rows, 0 = 1024) x column bands of 1024 owned
+                           columns (UWB_TILE_COLS), each tile with its own table over the
+                           tile + a 32-aligned halo >= g + b on each side: single large
+                           maps run as a batch of short strip chains. Equal to GLOBAL
+                           modulo the tie band; bit-identical to the reference run on
+                           each tile's buffer (cols % 32 != 0: row slabs only) */
 } uwb_sat_mode;
 
 /* CfarParams (cfar.hpp:19-32) generalised to per-axis radii; the reference's

@@ -38,6 +38,7 @@ UWB_NAIVE = 0
 UWB_INTEGRAL = 1
 UWB_SAT_GLOBAL = 0
 UWB_SAT_SLAB = 1
+UWB_SAT_TILE = 2
 
 
 class uwb_cfar_params(C.Structure):

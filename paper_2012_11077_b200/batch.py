@@ -18,7 +18,7 @@ from .api import DETECTION_DTYPE, CfarParams
 from .errors import CapacityError, InputError, raise_for
 
 _DT = {torch.float32: N.UWB_F32, torch.float64: N.UWB_F64}
-_MODES = {"global": N.UWB_SAT_GLOBAL, "slab": N.UWB_SAT_SLAB}
+_MODES = {"global": N.UWB_SAT_GLOBAL, "slab": N.UWB_SAT_SLAB, "tile": N.UWB_SAT_TILE}
 
 
 class BatchCfar:

@@ -150,6 +150,7 @@ std::string degenerate_msg(const uwb_cfar_params& p, uint64_t rows, uint64_t col
 struct Plan {
     JobGeometry geo;
     int64_t n_maps, cols, n_jobs, table_ld, table_stride, strips, max_rows, edge_stride;
+    int64_t sat_jobs, sat_cols; // SAT jobs (map, slab, band) and table source columns per job
     int cpl;
     size_t off_tables, off_edge, off_prog, off_counter, off_scratch, total;
 };
@@ -168,7 +169,9 @@ Plan make_plan(const uwb_map_batch& b, const uwb_cfar_params* p, int sat_mode, u
     P.geo.buf_row0 = static_cast<int64_t>(win ? win->buf_row0 : 0);
     P.geo.buf_rows = static_cast<int64_t>(b.rows);
     const int64_t owned = P.geo.row_hi - P.geo.row_lo;
-    if (win || (sat_mode == UWB_SAT_SLAB && slab_rows > 0 && static_cast<int64_t>(slab_rows) < owned)) {
+    if (sat_mode == UWB_SAT_TILE && !win && slab_rows == 0) slab_rows = 1024;
+    if (win || ((sat_mode == UWB_SAT_SLAB || sat_mode == UWB_SAT_TILE) && slab_rows > 0 &&
+                static_cast<int64_t>(slab_rows) < owned)) {
         P.geo.slab_rows = slab_rows > 0 && static_cast<int64_t>(slab_rows) < owned ? static_cast<int64_t>(slab_rows)
                                                                                   : (owned > 0 ? owned : 1);
         P.geo.halo = p ? p->guard_rows + p->background_rows : 0;
@@ -179,10 +182,32 @@ Plan make_plan(const uwb_map_batch& b, const uwb_cfar_params* p, int sat_mode, u
     P.geo.n_slabs = owned > 0 ? (owned + P.geo.slab_rows - 1) / P.geo.slab_rows : 0;
     P.n_jobs = P.n_maps * P.geo.n_slabs;
     P.max_rows = P.geo.max_table_rows();
-    P.table_ld = table_ld_for(P.cols);
+    // column bands (UWB_SAT_TILE): band tables of band_cols owned columns plus a
+    // 32-aligned halo >= g_c + b_c per side; only when the bands are narrower
+    // than the map and the map width keeps every band start 32-aligned
+    P.geo.map_cols = P.cols;
+    P.geo.n_bands = 1;
+    P.geo.band_cols = P.cols;
+    P.geo.band_width = P.cols;
+    P.sat_cols = P.cols;
+    if (sat_mode == UWB_SAT_TILE && p && P.cols % 32 == 0) {
+        int64_t bc = 1024;
+        if (const char* e = getenv("UWB_TILE_COLS")) bc = atoll(e);
+        bc = round_up(bc < 128 ? 128 : bc, 128);
+        const int64_t hp = round_up(p->guard_cols + p->background_cols, 32);
+        if (bc + 2 * hp < P.cols) {
+            P.geo.n_bands = (P.cols + bc - 1) / bc;
+            P.geo.band_cols = bc;
+            P.geo.band_width = bc + 2 * hp;
+            P.sat_cols = P.geo.band_width;
+        }
+    }
+    P.geo.band_seg = table_ld_for(P.sat_cols);
+    P.table_ld = P.geo.band_seg * P.geo.n_bands;
     P.table_stride = (P.max_rows + 1) * P.table_ld;
-    P.cpl = sat_cpl_for(P.n_jobs, P.cols);
-    P.strips = sat_strips(P.cols, P.cpl);
+    P.sat_jobs = P.n_jobs * P.geo.n_bands;
+    P.cpl = sat_cpl_for(P.sat_jobs, P.sat_cols);
+    P.strips = sat_strips(P.sat_cols, P.cpl);
     size_t off = 0;
     auto take = [&](size_t bytes) {
         const size_t o = off;
@@ -192,8 +217,8 @@ Plan make_plan(const uwb_map_batch& b, const uwb_cfar_params* p, int sat_mode, u
     P.off_tables = take(sizeof(double) * static_cast<size_t>(P.n_jobs) * P.table_stride);
     P.edge_stride = round_up(P.max_rows, 32);
     // S(r, strip's last column) handed from each strip to the next, contiguous per strip
-    P.off_edge = take(P.strips > 1 ? sizeof(double) * static_cast<size_t>(P.n_jobs) * P.strips * P.edge_stride : 0);
-    P.off_prog = take(sizeof(unsigned) * P.n_jobs * P.strips);
+    P.off_edge = take(P.strips > 1 ? sizeof(double) * static_cast<size_t>(P.sat_jobs) * P.strips * P.edge_stride : 0);
+    P.off_prog = take(sizeof(unsigned) * P.sat_jobs * P.strips);
     P.off_counter = take(sizeof(unsigned) * 4);
     P.off_scratch = take(det_cap > 2048 ? sizeof(uwb_detection) * P.n_maps * det_cap : 0);
     P.total = off;
@@ -205,9 +230,9 @@ SatLaunch sat_launch(const Plan& P, const uwb_map_batch& b, char* ws, unsigned l
     L.maps = b.maps;
     L.ld = static_cast<int64_t>(b.ld);
     L.map_stride = static_cast<int64_t>(b.map_stride);
-    L.cols = P.cols;
+    L.cols = P.sat_cols;
     L.geo = P.geo;
-    L.n_jobs = P.n_jobs;
+    L.n_jobs = P.sat_jobs;
     L.table = reinterpret_cast<double*>(ws + P.off_tables);
     L.table_ld = P.table_ld;
     L.table_stride = P.table_stride;
@@ -226,7 +251,7 @@ SatLaunch sat_launch(const Plan& P, const uwb_map_batch& b, char* ws, unsigned l
 }
 
 cudaError_t run_sat(const Plan& P, const SatLaunch& L, int dtype, cudaStream_t s) {
-    cudaError_t e = cudaMemsetAsync(L.gprog, 0, sizeof(unsigned) * P.n_jobs * P.strips, s);
+    cudaError_t e = cudaMemsetAsync(L.gprog, 0, sizeof(unsigned) * P.sat_jobs * P.strips, s);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(L.tile_counter, 0, sizeof(unsigned), s);
     if (e != cudaSuccess) return e;
@@ -310,7 +335,7 @@ uwb_status dev_cfar(const uwb_map_batch& b, const uwb_cfar_params& p, const doub
             // is left in the workspace; falls through to the two kernels when
             // the geometry does not qualify)
             const SatLaunch SL = sat_launch(P, b, ws, reinterpret_cast<unsigned long long*>(o.first_bad));
-            UWB_CUDA_TRY(cudaMemsetAsync(SL.gprog, 0, sizeof(unsigned) * P.n_jobs * P.strips, s));
+            UWB_CUDA_TRY(cudaMemsetAsync(SL.gprog, 0, sizeof(unsigned) * P.sat_jobs * P.strips, s));
             UWB_CUDA_TRY(cudaMemsetAsync(SL.tile_counter, 0, sizeof(unsigned), s));
             if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[1], s));
             const cudaError_t e = launch_cfar_fused(SL, cfar_launch(P, b, p, alpha, ws, o), b.dtype, s);

@@ -679,7 +679,7 @@ cudaError_t launch_cfar_fused(const SatLaunch& S, const CfarLaunch& C, int dtype
     if (const char* e = getenv("UWB_FUSED"))
         if (atoi(e) == 0) return cudaErrorNotSupported;
     const JobGeometry& g = C.geo;
-    if (g.n_slabs != 1 || g.row_lo != 0 || g.row_hi != g.rows || g.buf_row0 != 0 || g.buf_rows != g.rows)
+    if (g.n_slabs != 1 || g.n_bands != 1 || g.row_lo != 0 || g.row_hi != g.rows || g.buf_row0 != 0 || g.buf_rows != g.rows)
         return cudaErrorNotSupported;
     if (g.rows < 1 || g.rows >= (int64_t(1) << 30) || C.cols < 1 || C.cols >= (int64_t(1) << 30))
         return cudaErrorNotSupported;

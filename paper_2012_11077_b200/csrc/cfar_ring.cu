@@ -156,6 +156,10 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
 
     // table storage columns of the ring rows: [e_lo, e_lo + BOXC), 16-byte aligned
     const int e_lo = (kTabShift + max(0, c0 - hc)) & ~1;
+    // TMA column of e_lo: shifted into this tile's band table (UWB_SAT_TILE; 0
+    // otherwise). Bands own whole 128-column tiles and the shift is even, so
+    // the consumers' offsets from e_lo are unchanged.
+    const int e_tx = e_lo + static_cast<int>(L.geo.band_dx_for_col(c0));
     // padded table rows needed by output rows [ra, rb), in groups of kG from i_lo
     const int i_lo = max(0, ra - hr);
     const int i_hi = min(rows, rb + hr);
@@ -181,7 +185,7 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
         if (lane != 0) return;
         const int last_grp = (i_hi - i_lo) / kG;
         for (int g = 0; g <= min(last_grp, kPfGroups - 1); ++g)
-            tma_prefetch3(&tmap_tab, e_lo, i_lo + g * kG - trow0, static_cast<int>(job));
+            tma_prefetch3(&tmap_tab, e_tx, i_lo + g * kG - trow0, static_cast<int>(job));
         const int buf0 = static_cast<int>(L.geo.buf_row0);
         for (int g = 0; g < min(n_cg, kPfGroups); ++g)
             tma_prefetch3(&tmap_cut, c0, ra + g * kG - buf0, static_cast<int>(map));
@@ -199,13 +203,13 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
                 // the first SG groups are mirrored after the last slot, so RS
                 // consecutive ring rows are always contiguous in memory
                 mbar_expect_tx(&full_t[gslot], gslot < SG ? 2 * kTabBox : kTabBox);
-                tma_box3(slots + static_cast<size_t>(gslot * kG) * BOXC, &tmap_tab, e_lo, first - trow0,
+                tma_box3(slots + static_cast<size_t>(gslot * kG) * BOXC, &tmap_tab, e_tx, first - trow0,
                          static_cast<int>(job), &full_t[gslot]);
                 if (gslot < SG)
-                    tma_box3(slots + static_cast<size_t>(G.nr + gslot * kG) * BOXC, &tmap_tab, e_lo, first - trow0,
+                    tma_box3(slots + static_cast<size_t>(G.nr + gslot * kG) * BOXC, &tmap_tab, e_tx, first - trow0,
                              static_cast<int>(job), &full_t[gslot]);
                 if (grp + kPfGroups <= last_grp)
-                    tma_prefetch3(&tmap_tab, e_lo, first + kPfGroups * kG - trow0, static_cast<int>(job));
+                    tma_prefetch3(&tmap_tab, e_tx, first + kPfGroups * kG - trow0, static_cast<int>(job));
                 if (++gslot == G.ng) { gslot = 0; gphase ^= 1; }
                 ++grp;
             } else {

@@ -40,6 +40,17 @@ struct JobGeometry {
     int64_t row_hi;     // end of the owned rows
     int64_t buf_row0;   // global row of the input buffer's row 0
     int64_t buf_rows;   // rows present in the input buffer
+    // Column bands (UWB_SAT_TILE): band k owns columns [k*band_cols, (k+1)*band_cols)
+    // and its table covers band_width source columns from band_c0(k) (the owned
+    // columns plus a 32-aligned halo >= g_c + b_c on each side, moved inward at
+    // the map edges, so every band table has the same width). Band k's table is
+    // the column segment [k*band_seg, (k+1)*band_seg) of the job's table rows.
+    // n_bands == 1: no bands (band_width = map_cols, band_seg = table ld).
+    int64_t map_cols;   // global map columns (clamp bounds)
+    int64_t n_bands;
+    int64_t band_cols;
+    int64_t band_width;
+    int64_t band_seg;
 
     __host__ __device__ int64_t owned_begin(int64_t s) const { return row_lo + s * slab_rows; }
     __host__ __device__ int64_t owned_end(int64_t s) const {
@@ -55,6 +66,19 @@ struct JobGeometry {
         const int64_t e = owned_end(s) + halo;
         return e < rows ? e : rows;
     }
+    __host__ __device__ int64_t band_c0(int64_t k) const {
+        if (n_bands <= 1) return 0;
+        int64_t c = k * band_cols - (band_width - band_cols) / 2;
+        c = c > 0 ? c : 0;
+        return c < map_cols - band_width ? c : map_cols - band_width;
+    }
+    // table storage column of map column c minus (kTabShift + 1 + c): the band
+    // segment's offset minus its first source column
+    __host__ __device__ int64_t band_dx_for_col(int64_t c) const {
+        if (n_bands <= 1) return 0;
+        const int64_t k = c / band_cols;
+        return k * band_seg - band_c0(k);
+    }
     // rows of the largest table (source rows, excluding the zero row)
     __host__ __device__ int64_t max_table_rows() const {
         const int64_t r = slab_rows + 2 * halo;
@@ -68,7 +92,7 @@ struct SatLaunch {
     int64_t map_stride;  // elements between maps
     int64_t cols;
     JobGeometry geo;
-    int64_t n_jobs;      // n_maps * n_slabs
+    int64_t n_jobs;      // n_maps * n_slabs * n_bands
     double* table;       // padded tables, shifted layout
     int64_t table_ld;
     int64_t table_stride; // doubles between job tables
@@ -90,19 +114,25 @@ struct SatJobView {
     const void* src;
     int64_t rows;
     int64_t row0;        // map row of table source row 0
+    int64_t col0;        // map column of table source column 0 (column bands)
     double* table;
     unsigned long long* nonfinite;
 };
 
 __host__ __device__ inline SatJobView sat_job(const SatLaunch& L, int64_t job) {
-    const int64_t m = job / L.geo.n_slabs;
-    const int64_t s = job % L.geo.n_slabs;
+    // SAT jobs are (map, slab, band); the CFAR's jobs are (map, slab)
+    const int64_t k = job % L.geo.n_bands;
+    const int64_t ms = job / L.geo.n_bands;
+    const int64_t m = ms / L.geo.n_slabs;
+    const int64_t s = ms % L.geo.n_slabs;
     const int64_t b = L.geo.table_begin(s);
+    const int64_t c0 = L.geo.band_c0(k);
     SatJobView v;
-    v.src = static_cast<const char*>(L.maps) + (m * L.map_stride + (b - L.geo.buf_row0) * L.ld) * L.elem_bytes;
+    v.src = static_cast<const char*>(L.maps) + (m * L.map_stride + (b - L.geo.buf_row0) * L.ld + c0) * L.elem_bytes;
     v.rows = L.geo.table_end(s) - b;
     v.row0 = b;
-    v.table = L.table + job * L.table_stride;
+    v.col0 = c0;
+    v.table = L.table + ms * L.table_stride + k * L.geo.band_seg;
     v.nonfinite = L.first_bad ? L.first_bad + 2 * m : nullptr;
     return v;
 }

@@ -444,7 +444,7 @@ sat_systolic_kernel(SatLaunch L) {
                 int col = c;
                 const int bad = first_nonfinite<T>(src, ld, c, nvalid, min(rows, s0 + kWarp), &col);
                 if (bad != INT_MAX)
-                    report_min(J.nonfinite, static_cast<unsigned long long>((J.row0 + bad) * L.cols + col));
+                    report_min(J.nonfinite, static_cast<unsigned long long>((J.row0 + bad) * L.geo.map_cols + J.col0 + col));
             }
             if (late_fetch) e_cur = fetch_left(s0 + kWarp);
             // hand over the edge rows stored so far (warp-uniform); a fast block

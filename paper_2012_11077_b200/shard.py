@@ -56,3 +56,43 @@ def reduce_count(count, group=None):
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(count, op=dist.ReduceOp.SUM, group=group)
     return count
+
+
+@dataclass(frozen=True)
+class Tile:
+    """One table of UWB_SAT_TILE: owned rows/cols and the buffer its table covers."""
+    owned_rows: tuple[int, int]
+    owned_cols: tuple[int, int]
+    buf_rows: tuple[int, int]
+    buf_cols: tuple[int, int]
+
+
+def tiles(rows: int, cols: int, guard_rows: int, guard_cols: int, background_rows: int,
+          background_cols: int, slab_rows: int = 0, band_cols: int = 1024) -> list[Tile]:
+    """Host mirror of the UWB_SAT_TILE decomposition (csrc/capi.cu make_plan,
+    csrc/kernels.cuh JobGeometry::band_c0): row slabs of ``slab_rows`` (0 = 1024)
+    owned rows with a g_r + b_r halo, column bands of ``band_cols`` (rounded up
+    to 128) owned columns whose tables span band_cols + 2 hp source columns,
+    hp = g_c + b_c rounded up to 32, moved inward at the map edges. Every owned
+    cell's clamped window lies inside its tile's buffer and the buffer's edges
+    are map edges wherever the window clamps, so the CFAR of a tile equals the
+    reference's cfar2d_integral run on the buffer alone (the parity oracle)."""
+    slab = slab_rows or 1024
+    if slab >= rows:
+        slab = rows
+    hr = guard_rows + background_rows
+    bc = -(-max(band_cols, 128) // 128) * 128
+    hp = -(-(guard_cols + background_cols) // 32) * 32
+    banded = cols % 32 == 0 and bc + 2 * hp < cols
+    out = []
+    for r0 in range(0, rows, slab):
+        r1 = min(rows, r0 + slab)
+        br = (max(0, r0 - hr), min(rows, r1 + hr)) if slab < rows else (0, rows)
+        if not banded:
+            out.append(Tile((r0, r1), (0, cols), br, (0, cols)))
+            continue
+        width = bc + 2 * hp
+        for k in range(-(-cols // bc)):
+            c0 = min(max(k * bc - hp, 0), cols - width)
+            out.append(Tile((r0, r1), (k * bc, min(cols, (k + 1) * bc)), br, (c0, c0 + width)))
+    return out
