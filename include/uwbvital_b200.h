@@ -225,12 +225,15 @@ uwb_status uwb_dev_cfar2d(const uwb_map_batch* batch, const uwb_cfar_params* par
  * plus g_r + b_r halo rows on each side (clipped to the map). Tables are
  * slab-local (UWB_SAT_SLAB semantics, slab_rows 0 = one slab for the window),
  * windows clamp with the global row count, detections carry global rows, and
- * mask rows / per-cell outputs are indexed by row - row_begin. */
+ * mask rows / per-cell outputs are indexed by row - row_begin.
+ * col_bands > 0 also cuts the columns into bands of col_bands owned columns
+ * (rounded up to 128) with their own tables (UWB_SAT_TILE semantics); 0 = none. */
 typedef struct uwb_row_window {
     uint64_t global_rows;
     uint64_t buf_row0;
     uint64_t row_begin;
     uint64_t row_end;
+    uint64_t col_bands;
 } uwb_row_window;
 
 uint64_t uwb_dev_cfar2d_window_workspace(const uwb_map_batch* batch, const uwb_row_window* win,

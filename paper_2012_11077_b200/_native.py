@@ -67,7 +67,7 @@ class uwb_map_batch(C.Structure):
 
 class uwb_row_window(C.Structure):
     _fields_ = [("global_rows", C.c_uint64), ("buf_row0", C.c_uint64), ("row_begin", C.c_uint64),
-                ("row_end", C.c_uint64)]
+                ("row_end", C.c_uint64), ("col_bands", C.c_uint64)]
 
 
 class uwb_rfrm_info(C.Structure):

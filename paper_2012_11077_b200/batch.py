@@ -27,10 +27,12 @@ class BatchCfar:
                  det_capacity: int = 1024, device=None, want_mask_u8: bool = False,
                  want_thresholds: bool = False, window: tuple[int, int, int, int] | None = None,
                  workspace: torch.Tensor | None = None):
-        """``window = (global_rows, buf_row0, row_begin, row_end)``: the maps passed
-        to each call hold rows [buf_row0, buf_row0 + rows) of maps with
+        """``window = (global_rows, buf_row0, row_begin, row_end[, col_bands])``: the
+        maps passed to each call hold rows [buf_row0, buf_row0 + rows) of maps with
         ``global_rows`` rows and the call owns rows [row_begin, row_end) (one
-        rank's row slab); outputs then cover the owned rows only."""
+        rank's row slab); outputs then cover the owned rows only.
+        ``col_bands`` > 0 also gives every band of that many columns its own
+        table (``sat_mode="tile"`` semantics)."""
         if dtype not in _DT:
             raise ValueError("maps must be float32 or float64")
         params.validate()
@@ -42,7 +44,7 @@ class BatchCfar:
         self.slab_rows = int(slab_rows)
         self.det_capacity = int(det_capacity)
         self.words_per_row = (self.cols + 31) // 32
-        self.window = None if window is None else N.uwb_row_window(*(int(x) for x in window))
+        self.window = None if window is None else N.uwb_row_window(*(int(x) for x in tuple(window) + (0,) * (5 - len(window))))
         out_rows = self.rows if window is None else int(window[3]) - int(window[2])
         self.out_rows = out_rows
         dev = self.device

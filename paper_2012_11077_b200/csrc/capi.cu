@@ -190,9 +190,9 @@ Plan make_plan(const uwb_map_batch& b, const uwb_cfar_params* p, int sat_mode, u
     P.geo.band_cols = P.cols;
     P.geo.band_width = P.cols;
     P.sat_cols = P.cols;
-    if (sat_mode == UWB_SAT_TILE && p && P.cols % 32 == 0) {
-        int64_t bc = 1024;
-        if (const char* e = getenv("UWB_TILE_COLS")) bc = atoll(e);
+    if (((sat_mode == UWB_SAT_TILE && !win) || (win && win->col_bands)) && p && P.cols % 32 == 0) {
+        int64_t bc = win ? static_cast<int64_t>(win->col_bands) : 1024;
+        if (const char* e = getenv("UWB_TILE_COLS"); e && !win) bc = atoll(e);
         bc = round_up(bc < 128 ? 128 : bc, 128);
         const int64_t hp = round_up(p->guard_cols + p->background_cols, 32);
         if (bc + 2 * hp < P.cols) {

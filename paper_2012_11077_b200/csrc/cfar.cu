@@ -253,6 +253,52 @@ sort_detections_kernel(uwb_detection* dets, int64_t cap, const unsigned long lon
         for (int64_t i = threadIdx.x; i < count; i += blockDim.x) src[i] = in[i];
 }
 
+// Phase 2 for few long lists: one merge pass over every list, CTA (x, map)
+// producing output entries [x * kMergeTile, +kMergeTile) of the map's merged
+// pairs of width-`width` runs (kMergeTile divides 2 * width). The CTA finds its
+// input ranges by two merge-path searches, stages them in shared memory and
+// merges kItems per thread there. width >= count is a plain copy.
+constexpr int kMergeTile = 2048;
+constexpr int kMergeThreads = 256;
+__global__ void __launch_bounds__(kMergeThreads)
+merge_pass_kernel(const uwb_detection* in_all, uwb_detection* out_all, int64_t cap,
+                  const unsigned long long* counts, int64_t width) {
+    extern __shared__ uwb_detection smem_det[];
+    __shared__ int split[2];
+    const int64_t map = blockIdx.y;
+    const int64_t count = imin(static_cast<int64_t>(counts[map]), cap);
+    const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kMergeTile;
+    if (count <= kSortRun || t0 >= count) return; // short lists stay sorted in place
+    const uwb_detection* in = in_all + map * cap;
+    uwb_detection* out = out_all + map * cap;
+    const int64_t base = (t0 / (2 * width)) * (2 * width);
+    const int64_t a0 = base, a1 = imin(base + width, count);
+    const int64_t b0 = a1, b1 = imin(base + 2 * width, count);
+    const int na = static_cast<int>(a1 - a0), nb = static_cast<int>(b1 - b0);
+    const int d0 = static_cast<int>(t0 - base);
+    const int d1 = min(d0 + kMergeTile, na + nb);
+    if (threadIdx.x == 0) split[0] = merge_path(in + a0, na, in + b0, nb, d0);
+    if (threadIdx.x == 32) split[1] = merge_path(in + a0, na, in + b0, nb, d1);
+    __syncthreads();
+    const int i0 = split[0], j0 = d0 - split[0];
+    const int la = split[1] - i0, lb = (d1 - split[1]) - j0;
+    for (int k = threadIdx.x; k < la + lb; k += blockDim.x)
+        smem_det[k] = k < la ? in[a0 + i0 + k] : in[b0 + j0 + (k - la)];
+    __syncthreads();
+    constexpr int kItems = kMergeTile / kMergeThreads;
+    const int k0 = static_cast<int>(threadIdx.x) * kItems;
+    if (k0 >= la + lb) return;
+    const uwb_detection* sa = smem_det;
+    const uwb_detection* sb = smem_det + la;
+    int i = merge_path(sa, la, sb, lb, k0);
+    int j = k0 - i;
+    const int kend = min(k0 + kItems, la + lb);
+    for (int k = k0; k < kend; ++k) {
+        const bool take_a = i < la && (j >= lb || !before(sb[j], sa[i]));
+        out[t0 + k] = take_a ? sa[i++] : sb[j++];
+    }
+}
+
 CfarLaunch grid_shape(const CfarLaunch& L0, dim3& grid) {
     CfarLaunch L = L0;
     L.col_tiles = (L.cols + kCfarThreads - 1) / kCfarThreads;
@@ -302,6 +348,30 @@ cudaError_t launch_sort_detections(uwb_detection* dets, int64_t cap, const unsig
                            stream>>>(dets, cap, counts);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         if (!scratch) return cudaSuccess;
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (n_maps < sms && !getenv("UWB_SORT_ONE_CTA")) {
+            // few long lists (single large maps): every merge pass spreads each
+            // list over many CTAs; an even number of passes ends in `dets`
+            const int64_t tiles = (cap + kMergeTile - 1) / kMergeTile;
+            if (tiles > 65535) return cudaErrorNotSupported;
+            const size_t msmem = sizeof(uwb_detection) * kMergeTile;
+            e = cudaFuncSetAttribute(merge_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(msmem));
+            if (e != cudaSuccess) return e;
+            int passes = 0;
+            for (int64_t w = kSortRun; w < cap; w *= 2) ++passes;
+            passes += passes & 1;
+            int64_t w = kSortRun;
+            for (int q = 0; q < passes; ++q, w *= 2) {
+                ++g_kernel_launches;
+                merge_pass_kernel<<<dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(n_maps)), kMergeThreads,
+                                    msmem, stream>>>(q % 2 ? scratch : dets, q % 2 ? dets : scratch, cap, counts, w);
+                if ((e = cudaGetLastError()) != cudaSuccess) return e;
+            }
+            return cudaSuccess;
+        }
         ++g_kernel_launches;
         sort_detections_kernel<<<static_cast<unsigned>(n_maps), kSortThreads, smem, stream>>>(dets, cap, counts, scratch,
                                                                                             true);

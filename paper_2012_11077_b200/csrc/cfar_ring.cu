@@ -605,8 +605,12 @@ cudaError_t go(const CfarLaunch& L0, cudaStream_t stream) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    L.ring_rows = kRingRows;
+    // tall windows (config 4: 2 hr + 1 = 73) take 512-row chunks: each chunk
+    // re-reads its 2 hr + 1 halo rows and fills its ring before the first step
+    // (cfg 4: 1.62 -> 1.48 ms)
+    L.ring_rows = 2 * L.hr + 1 > 48 ? 2 * kRingRows : kRingRows;
     auto ctas = [&](int64_t rr) { return L.col_tiles * ((L.geo.slab_rows + rr - 1) / rr) * L.n_jobs; };
+    if (const char* e = getenv("UWB_RING_ROWS")) L.ring_rows = atoi(e) > 0 ? atoi(e) : kRingRows;
     while (L.ring_rows > 32 && ctas(L.ring_rows) < 2 * sms && !getenv("UWB_RING_FIXED_ROWS")) L.ring_rows /= 2;
     L.row_chunks = (L.geo.slab_rows + L.ring_rows - 1) / L.ring_rows;
     const int64_t n_maps = L.n_jobs / L.geo.n_slabs;

@@ -122,3 +122,36 @@ def test_tiles_report_first_bad_cell_in_map_coordinates(uwb, cuda):
     with pytest.raises(InputError) as e:
         b.check_inputs()
     assert "(300, 2050)" in str(e.value)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_window_col_bands_ranks_vs_reference_per_tile(uwb, ref, cuda, world):
+    """Config-4 sharding with column bands (bench.py --config 4 at any N): each
+    rank holds its row slab + halo and runs uwb_dev_cfar2d_window with col_bands;
+    every tile equals the reference run on the tile's buffer."""
+    from paper_2012_11077_b200 import synth
+    from paper_2012_11077_b200.batch import BatchCfar
+    from paper_2012_11077_b200.shard import row_slab, tiles
+    rows, cols, halo = 1800, 3072, 36
+    m = synth.cfg4_map(seed=21, device=cuda, rows=rows, cols=cols)
+    host = m.double().cpu().numpy()
+    p = uwb.CfarParams(4, 32, 1e-5)
+    per = -(-rows // world)
+    mask, thr, dets = _expected(host, tiles(rows, cols, 4, 4, 32, 32, per, 1024),
+                                lambda s: ref.cfar2d(s, 4, 32, 1e-5, "integral"))
+    got = []
+    for rank in range(world):
+        s = row_slab(rows, world, rank, halo)
+        local = m[s.load_begin:s.load_end].contiguous().unsqueeze(0)
+        b = BatchCfar(1, s.load_end - s.load_begin, cols, p, torch.float32, det_capacity=1 << 15,
+                      want_mask_u8=True, want_thresholds=True,
+                      window=(rows, s.load_begin, s.owned_begin, s.owned_end, 1024))
+        b(local)
+        torch.cuda.synchronize()
+        o0, o1 = s.owned_begin, s.owned_end
+        assert_bitwise(b.thresholds[0].cpu().numpy(), thr[o0:o1], f"rank {rank} thresholds")
+        assert np.array_equal(b.mask(0), mask[o0:o1]), f"rank {rank} mask"
+        got.append(b.detections(0))
+    d = np.concatenate(got)
+    d = d[np.lexsort((d["col"], d["row"], -d["value"]))]
+    assert d.tobytes() == dets.tobytes()
