@@ -42,7 +42,13 @@ namespace {
 constexpr int kRingRows = 256;  // output rows per CTA
 constexpr int kG = 4;           // rows per group (output step, TMA box height)
 constexpr int kW = 128;         // output columns per CTA
-constexpr int kCutGroups = 4;   // CUT ring depth (groups)
+constexpr int kCutGroups = 4;   // CUT ring depth (groups) at 3-4 CTAs per SM
+// CUT ring depth at `occ` CTAs per SM: each step consumes one CUT group, so a
+// CTA runs at most (depth / TMA latency) steps per second; one or two CTAs per
+// SM need the deeper ring (measured: consumers starved on full_c at depth 4)
+__host__ __device__ constexpr int cut_groups_for(int occ, int esz) {
+    return occ == 1 ? (esz == 4 ? 16 : 8) : kCutGroups;
+}
 constexpr int kMaxAhead = 8;    // most table groups of look-ahead beyond the window
 constexpr int kPfGroups = 6;    // L2 prefetch distance of both streams (groups)
 
@@ -62,10 +68,10 @@ __host__ __device__ inline RingGeom ring_geom(int hr, int sg, int ahead) {
 }
 
 template <typename T>
-inline size_t ring_smem_bytes(int hr, int boxc, int sg, int ahead) {
+inline size_t ring_smem_bytes(int hr, int boxc, int sg, int ahead, int ncut) {
     const RingGeom g = ring_geom(hr, sg, ahead);
     return 128 /* alignment slack */ + sizeof(double) * static_cast<size_t>(g.nr + kG * sg) * boxc +
-           sizeof(T) * static_cast<size_t>(kCutGroups) * kG * kW + 2 * sizeof(uint64_t) * (g.ng + kCutGroups);
+           sizeof(T) * static_cast<size_t>(ncut) * kG * kW + 2 * sizeof(uint64_t) * (g.ng + ncut);
 }
 
 // Blocking wait that suspends the thread in the barrier unit (up to hint_ns per
@@ -119,12 +125,17 @@ __device__ __forceinline__ void tma_box3(void* dst, const CUtensorMap* map, int 
 
 // NCW consumer warps x CPT columns per thread = kW columns; BOXC = ring row
 // width in doubles (the table box width, >= kW + 2 hc + 4, multiple of 4).
-template <typename T, int NCW, int CPT, int BOXC, int SG, int OCC>
-__global__ void __launch_bounds__((NCW + 1) * kWarp, OCC)
+// NGRP consumer warp groups take alternate steps (NGRP = 2 at one CTA per SM:
+// twice the consumer warps on the same ring); every consumer warp hands back
+// every table group, each group's CUT groups come back from its NCW warps.
+template <typename T, int NCW, int CPT, int BOXC, int SG, int OCC, int NGRP>
+__global__ void __launch_bounds__((NCW * NGRP + 1) * kWarp, OCC)
 cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUtensorMap tmap_tab,
                const __grid_constant__ CUtensorMap tmap_cut) {
     static_assert(NCW * CPT * kWarp == kW, "tile width");
-    static_assert(kCutGroups % SG == 0, "CUT ring depth");
+    constexpr int kCutG = cut_groups_for(OCC, sizeof(T));
+    static_assert(kCutG % SG == 0, "CUT ring depth");
+    static_assert(NGRP == 1 || (SG == 1 && kCutG % NGRP == 0), "interleaved steps");
     constexpr int RS = kG * SG; // output rows per consumer step
     constexpr unsigned kRowBytes = 8u * BOXC;
     constexpr unsigned kTabBox = kG * kRowBytes;
@@ -136,9 +147,9 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
     double* slots = reinterpret_cast<double*>(ring_smem);
     const char* ring = reinterpret_cast<const char*>(ring_smem);
     T* cuts = reinterpret_cast<T*>(slots + static_cast<size_t>(G.nr + RS) * BOXC);
-    uint64_t* full_t = reinterpret_cast<uint64_t*>(cuts + static_cast<size_t>(kCutGroups) * kG * kW);
+    uint64_t* full_t = reinterpret_cast<uint64_t*>(cuts + static_cast<size_t>(kCutG) * kG * kW);
     uint64_t* full_c = full_t + G.ng;
-    uint64_t* empty_t = full_c + kCutGroups;
+    uint64_t* empty_t = full_c + kCutG;
     uint64_t* empty_c = empty_t + G.ng;
 
     const int64_t job = blockIdx.y;
@@ -169,9 +180,9 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
     // ring byte offset of padded table row i (i_lo <= i <= i_hi)
     auto ring_off = [&](int i) { return static_cast<unsigned>((i - i_lo) % G.nr) * kRowBytes; };
     if (threadIdx.x == 0) {
-        for (int s = 0; s < G.ng + kCutGroups; ++s) {
+        for (int s = 0; s < G.ng + kCutG; ++s) {
             mbar_init(&full_t[s], 1);
-            mbar_init(&empty_t[s], NCW);
+            mbar_init(&empty_t[s], s < G.ng ? NCW * NGRP : NCW);
         }
         mbar_fence_init();
     }
@@ -180,14 +191,15 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
     const int warp = threadIdx.x / kWarp;
     const int lane = threadIdx.x % kWarp;
 
-    if (warp == NCW) {
+    if (warp == NCW * NGRP) {
         // =========================== producer thread ===========================
         if (lane != 0) return;
         const int last_grp = (i_hi - i_lo) / kG;
-        for (int g = 0; g <= min(last_grp, kPfGroups - 1); ++g)
+        const int pf = L.pf_groups;
+        for (int g = 0; g <= min(last_grp, pf - 1); ++g)
             tma_prefetch3(&tmap_tab, e_tx, i_lo + g * kG - trow0, static_cast<int>(job));
         const int buf0 = static_cast<int>(L.geo.buf_row0);
-        for (int g = 0; g < min(n_cg, kPfGroups); ++g)
+        for (int g = 0; g < min(n_cg, pf); ++g)
             tma_prefetch3(&tmap_cut, c0, ra + g * kG - buf0, static_cast<int>(map));
         int grp = 0, gslot = 0, gphase = 0;   // next table group, its slot and empty-phase
         int cstep = 0, cslot = 0, cphase = 0; // next CUT group
@@ -208,19 +220,19 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
                 if (gslot < SG)
                     tma_box3(slots + static_cast<size_t>(G.nr + gslot * kG) * BOXC, &tmap_tab, e_tx, first - trow0,
                              static_cast<int>(job), &full_t[gslot]);
-                if (grp + kPfGroups <= last_grp)
-                    tma_prefetch3(&tmap_tab, e_tx, first + kPfGroups * kG - trow0, static_cast<int>(job));
+                if (grp + pf <= last_grp)
+                    tma_prefetch3(&tmap_tab, e_tx, first + pf * kG - trow0, static_cast<int>(job));
                 if (++gslot == G.ng) { gslot = 0; gphase ^= 1; }
                 ++grp;
             } else {
-                if (cstep >= kCutGroups) mbar_wait_susp(&empty_c[cslot], static_cast<unsigned>(cphase ^ 1), L.sleep_ns);
+                if (cstep >= kCutG) mbar_wait_susp(&empty_c[cslot], static_cast<unsigned>(cphase ^ 1), L.sleep_ns);
                 const int first = ra + cstep * kG;
                 mbar_expect_tx(&full_c[cslot], kCutBox);
                 tma_box3(cuts + static_cast<size_t>(cslot) * kG * kW, &tmap_cut, c0, first - buf0,
                          static_cast<int>(map), &full_c[cslot]);
-                if (cstep + kPfGroups < n_cg)
-                    tma_prefetch3(&tmap_cut, c0, first + kPfGroups * kG - buf0, static_cast<int>(map));
-                if (++cslot == kCutGroups) { cslot = 0; cphase ^= 1; }
+                if (cstep + pf < n_cg)
+                    tma_prefetch3(&tmap_cut, c0, first + pf * kG - buf0, static_cast<int>(map));
+                if (++cslot == kCutG) { cslot = 0; cphase ^= 1; }
                 ++cstep;
             }
         }
@@ -228,8 +240,10 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
     }
 
     // ============================ consumer warps ============================
-    const int wc0 = c0 + warp * kWarp * CPT; // first column of my warp
-    const int tc = warp * kWarp * CPT + lane; // my first column within the tile
+    const int grp_id = warp / NCW;            // my steps: grp_id, grp_id + NGRP, ...
+    const int cw = warp % NCW;
+    const int wc0 = c0 + cw * kWarp * CPT; // first column of my warp
+    const int tc = cw * kWarp * CPT + lane; // my first column within the tile
     ColConst K[CPT];
     bool okc[CPT];
 #pragma unroll
@@ -254,15 +268,17 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
 
     // ring slots of the (unclamped) tap rows of output row r0, advanced 4 rows per step
     auto slot0 = [&](int i) { return ((i - i_lo) % G.nr + G.nr) % G.nr; };
-    int sA = slot0(ra - hr), sB = slot0(ra + hr + 1), sC = slot0(ra - gr), sD = slot0(ra + gr + 1);
+    const int rg = ra + grp_id * RS;
+    int sA = slot0(rg - hr), sB = slot0(rg + hr + 1), sC = slot0(rg - gr), sD = slot0(rg + gr + 1);
     constexpr unsigned kHint = 20000; // ns a waiting consumer may sleep in the barrier unit
+    const bool spin = (L.debug & 2u) != 0; // probe: spin in try_wait without a suspend hint
     const unsigned full_t_u = smem_u32(full_t), full_c_u = smem_u32(full_c);
     const unsigned empty_t_u = smem_u32(empty_t), empty_c_u = smem_u32(empty_c);
     // table groups needed through step s: min(last, need_base + s) in the interior
     const int last_grp_c = (i_hi - i_lo) / kG;
     int waited = -1, wslot = 0, wphase = 0; // full_t groups known resident
     int released = -1, rslot = 0;            // table groups handed back
-    int cslot = 0, cphase = 0;
+    int cslot = grp_id * SG, cphase = 0;
     // per-column alpha cache for the general path
     int ncache[CPT];
     double kcache[CPT];
@@ -284,8 +300,10 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
     const bool steady = SG == 1 && fast_cols && !(L.debug & 1u) && steady_lo < steady_hi;
     constexpr unsigned kCutBytes = kG * kW * sizeof(T);
 
-    for (int step = 0; step < n_steps; ++step) {
-        if (steady && step == steady_lo) {
+    // my first step in the steady run
+    const int my_steady_lo = steady_lo + ((grp_id - steady_lo) % NGRP + NGRP) % NGRP;
+    for (int step = grp_id; step < n_steps; step += NGRP) {
+        if (steady && step == my_steady_lo && step < steady_hi) {
             int need = min(last_grp_c, (ra + step * RS + RS + hr - i_lo) / kG);
             int done = (ra + step * RS + RS - hr - i_lo) / kG - 1;
             while (waited < need - 1) { // catch up; then one group per step
@@ -327,15 +345,20 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
                     if (++rslot == G.ng) rslot = 0;
                 }
             }
-            for (; step < steady_hi; ++step) {
+            for (; step < steady_hi; step += NGRP) {
                 const int r0 = ra + step * RS;
-                if (waited < need) {
-                    mbar_wait_u<kHint>(ft_u + 8u * wslot, static_cast<unsigned>(wphase));
-                    ++waited;
-                    if (++wslot == G.ng) { wslot = 0; wphase ^= 1; }
+#pragma unroll
+                for (int q = 0; q < NGRP; ++q) { // one more table group per step
+                    if (waited < need) {
+                        if (spin) mbar_wait_u<0>(ft_u + 8u * wslot, static_cast<unsigned>(wphase));
+                        else mbar_wait_u<kHint>(ft_u + 8u * wslot, static_cast<unsigned>(wphase));
+                        ++waited;
+                        if (++wslot == G.ng) { wslot = 0; wphase ^= 1; }
+                    }
                 }
-                need = min(last_grp_c, need + 1);
-                mbar_wait_u<kHint>(fc_u + 8u * cslot, static_cast<unsigned>(cphase));
+                need = min(last_grp_c, need + NGRP);
+                if (spin) mbar_wait_u<0>(fc_u + 8u * cslot, static_cast<unsigned>(cphase));
+                else mbar_wait_u<kHint>(fc_u + 8u * cslot, static_cast<unsigned>(cphase));
                 const unsigned cg = cut_s + cslot * kCutBytes;
                 double v[RS][CPT], thr[RS][CPT], sum[RS][CPT];
                 bool hit[RS][CPT];
@@ -375,19 +398,25 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
                 } else if (has_word) { // no hit in the block: zero mask words
                     *mword = 0u;
                 }
-                mword += mstep;
+                mword += mstep * NGRP;
                 __syncwarp();
                 if (lane == 0) {
                     mbar_arrive_u(ec_u + 8u * cslot);
-                    if (step + 1 < n_steps && released < done) {
-                        ++released;
-                        mbar_arrive_u(et_u + 8u * rslot);
-                        if (++rslot == G.ng) rslot = 0;
+                    if (step + 1 < n_steps) {
+#pragma unroll
+                        for (int q = 0; q < NGRP; ++q) {
+                            if (released < done) {
+                                ++released;
+                                mbar_arrive_u(et_u + 8u * rslot);
+                                if (++rslot == G.ng) rslot = 0;
+                            }
+                        }
                     }
                 }
-                ++done;
-                if (++cslot == kCutGroups) { cslot = 0; cphase ^= 1; }
-                constexpr unsigned kAdv = RS * kRowBytes;
+                done += NGRP;
+                cslot += NGRP;
+                if (cslot >= kCutG) { cslot -= kCutG; cphase ^= 1; }
+                constexpr unsigned kAdv = RS * NGRP * kRowBytes;
                 oA += kAdv; if (oA >= ring_end) oA -= ring_end;
                 oB += kAdv; if (oB >= ring_end) oB -= ring_end;
                 oC += kAdv; if (oC >= ring_end) oC -= ring_end;
@@ -554,12 +583,12 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
                 }
             }
         }
-        cslot += SG;
-        if (cslot == kCutGroups) { cslot = 0; cphase ^= 1; }
-        sA += RS; if (sA >= G.nr) sA -= G.nr;
-        sB += RS; if (sB >= G.nr) sB -= G.nr;
-        sC += RS; if (sC >= G.nr) sC -= G.nr;
-        sD += RS; if (sD >= G.nr) sD -= G.nr;
+        cslot += SG * NGRP;
+        if (cslot >= kCutG) { cslot -= kCutG; cphase ^= 1; }
+        sA += RS * NGRP; if (sA >= G.nr) sA -= G.nr;
+        sB += RS * NGRP; if (sB >= G.nr) sB -= G.nr;
+        sC += RS * NGRP; if (sC >= G.nr) sC -= G.nr;
+        sD += RS * NGRP; if (sD >= G.nr) sD -= G.nr;
     }
 }
 
@@ -591,11 +620,13 @@ bool encode3(CUtensorMap* m, CUtensorMapDataType dt, size_t esz, const void* bas
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <typename T, int NCW, int CPT, int BOXC, int SG, int OCC>
+template <typename T, int NCW, int CPT, int BOXC, int SG, int OCC, int NGRP = 1>
 cudaError_t go(const CfarLaunch& L0, cudaStream_t stream) {
     CfarLaunch L = L0;
     L.sleep_ns = 20000;
     if (const char* e = getenv("UWB_RING_SLEEP_NS")) L.sleep_ns = static_cast<unsigned>(atoi(e));
+    L.pf_groups = kPfGroups;
+    if (const char* e = getenv("UWB_RING_PF")) L.pf_groups = atoi(e) > 0 ? atoi(e) : kPfGroups;
     L.debug = 0;
     if (const char* e = getenv("UWB_RING_DEBUG")) L.debug = static_cast<unsigned>(atoi(e));
     L.col_tiles = (L.cols + kW - 1) / kW;
@@ -624,14 +655,14 @@ cudaError_t go(const CfarLaunch& L0, cudaStream_t stream) {
     if (!encode3(&tmap_cut, sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
                  sizeof(T), L.maps, L.cols, L.geo.buf_rows, n_maps, L.ld, mstride, kW, kG))
         return cudaErrorNotSupported;
-    const size_t smem = ring_smem_bytes<T>(L.hr, BOXC, SG, L.ring_ahead);
+    const size_t smem = ring_smem_bytes<T>(L.hr, BOXC, SG, L.ring_ahead, cut_groups_for(OCC, sizeof(T)));
     if (smem > 227 * 1024) return cudaErrorNotSupported;
     const dim3 grid(static_cast<unsigned>(L.col_tiles * L.row_chunks), static_cast<unsigned>(L.n_jobs), 1);
-    cudaError_t e = cudaFuncSetAttribute(cfar_ws_kernel<T, NCW, CPT, BOXC, SG, OCC>,
+    cudaError_t e = cudaFuncSetAttribute(cfar_ws_kernel<T, NCW, CPT, BOXC, SG, OCC, NGRP>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     ++g_kernel_launches;
-    cfar_ws_kernel<T, NCW, CPT, BOXC, SG, OCC><<<grid, (NCW + 1) * kWarp, smem, stream>>>(L, tmap_tab, tmap_cut);
+    cfar_ws_kernel<T, NCW, CPT, BOXC, SG, OCC, NGRP><<<grid, (NCW * NGRP + 1) * kWarp, smem, stream>>>(L, tmap_tab, tmap_cut);
     return cudaGetLastError();
 }
 
@@ -643,7 +674,7 @@ cudaError_t go_occ(const CfarLaunch& L, cudaStream_t stream) {
     int occ = 0;
     const int pinned = getenv("UWB_RING_OCC") ? atoi(getenv("UWB_RING_OCC")) : 0;
     auto fits = [&](int o, int ahead) {
-        return ring_smem_bytes<T>(L.hr, BOXC, 1, ahead) <= static_cast<size_t>(233472 / o - 1024);
+        return ring_smem_bytes<T>(L.hr, BOXC, 1, ahead, cut_groups_for(o, sizeof(T))) <= static_cast<size_t>(233472 / o - 1024);
     };
     for (int o : {4, 3, 2, 1}) {
         if (pinned && o != pinned) continue;
@@ -660,7 +691,15 @@ cudaError_t go_occ(const CfarLaunch& L, cudaStream_t stream) {
         case 4: return go<T, 4, 1, BOXC, 1, 4>(La, stream);
         case 3: return go<T, 4, 1, BOXC, 1, 3>(La, stream);
         case 2: return go<T, 4, 1, BOXC, 1, 2>(La, stream);
-        default: return go<T, 4, 1, BOXC, 1, 1>(La, stream);
+        default:
+            // one CTA per SM (tall windows): two consumer warp groups on alternate steps
+            {
+                const char* e = getenv("UWB_RING_GROUPS");
+                const int ngrp = e ? atoi(e) : 2;
+                if (ngrp == 4) return go<T, 4, 1, BOXC, 1, 1, 4>(La, stream);
+                if (ngrp == 1) return go<T, 4, 1, BOXC, 1, 1>(La, stream);
+                return go<T, 4, 1, BOXC, 1, 1, 2>(La, stream);
+            }
     }
 }
 

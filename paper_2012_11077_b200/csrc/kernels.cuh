@@ -164,6 +164,7 @@ struct CfarLaunch {
     unsigned sleep_ns;   // barrier-wait suspend hint of the CFAR ring kernel (ns)
     unsigned debug;      // bit 0: consumers skip the cell arithmetic (data-movement probe)
     int ring_ahead;      // CFAR ring: table groups of look-ahead beyond the window
+    int pf_groups;       // CFAR ring: L2 prefetch distance of both streams (groups)
     int64_t col_tiles;
 };
 

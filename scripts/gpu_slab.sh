@@ -1,10 +1,8 @@
-# cfg 4: tile-mode SAT, CFAR ring row chunks, multi-CTA merge sort
+# cfg 4 CFAR at one CTA per SM: consumer wait mode
 export PYTHONPATH=.
-mkdir -p gpurun_out
-timeout -s KILL 900 python -m pytest tests/test_gpu_tiles.py tests/test_gpu_batch.py tests/test_gpu_fullsize.py -x -q > gpurun_out/tiles_tests.log 2>&1
-tail -3 gpurun_out/tiles_tests.log
-for v in "MODE=tile SLAB_ROWS=512" "MODE=tile SLAB_ROWS=512 UWB_SORT_ONE_CTA=1" \
-         "MODE=tile SLAB_ROWS=512 UWB_RING_ROWS=512" "MODE=tile SLAB_ROWS=512 UWB_RING_ROWS=1024" \
-         "MODE=tile SLAB_ROWS=512 UWB_RING_ROWS=2048" "MODE=tile SLAB_ROWS=512 UWB_RING_ROWS=128"; do
-  echo "[$v] $(env $v timeout 120 python scripts/cfg4_probe.py 2>&1 | tail -1)"
+for v in "UWB_RING_DEBUG=0" "UWB_RING_DEBUG=2" "UWB_RING_DEBUG=2 UWB_RING_GROUPS=1" "UWB_RING_DEBUG=1" "UWB_RING_DEBUG=3"; do
+  echo "[$v] $(env MODE=tile SLAB_ROWS=512 $v timeout -s KILL 120 python scripts/cfg4_probe.py 2>&1 | tail -1)"
+done
+for v in "UWB_RING_DEBUG=0" "UWB_RING_DEBUG=2"; do
+echo "cfg3 [$v]: $(env $v timeout -s KILL 300 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline 2>&1 | tail -1 | grep -o '"phases_ms": {[^}]*}')"
 done
