@@ -203,7 +203,7 @@ Plan make_plan(const uwb_map_batch& b, const uwb_cfar_params* p, int sat_mode, u
         }
     }
     P.geo.band_seg = table_ld_for(P.sat_cols);
-    P.table_ld = P.geo.band_seg * P.geo.n_bands;
+    P.table_ld = P.geo.band_seg;
     P.table_stride = (P.max_rows + 1) * P.table_ld;
     P.sat_jobs = P.n_jobs * P.geo.n_bands;
     P.cpl = sat_cpl_for(P.sat_jobs, P.sat_cols);
@@ -214,7 +214,7 @@ Plan make_plan(const uwb_map_batch& b, const uwb_cfar_params* p, int sat_mode, u
         off += round_up(static_cast<int64_t>(bytes), 256);
         return o;
     };
-    P.off_tables = take(sizeof(double) * static_cast<size_t>(P.n_jobs) * P.table_stride);
+    P.off_tables = take(sizeof(double) * static_cast<size_t>(P.sat_jobs) * P.table_stride);
     P.edge_stride = round_up(P.max_rows, 32);
     // S(r, strip's last column) handed from each strip to the next, contiguous per strip
     P.off_edge = take(P.strips > 1 ? sizeof(double) * static_cast<size_t>(P.sat_jobs) * P.strips * P.edge_stride : 0);

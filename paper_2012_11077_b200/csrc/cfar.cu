@@ -50,7 +50,8 @@ cfar_integral_kernel(CfarLaunch L) {
     const int rb = min(ra + kCfarRowChunk, static_cast<int>(L.geo.owned_end(slab)));
     if (ra >= rb) return;
     const int trow0 = static_cast<int>(L.geo.table_begin(slab));
-    const double* tab = L.table + job * L.table_stride + (col_ok ? L.geo.band_dx_for_col(c) : 0);
+    const int64_t band = col_ok ? L.geo.band_of(c) : 0; // band tables: local columns
+    const double* tab = L.table + (job * L.geo.n_bands + band) * L.table_stride - L.geo.band_c0(band);
     const int64_t ld = L.table_ld;
     const T* cut_base = static_cast<const T*>(L.maps) + map * L.map_stride;
 

@@ -167,10 +167,12 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
 
     // table storage columns of the ring rows: [e_lo, e_lo + BOXC), 16-byte aligned
     const int e_lo = (kTabShift + max(0, c0 - hc)) & ~1;
-    // TMA column of e_lo: shifted into this tile's band table (UWB_SAT_TILE; 0
-    // otherwise). Bands own whole 128-column tiles and the shift is even, so
-    // the consumers' offsets from e_lo are unchanged.
-    const int e_tx = e_lo + static_cast<int>(L.geo.band_dx_for_col(c0));
+    // TMA column / table index of this tile's band table (UWB_SAT_TILE; the
+    // job's own table otherwise). Bands own whole 128-column tiles and start on
+    // even columns, so the consumers' offsets from e_lo are unchanged.
+    const int64_t band = L.geo.band_of(c0);
+    const int e_tx = e_lo - static_cast<int>(L.geo.band_c0(band));
+    const int z_tab = static_cast<int>(job * L.geo.n_bands + band);
     // padded table rows needed by output rows [ra, rb), in groups of kG from i_lo
     const int i_lo = max(0, ra - hr);
     const int i_hi = min(rows, rb + hr);
@@ -197,7 +199,7 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
         const int last_grp = (i_hi - i_lo) / kG;
         const int pf = L.pf_groups;
         for (int g = 0; g <= min(last_grp, pf - 1); ++g)
-            tma_prefetch3(&tmap_tab, e_tx, i_lo + g * kG - trow0, static_cast<int>(job));
+            tma_prefetch3(&tmap_tab, e_tx, i_lo + g * kG - trow0, z_tab);
         const int buf0 = static_cast<int>(L.geo.buf_row0);
         for (int g = 0; g < min(n_cg, pf); ++g)
             tma_prefetch3(&tmap_cut, c0, ra + g * kG - buf0, static_cast<int>(map));
@@ -216,12 +218,12 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
                 // consecutive ring rows are always contiguous in memory
                 mbar_expect_tx(&full_t[gslot], gslot < SG ? 2 * kTabBox : kTabBox);
                 tma_box3(slots + static_cast<size_t>(gslot * kG) * BOXC, &tmap_tab, e_tx, first - trow0,
-                         static_cast<int>(job), &full_t[gslot]);
+                         z_tab, &full_t[gslot]);
                 if (gslot < SG)
                     tma_box3(slots + static_cast<size_t>(G.nr + gslot * kG) * BOXC, &tmap_tab, e_tx, first - trow0,
-                             static_cast<int>(job), &full_t[gslot]);
+                             z_tab, &full_t[gslot]);
                 if (grp + pf <= last_grp)
-                    tma_prefetch3(&tmap_tab, e_tx, first + pf * kG - trow0, static_cast<int>(job));
+                    tma_prefetch3(&tmap_tab, e_tx, first + pf * kG - trow0, z_tab);
                 if (++gslot == G.ng) { gslot = 0; gphase ^= 1; }
                 ++grp;
             } else {
@@ -647,7 +649,7 @@ cudaError_t go(const CfarLaunch& L0, cudaStream_t stream) {
     const int64_t n_maps = L.n_jobs / L.geo.n_slabs;
     CUtensorMap tmap_tab, tmap_cut;
     const uint64_t tab_rows = static_cast<uint64_t>(L.table_stride / L.table_ld);
-    if (!encode3(&tmap_tab, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, L.table, L.table_ld, tab_rows, L.n_jobs, L.table_ld,
+    if (!encode3(&tmap_tab, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, L.table, L.table_ld, tab_rows, L.n_jobs * L.geo.n_bands, L.table_ld,
                  L.table_stride, BOXC, kG))
         return cudaErrorNotSupported;
     // a single map's stride is never used; give the encoder a valid one

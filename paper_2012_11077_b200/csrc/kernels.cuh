@@ -43,9 +43,9 @@ struct JobGeometry {
     // Column bands (UWB_SAT_TILE): band k owns columns [k*band_cols, (k+1)*band_cols)
     // and its table covers band_width source columns from band_c0(k) (the owned
     // columns plus a 32-aligned halo >= g_c + b_c on each side, moved inward at
-    // the map edges, so every band table has the same width). Band k's table is
-    // the column segment [k*band_seg, (k+1)*band_seg) of the job's table rows.
-    // n_bands == 1: no bands (band_width = map_cols, band_seg = table ld).
+    // the map edges, so every band table has the same width). Band tables are
+    // separate pitched tables (ld = band_seg), band k of CFAR job j at table
+    // index j * n_bands + k. n_bands == 1: no bands (band_width = map_cols).
     int64_t map_cols;   // global map columns (clamp bounds)
     int64_t n_bands;
     int64_t band_cols;
@@ -72,13 +72,7 @@ struct JobGeometry {
         c = c > 0 ? c : 0;
         return c < map_cols - band_width ? c : map_cols - band_width;
     }
-    // table storage column of map column c minus (kTabShift + 1 + c): the band
-    // segment's offset minus its first source column
-    __host__ __device__ int64_t band_dx_for_col(int64_t c) const {
-        if (n_bands <= 1) return 0;
-        const int64_t k = c / band_cols;
-        return k * band_seg - band_c0(k);
-    }
+    __host__ __device__ int64_t band_of(int64_t c) const { return n_bands > 1 ? c / band_cols : 0; }
     // rows of the largest table (source rows, excluding the zero row)
     __host__ __device__ int64_t max_table_rows() const {
         const int64_t r = slab_rows + 2 * halo;
@@ -132,7 +126,7 @@ __host__ __device__ inline SatJobView sat_job(const SatLaunch& L, int64_t job) {
     v.rows = L.geo.table_end(s) - b;
     v.row0 = b;
     v.col0 = c0;
-    v.table = L.table + ms * L.table_stride + k * L.geo.band_seg;
+    v.table = L.table + job * L.table_stride;
     v.nonfinite = L.first_bad ? L.first_bad + 2 * m : nullptr;
     return v;
 }
