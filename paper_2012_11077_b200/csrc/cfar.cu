@@ -258,18 +258,23 @@ sort_detections_kernel(uwb_detection* dets, int64_t cap, const unsigned long lon
 // producing output entries [x * kMergeTile, +kMergeTile) of the map's merged
 // pairs of width-`width` runs (kMergeTile divides 2 * width). The CTA finds its
 // input ranges by two merge-path searches, stages them in shared memory and
-// merges kItems per thread there. width >= count is a plain copy.
+// merges kItems per thread there. A list needs P = ceil(log2(count / kSortRun))
+// passes; pass q >= P does nothing, except that an odd P ends in the scratch
+// buffer and pass P (reading it, width >= count) copies the list back.
 constexpr int kMergeTile = 2048;
 constexpr int kMergeThreads = 256;
 __global__ void __launch_bounds__(kMergeThreads)
 merge_pass_kernel(const uwb_detection* in_all, uwb_detection* out_all, int64_t cap,
-                  const unsigned long long* counts, int64_t width) {
+                  const unsigned long long* counts, int64_t width, int q) {
     extern __shared__ uwb_detection smem_det[];
     __shared__ int split[2];
     const int64_t map = blockIdx.y;
     const int64_t count = imin(static_cast<int64_t>(counts[map]), cap);
     const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kMergeTile;
     if (count <= kSortRun || t0 >= count) return; // short lists stay sorted in place
+    int passes = 0;
+    for (int64_t w = kSortRun; w < count; w *= 2) ++passes;
+    if (q > passes || (q == passes && passes % 2 == 0)) return;
     const uwb_detection* in = in_all + map * cap;
     uwb_detection* out = out_all + map * cap;
     const int64_t base = (t0 / (2 * width)) * (2 * width);
@@ -368,7 +373,7 @@ cudaError_t launch_sort_detections(uwb_detection* dets, int64_t cap, const unsig
             for (int q = 0; q < passes; ++q, w *= 2) {
                 ++g_kernel_launches;
                 merge_pass_kernel<<<dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(n_maps)), kMergeThreads,
-                                    msmem, stream>>>(q % 2 ? scratch : dets, q % 2 ? dets : scratch, cap, counts, w);
+                                    msmem, stream>>>(q % 2 ? scratch : dets, q % 2 ? dets : scratch, cap, counts, w, q);
                 if ((e = cudaGetLastError()) != cudaSuccess) return e;
             }
             return cudaSuccess;
