@@ -273,7 +273,6 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
     const int rg = ra + grp_id * RS;
     int sA = slot0(rg - hr), sB = slot0(rg + hr + 1), sC = slot0(rg - gr), sD = slot0(rg + gr + 1);
     constexpr unsigned kHint = 20000; // ns a waiting consumer may sleep in the barrier unit
-    const bool spin = (L.debug & 2u) != 0; // probe: spin in try_wait without a suspend hint
     const unsigned full_t_u = smem_u32(full_t), full_c_u = smem_u32(full_c);
     const unsigned empty_t_u = smem_u32(empty_t), empty_c_u = smem_u32(empty_c);
     // table groups needed through step s: min(last, need_base + s) in the interior
@@ -352,15 +351,13 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
 #pragma unroll
                 for (int q = 0; q < NGRP; ++q) { // one more table group per step
                     if (waited < need) {
-                        if (spin) mbar_wait_u<0>(ft_u + 8u * wslot, static_cast<unsigned>(wphase));
-                        else mbar_wait_u<kHint>(ft_u + 8u * wslot, static_cast<unsigned>(wphase));
+                        mbar_wait_u<kHint>(ft_u + 8u * wslot, static_cast<unsigned>(wphase));
                         ++waited;
                         if (++wslot == G.ng) { wslot = 0; wphase ^= 1; }
                     }
                 }
                 need = min(last_grp_c, need + NGRP);
-                if (spin) mbar_wait_u<0>(fc_u + 8u * cslot, static_cast<unsigned>(cphase));
-                else mbar_wait_u<kHint>(fc_u + 8u * cslot, static_cast<unsigned>(cphase));
+                mbar_wait_u<kHint>(fc_u + 8u * cslot, static_cast<unsigned>(cphase));
                 const unsigned cg = cut_s + cslot * kCutBytes;
                 double v[RS][CPT], thr[RS][CPT], sum[RS][CPT];
                 bool hit[RS][CPT];
