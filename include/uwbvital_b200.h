@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define UWB_B200_ABI_VERSION 1
+#define UWB_B200_ABI_VERSION 2
 
 /* Status codes; 1..5 correspond one-to-one to the reference exception classes
  * of proj/include/uwbvital/errors.hpp:13-41. */
@@ -189,6 +189,18 @@ typedef struct uwb_cfar_outputs {
     uint64_t* det_counts;      /* per map total count (may exceed capacity) */
     uint64_t* first_bad;       /* per map 2 entries: first non-finite, first negative
                                   cell as row-major index, UINT64_MAX if none */
+    /* Tie band of the north star (optional, certified path): cells whose CUT lies
+     * within 1e-6 relative of T, |cut - T| <= 1e-6 T. tie_counts: per map count
+     * (UINT64_MAX for a map the certified path handed to the exact path);
+     * ties: per map tie_capacity records {row, col, cut, T} in no order. */
+    uint64_t* tie_counts;
+    uwb_detection* ties;
+    uint64_t tie_capacity;
+    /* optional, per map: 0 = decided by the certified path, bit 0 = candidate
+     * list overflow, bit 1 = a value outside the certified range (both ran the
+     * exact path instead; same results), UINT32_MAX = the call used the exact
+     * path for every map. */
+    uint32_t* cert_status;
 } uwb_cfar_outputs;
 
 /* Device workspace bytes needed by uwb_dev_cfar2d for this batch and mode.
@@ -212,7 +224,16 @@ uint64_t uwb_dev_cfar2d_workspace(const uwb_map_batch* batch, const uwb_cfar_par
  *   on an otherwise idle B200 the two-kernel default is measured slightly
  *   faster). No table is left in `workspace`.
  * flags bit 3: the naive backend instead (cfar.cpp:200-216: explicit ring sums,
- *   no table; GLOBAL mode only) - the baseline of the paper's Table I. */
+ *   no table; GLOBAL mode only) - the baseline of the paper's Table I.
+ * flags bit 6: force the exact two-kernel path (full table + cfar_ws_kernel).
+ *   By default a call that wants masks and detection lists (no thresholds, no
+ *   mask_u8, no bits 2/4) and whose window is one of the instantiated shapes
+ *   (g+b, g) per axis in {(10,2), (5,1), (36,4), (19,3)} runs the certified-
+ *   decision path (cfar_cert.cu): a quantised window-sum pass certifies almost
+ *   every cell below T against an a-priori bound of the reference's table
+ *   rounding, the SAT stores only the taps of the remaining candidates, and
+ *   those are decided exactly. Results are identical to the exact path; a call
+ *   that should leave its tables for a later bit-2 call must set bit 6. */
 uwb_status uwb_dev_cfar2d(const uwb_map_batch* batch, const uwb_cfar_params* params,
                           const double* alpha_dev, int32_t sat_mode, uint64_t slab_rows,
                           const uwb_cfar_outputs* out, void* workspace, uint64_t workspace_bytes,
@@ -308,6 +329,9 @@ uwb_status uwb_dev_rfrm_to_frames(const float* payload, uint64_t n_rec, uint64_t
  * triples {sat_ms, cfar_ms, sort_ms} and clears the ring. Returns the count. */
 uint64_t uwb_kernel_launches(void);
 int32_t uwb_dev_phase_ms(float* out, int32_t max_calls);
+/* Same ring, four phases per call {certify (+ tap marking), SAT, CFAR (certified
+ * resolve or the exact kernel), sort}; the exact path's certify phase is ~0. */
+int32_t uwb_dev_phase_ms4(float* out, int32_t max_calls);
 
 /* Pinned host allocation helpers (cudaHostAlloc / cudaFreeHost). */
 void* uwb_host_alloc(uint64_t bytes);

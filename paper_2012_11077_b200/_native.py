@@ -79,7 +79,9 @@ class uwb_cfar_outputs(C.Structure):
     _fields_ = [("mask_bits", C.c_void_p), ("words_per_row", C.c_uint64),
                 ("mask_map_stride", C.c_uint64), ("mask_u8", C.c_void_p),
                 ("thresholds", C.c_void_p), ("dets", C.c_void_p), ("det_capacity", C.c_uint64),
-                ("det_counts", C.c_void_p), ("first_bad", C.c_void_p)]
+                ("det_counts", C.c_void_p), ("first_bad", C.c_void_p),
+                ("tie_counts", C.c_void_p), ("ties", C.c_void_p), ("tie_capacity", C.c_uint64),
+                ("cert_status", C.c_void_p)]
 
 
 _P = C.c_void_p
@@ -121,6 +123,7 @@ SIGNATURES = {
     "uwb_host_cfar2d_batch": (_S, [_P, _P, C.c_int32, _U64, _P, _P, _U64, _P, _U64]),
     "uwb_kernel_launches": (_U64, []),
     "uwb_dev_phase_ms": (C.c_int32, [_P, C.c_int32]),
+    "uwb_dev_phase_ms4": (C.c_int32, [_P, C.c_int32]),
     "uwb_host_alloc": (_P, [_U64]),
     "uwb_host_free": (None, [_P]),
 }

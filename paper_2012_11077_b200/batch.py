@@ -26,7 +26,7 @@ class BatchCfar:
                  dtype: torch.dtype = torch.float32, sat_mode: str = "global", slab_rows: int = 0,
                  det_capacity: int = 1024, device=None, want_mask_u8: bool = False,
                  want_thresholds: bool = False, window: tuple[int, int, int, int] | None = None,
-                 workspace: torch.Tensor | None = None):
+                 workspace: torch.Tensor | None = None, tie_capacity: int = 64):
         """``window = (global_rows, buf_row0, row_begin, row_end[, col_bands])``: the
         maps passed to each call hold rows [buf_row0, buf_row0 + rows) of maps with
         ``global_rows`` rows and the call owns rows [row_begin, row_end) (one
@@ -57,6 +57,11 @@ class BatchCfar:
                         if want_mask_u8 else None)
         self.thresholds = (torch.zeros((self.n_maps, out_rows, self.cols), dtype=torch.float64, device=dev)
                            if want_thresholds else None)
+        # tie band (|cut - T| <= 1e-6 T) and per-map certificate status (certified path)
+        self.tie_capacity = int(tie_capacity)
+        self.tie_counts = torch.zeros(self.n_maps, dtype=torch.int64, device=dev)
+        self.ties = torch.zeros((self.n_maps, max(1, self.tie_capacity), 32), dtype=torch.uint8, device=dev)
+        self.cert_status = torch.zeros(self.n_maps, dtype=torch.int32, device=dev)
         self._cparams = params.to_c()
         self._batch = N.uwb_map_batch(None, _DT[dtype], 0, self.n_maps, self.rows, self.cols, self.cols,
                                       self.rows * self.cols)
@@ -77,17 +82,22 @@ class BatchCfar:
             self.mask_bits.data_ptr(), self.words_per_row, out_rows * self.words_per_row,
             self.mask_u8.data_ptr() if self.mask_u8 is not None else None,
             self.thresholds.data_ptr() if self.thresholds is not None else None,
-            self.dets.data_ptr(), self.det_capacity, self.counts.data_ptr(), self.first_bad.data_ptr())
+            self.dets.data_ptr(), self.det_capacity, self.counts.data_ptr(), self.first_bad.data_ptr(),
+            self.tie_counts.data_ptr(), self.ties.data_ptr(), self.tie_capacity, self.cert_status.data_ptr())
 
     def __call__(self, maps: torch.Tensor, sort: bool = True, stream=None, phase_events: bool = False,
-                 reuse_tables: bool = False, naive: bool = False, fused: bool = False) -> None:
+                 reuse_tables: bool = False, naive: bool = False, fused: bool = False,
+                 exact: bool = False, dense_tables: bool = False) -> None:
         """Launch SAT + CFAR (+ sort) for ``maps`` of shape (n_maps, rows, cols).
         ``phase_events`` records per-phase CUDA events (read with :func:`phase_ms`).
         ``reuse_tables`` skips the SAT: the (shared) workspace already holds the
         tables of these maps from the previous call (another parameter set).
         ``naive`` runs the naive backend (explicit window sums, no table).
         ``fused`` runs SAT and CFAR as one kernel with the table kept on chip
-        (whole-map batches; no table is left for ``reuse_tables``)."""
+        (whole-map batches; no table is left for ``reuse_tables``).
+        ``exact`` forces the two-kernel path (full table, then the ring CFAR)
+        instead of the default certified-decision path; a call whose tables a
+        later ``reuse_tables`` call reads must pass it."""
         if maps.dtype != self.dtype or tuple(maps.shape) != (self.n_maps, self.rows, self.cols):
             raise ValueError(f"expected {(self.n_maps, self.rows, self.cols)} {self.dtype}, got "
                              f"{tuple(maps.shape)} {maps.dtype}")
@@ -95,7 +105,7 @@ class BatchCfar:
             raise ValueError("maps must be a contiguous CUDA tensor")
         self._batch.maps = maps.data_ptr()
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
-        flags = (0 if sort else 1) | (2 if phase_events else 0) | (4 if reuse_tables else 0) | (8 if naive else 0) | (16 if fused else 0)
+        flags = (0 if sort else 1) | (2 if phase_events else 0) | (4 if reuse_tables else 0) | (8 if naive else 0) | (16 if fused else 0) | (64 if exact else 0) | (128 if dense_tables else 0)
         if self.window is None:
             st = N.lib.uwb_dev_cfar2d(C.byref(self._batch), C.byref(self._cparams), self.alpha.data_ptr(),
                                       self.sat_mode, C.c_uint64(self.slab_rows), C.byref(self._out),
@@ -122,6 +132,18 @@ class BatchCfar:
 
     def detection_counts(self) -> np.ndarray:
         return self.counts.cpu().numpy()
+
+    def tie_band(self, i: int) -> np.ndarray:
+        """Map i's tie-band cells (|cut - T| <= 1e-6 T) from the certified path,
+        as detection records {row, col, value=cut, threshold=T}, sorted by (row, col)."""
+        n = int(self.tie_counts[i].item())
+        if n < 0 or n == 0xFFFFFFFFFFFFFFFF:
+            raise RuntimeError(f"map {i}: tie band unknown (the map ran the exact path)")
+        if n > self.tie_capacity:
+            raise CapacityError(f"map {i}: {n} tie-band cells > capacity {self.tie_capacity}", n)
+        raw = self.ties[i, :n].contiguous().cpu().numpy().reshape(-1)
+        t = np.frombuffer(raw.tobytes(), dtype=DETECTION_DTYPE, count=n).copy()
+        return t[np.lexsort((t["col"], t["row"]))]
 
     def detections(self, i: int) -> np.ndarray:
         n = int(self.counts[i].item())
@@ -203,6 +225,15 @@ class DetectBatch:
         words = self.mask_bits[i].cpu().numpy().view(np.uint32)
         bits = np.unpackbits(words.view(np.uint8).reshape(self.m, -1), axis=1, bitorder="little")
         return bits[:, : self.kept].astype(np.uint8)
+
+
+def phase_ms4(max_calls: int = 1024) -> np.ndarray:
+    """(calls, 4) array of {certify, sat, cfar, sort} milliseconds (certify is the
+    certified path's window-sum pass + tap marking; ~0 on the exact path; cfar is
+    the certified resolve or the exact ring kernel)."""
+    out = np.zeros((max_calls, 4), dtype=np.float32)
+    n = N.lib.uwb_dev_phase_ms4(out.ctypes.data_as(C.c_void_p), max_calls)
+    return out[:n].copy()
 
 
 def phase_ms(max_calls: int = 1024) -> np.ndarray:

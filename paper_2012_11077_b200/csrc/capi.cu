@@ -152,7 +152,10 @@ struct Plan {
     int64_t n_maps, cols, n_jobs, table_ld, table_stride, strips, max_rows, edge_stride;
     int64_t sat_jobs, sat_cols; // SAT jobs (map, slab, band) and table source columns per job
     int cpl;
-    size_t off_tables, off_edge, off_prog, off_counter, off_scratch, total;
+    size_t off_tables, off_edge, off_prog, off_counter, off_scratch;
+    // certified-decision CFAR (cfar_cert.cu): candidate lists, status, tap bitmap, K/E table
+    int64_t cand_cap, need_rows, n_int;
+    size_t off_cand, off_cand_count, off_status, off_need, off_ke, total;
 };
 
 // win == nullptr: the batch holds whole maps. Otherwise the batch buffer holds
@@ -221,6 +224,19 @@ Plan make_plan(const uwb_map_batch& b, const uwb_cfar_params* p, int sat_mode, u
     P.off_prog = take(sizeof(unsigned) * P.sat_jobs * P.strips);
     P.off_counter = take(sizeof(unsigned) * 4);
     P.off_scratch = take(det_cap > 2048 ? sizeof(uwb_detection) * P.n_maps * det_cap : 0);
+    if (p) {
+        // candidates: detections (about Pfa of the cells) plus the cells within
+        // the certification margin of T; 1/256 of the owned cells is >> both
+        const int64_t cells = owned * P.cols;
+        P.cand_cap = std::max<int64_t>(1024, (cells / 256 + 255) / 256 * 256);
+        P.need_rows = round_up(P.max_rows, 32);
+        P.n_int = static_cast<int64_t>(interior_count(*p));
+        P.off_cand = take(sizeof(int2) * P.n_maps * P.cand_cap);
+        P.off_cand_count = take(sizeof(unsigned) * P.n_maps);
+        P.off_status = take(sizeof(unsigned) * P.n_maps);
+        P.off_need = take(sizeof(unsigned) * P.sat_jobs * P.strips * P.need_rows);
+        P.off_ke = take(sizeof(float4) * (P.n_int + 1));
+    }
     P.total = off;
     return P;
 }
@@ -296,23 +312,86 @@ uwb_status check_batch(const uwb_map_batch* b) {
 }
 
 
-// Phase-event ring (flags bit 1 of uwb_dev_cfar2d).
+// Phase-event ring (flags bit 1 of uwb_dev_cfar2d): 5 events per call around
+// the phases {certify (+ tap marking), SAT, CFAR (certified resolve or the exact
+// ring kernel), sort}; the exact path's certify phase is empty.
 struct PhaseRing {
     static constexpr int kSlots = 1024;
+    static constexpr int kEv = 5;
     std::mutex mu;
-    std::vector<cudaEvent_t> ev; // 4 per slot
+    std::vector<cudaEvent_t> ev;
     int used = 0;
     cudaEvent_t* slot() {
         std::lock_guard<std::mutex> lk(mu);
         if (ev.empty()) {
-            ev.resize(static_cast<size_t>(kSlots) * 4);
+            ev.resize(static_cast<size_t>(kSlots) * kEv);
             for (auto& e : ev) cudaEventCreate(&e);
         }
         if (used >= kSlots) return nullptr;
-        return &ev[static_cast<size_t>(used++) * 4];
+        return &ev[static_cast<size_t>(used++) * kEv];
     }
 };
 PhaseRing g_phase;
+
+CertLaunch cert_launch(const Plan& P, const uwb_map_batch& b, const uwb_cfar_params& p, const double* alpha,
+                       char* ws, const uwb_cfar_outputs& o) {
+    CertLaunch L{};
+    L.maps = b.maps;
+    L.ld = static_cast<int64_t>(b.ld);
+    L.map_stride = static_cast<int64_t>(b.map_stride);
+    L.cols = P.cols;
+    L.geo = P.geo;
+    L.n_maps = P.n_maps;
+    L.gr = p.guard_rows;
+    L.gc = p.guard_cols;
+    L.hr = p.guard_rows + p.background_rows;
+    L.hc = p.guard_cols + p.background_cols;
+    L.alpha = alpha;
+    L.n_int = static_cast<int>(P.n_int);
+    L.ke = reinterpret_cast<const float4*>(ws + P.off_ke);
+    L.cand = reinterpret_cast<int2*>(ws + P.off_cand);
+    L.cand_count = reinterpret_cast<unsigned*>(ws + P.off_cand_count);
+    L.cand_cap = P.cand_cap;
+    L.status = reinterpret_cast<unsigned*>(ws + P.off_status);
+    L.first_bad = reinterpret_cast<unsigned long long*>(o.first_bad);
+    L.need = reinterpret_cast<unsigned*>(ws + P.off_need);
+    L.need_rows = P.need_rows;
+    L.strips = P.strips;
+    L.cpl = P.cpl;
+    L.table = reinterpret_cast<const double*>(ws + P.off_tables);
+    L.table_ld = P.table_ld;
+    L.table_stride = P.table_stride;
+    L.mask_bits = o.mask_bits;
+    L.words_per_row = static_cast<int64_t>(o.words_per_row);
+    L.mask_map_stride = static_cast<int64_t>(o.mask_map_stride);
+    L.dets = o.dets;
+    L.det_cap = static_cast<int64_t>(o.det_capacity);
+    L.det_counts = reinterpret_cast<unsigned long long*>(o.det_counts);
+    L.tie_counts = reinterpret_cast<unsigned long long*>(o.tie_counts);
+    L.ties = o.ties;
+    L.tie_cap = static_cast<int64_t>(o.tie_capacity);
+    int range = 9; // certified values lie in [0, 2^range)
+    if (const char* e = getenv("UWB_CERT_RANGE_LOG2")) range = std::max(0, std::min(20, atoi(e)));
+    cert_prepare(L, range);
+    return L;
+}
+
+// The certified path applies to mask + list outputs of the integral backend
+// with a window instantiated in cfar_cert.cu (the exact two-kernel path
+// otherwise; flags bit 6 forces it).
+bool cert_applies(const Plan& P, const uwb_map_batch& b, const uwb_cfar_params& p, const uwb_cfar_outputs& o,
+                  int backend, uint32_t flags) {
+    if (backend != UWB_INTEGRAL || (flags & (4u | 16u | 64u)) || o.thresholds || o.mask_u8 || !o.mask_bits)
+        return false;
+    // the certify kernel reads aligned column pairs (2x2 tiles)
+    const uint64_t esz = b.dtype == UWB_F32 ? 4 : 8;
+    if (b.cols % 2 || b.ld % 2 || (b.n_maps > 1 && b.map_stride % 2) ||
+        reinterpret_cast<uintptr_t>(b.maps) % (2 * esz))
+        return false;
+    if (P.cand_cap == 0 || P.geo.rows >= (int64_t(1) << 30) || P.cols >= (int64_t(1) << 30)) return false;
+    return cert_supported(p.guard_rows + p.background_rows, p.guard_rows, p.guard_cols + p.background_cols,
+                          p.guard_cols);
+}
 
 // Device-resident CFAR of a batch (no validation beyond layout; see uwb_dev_cfar2d).
 uwb_status dev_cfar(const uwb_map_batch& b, const uwb_cfar_params& p, const double* alpha,
@@ -327,8 +406,43 @@ uwb_status dev_cfar(const uwb_map_batch& b, const uwb_cfar_params& p, const doub
     cudaEvent_t* ev = (flags & 2u) ? g_phase.slot() : nullptr;
     UWB_CUDA_TRY(cudaMemsetAsync(o.det_counts, 0, sizeof(uint64_t) * b.n_maps, s));
     if (o.first_bad) UWB_CUDA_TRY(cudaMemsetAsync(o.first_bad, 0xff, sizeof(uint64_t) * 2 * b.n_maps, s));
+    if (o.tie_counts) UWB_CUDA_TRY(cudaMemsetAsync(o.tie_counts, 0, sizeof(uint64_t) * b.n_maps, s));
     if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[0], s));
-    if (backend == UWB_INTEGRAL) {
+    const bool cert = cert_applies(P, b, p, o, backend, flags);
+    if (o.cert_status) {
+        if (cert) UWB_CUDA_TRY(cudaMemsetAsync(o.cert_status, 0, sizeof(uint32_t) * b.n_maps, s));
+        else UWB_CUDA_TRY(cudaMemsetAsync(o.cert_status, 0xff, sizeof(uint32_t) * b.n_maps, s));
+    }
+    if (cert) {
+        // certify -> mark taps -> sparse SAT -> resolve (+ exact path for flagged maps)
+        const CertLaunch CL = cert_launch(P, b, p, alpha, ws, o);
+        UWB_CUDA_TRY(cudaMemsetAsync(CL.cand_count, 0, sizeof(unsigned) * P.n_maps, s));
+        UWB_CUDA_TRY(cudaMemsetAsync(CL.status, 0, sizeof(unsigned) * P.n_maps, s));
+        UWB_CUDA_TRY(cudaMemsetAsync(CL.need, 0, sizeof(unsigned) * P.sat_jobs * P.strips * P.need_rows, s));
+        UWB_CUDA_TRY(cudaMemset2DAsync(o.mask_bits, sizeof(uint32_t) * o.mask_map_stride, 0,
+                                       sizeof(uint32_t) * o.words_per_row * P.geo.out_rows(), b.n_maps, s));
+        UWB_CUDA_TRY(launch_cert_table(CL, const_cast<float4*>(CL.ke), static_cast<int>(P.n_int), s));
+        UWB_CUDA_TRY(launch_cert(CL, b.dtype, s));
+        UWB_CUDA_TRY(launch_cert_mark(CL, s));
+        if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[1], s));
+        SatLaunch SL = sat_launch(P, b, ws, reinterpret_cast<unsigned long long*>(o.first_bad));
+        SL.need = (flags & 128u) ? nullptr : CL.need; // bit 7 (test hook): full tables, same results
+        SL.need_rows = P.need_rows;
+        SL.map_full = CL.status;
+        SL.jobs_per_map = P.geo.n_slabs * P.geo.n_bands;
+        UWB_CUDA_TRY(run_sat(P, SL, b.dtype, s));
+        if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[2], s));
+        UWB_CUDA_TRY(launch_cert_resolve(CL, b.dtype, s));
+        // maps the certificate could not cover (values outside its range, or
+        // more candidates than the list holds) have full tables: exact kernel
+        CfarLaunch FL = cfar_launch(P, b, p, alpha, ws, o);
+        FL.map_filter = CL.status;
+        UWB_CUDA_TRY(launch_cfar_integral(FL, b.dtype, s));
+        if (o.cert_status)
+            UWB_CUDA_TRY(cudaMemcpyAsync(o.cert_status, CL.status, sizeof(uint32_t) * b.n_maps,
+                                         cudaMemcpyDeviceToDevice, s));
+    } else if (backend == UWB_INTEGRAL) {
+        if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[1], s));
         bool fused = false;
         if ((flags & 16u) && !(flags & 4u)) {
             // bit 4: SAT and CFAR as one kernel with the table on chip (no table
@@ -337,7 +451,7 @@ uwb_status dev_cfar(const uwb_map_batch& b, const uwb_cfar_params& p, const doub
             const SatLaunch SL = sat_launch(P, b, ws, reinterpret_cast<unsigned long long*>(o.first_bad));
             UWB_CUDA_TRY(cudaMemsetAsync(SL.gprog, 0, sizeof(unsigned) * P.sat_jobs * P.strips, s));
             UWB_CUDA_TRY(cudaMemsetAsync(SL.tile_counter, 0, sizeof(unsigned), s));
-            if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[1], s));
+            if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[2], s));
             const cudaError_t e = launch_cfar_fused(SL, cfar_launch(P, b, p, alpha, ws, o), b.dtype, s);
             if (e == cudaSuccess) {
                 fused = true;
@@ -352,19 +466,20 @@ uwb_status dev_cfar(const uwb_map_batch& b, const uwb_cfar_params& p, const doub
                 const SatLaunch SL = sat_launch(P, b, ws, reinterpret_cast<unsigned long long*>(o.first_bad));
                 UWB_CUDA_TRY(run_sat(P, SL, b.dtype, s));
             }
-            if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[1], s));
+            if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[2], s));
             UWB_CUDA_TRY(launch_cfar_integral(cfar_launch(P, b, p, alpha, ws, o), b.dtype, s));
         }
     } else {
         if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[1], s));
+        if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[2], s));
         UWB_CUDA_TRY(launch_cfar_naive(cfar_launch(P, b, p, alpha, nullptr, o), b.dtype, s));
     }
-    if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[2], s));
+    if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[3], s));
     struct Tail {
         cudaEvent_t* ev;
         cudaStream_t s;
         ~Tail() {
-            if (ev) cudaEventRecord(ev[3], s);
+            if (ev) cudaEventRecord(ev[4], s);
         }
     } tail{ev, s};
     if (!(flags & 1u)) {
@@ -1363,17 +1478,26 @@ uwb_status uwb_dev_rfrm_to_frames(const float* payload, uint64_t n_rec, uint64_t
 
 uint64_t uwb_kernel_launches(void) { return g_kernel_launches.load(); }
 
-int32_t uwb_dev_phase_ms(float* out, int32_t max_calls) {
+int32_t uwb_dev_phase_ms4(float* out, int32_t max_calls) {
     std::lock_guard<std::mutex> lk(g_phase.mu);
     const int n = std::min<int>(g_phase.used, max_calls);
     for (int i = 0; i < n; ++i) {
-        cudaEvent_t* e = &g_phase.ev[static_cast<size_t>(i) * 4];
-        cudaEventSynchronize(e[3]);
-        cudaEventElapsedTime(&out[3 * i + 0], e[0], e[1]);
-        cudaEventElapsedTime(&out[3 * i + 1], e[1], e[2]);
-        cudaEventElapsedTime(&out[3 * i + 2], e[2], e[3]);
+        cudaEvent_t* e = &g_phase.ev[static_cast<size_t>(i) * PhaseRing::kEv];
+        cudaEventSynchronize(e[4]);
+        for (int k = 0; k < 4; ++k) cudaEventElapsedTime(&out[4 * i + k], e[k], e[k + 1]);
     }
     g_phase.used = 0;
+    return n;
+}
+
+int32_t uwb_dev_phase_ms(float* out, int32_t max_calls) {
+    std::vector<float> q(static_cast<size_t>(std::max(0, max_calls)) * 4);
+    const int n = uwb_dev_phase_ms4(q.data(), max_calls);
+    for (int i = 0; i < n; ++i) { // {sat, cfar (certify + resolve), sort}
+        out[3 * i + 0] = q[4 * i + 1];
+        out[3 * i + 1] = q[4 * i + 0] + q[4 * i + 2];
+        out[3 * i + 2] = q[4 * i + 3];
+    }
     return n;
 }
 

@@ -41,6 +41,7 @@ cfar_integral_kernel(CfarLaunch L) {
     const int64_t job = blockIdx.y;
     const int64_t map = job / L.geo.n_slabs;
     const int64_t slab = job % L.geo.n_slabs;
+    if (L.map_filter && !L.map_filter[map]) return; // certified path: only flagged maps
     const int col_tile = static_cast<int>(blockIdx.x % L.col_tiles);
     const int chunk = static_cast<int>(blockIdx.x / L.col_tiles);
     const int c = col_tile * kCfarThreads + static_cast<int>(threadIdx.x);

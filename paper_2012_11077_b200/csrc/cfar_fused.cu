@@ -696,7 +696,9 @@ cudaError_t launch_cfar_fused(const SatLaunch& S, const CfarLaunch& C, int dtype
     F.gprog = S.gprog;
     F.unit_counter = S.tile_counter;
     F.c.debug = 0;
+#ifdef UWB_PROBE_BUILD // timing probes only: skip the arithmetic (never in the release library)
     if (const char* e = getenv("UWB_FUSED_DEBUG")) F.c.debug = static_cast<unsigned>(atoi(e));
+#endif
     return dtype == UWB_F32 ? go_fused_cpl<float>(F, stream) : go_fused_cpl<double>(F, stream);
 }
 

@@ -155,6 +155,7 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
     const int64_t job = blockIdx.y;
     const int64_t map = job / L.geo.n_slabs;
     const int64_t slab = job % L.geo.n_slabs;
+    if (L.map_filter && !L.map_filter[map]) return; // certified path: only flagged maps
     const int col_tile = static_cast<int>(blockIdx.x % L.col_tiles);
     const int chunk = static_cast<int>(blockIdx.x / L.col_tiles);
     const int rows = static_cast<int>(L.geo.rows), cols = static_cast<int>(L.cols);
@@ -627,7 +628,9 @@ cudaError_t go(const CfarLaunch& L0, cudaStream_t stream) {
     L.pf_groups = kPfGroups;
     if (const char* e = getenv("UWB_RING_PF")) L.pf_groups = atoi(e) > 0 ? atoi(e) : kPfGroups;
     L.debug = 0;
+#ifdef UWB_PROBE_BUILD // timing probes only: skip the arithmetic (never in the release library)
     if (const char* e = getenv("UWB_RING_DEBUG")) L.debug = static_cast<unsigned>(atoi(e));
+#endif
     L.col_tiles = (L.cols + kW - 1) / kW;
     // row chunks of kRingRows; a batch too small to give every SM two CTAs
     // (single small maps) takes shorter chunks (each re-reads its window's

@@ -100,8 +100,14 @@ struct SatLaunch {
     int elem_bytes;
     unsigned flags;      // bit 1: low-latency strip chain (set by the launcher)
     int cpl;             // columns per lane (strips of 32 * cpl columns): 1, 2 or 4
-    unsigned long long* trace; // debug (UWB_SAT_TRACE): per tile: SM id, globaltimer at the first
-                               // fetch, blocks 0..4 and the end, clock64 after each first-block step
+    // Sparse mode (certified CFAR, cfar_cert.cu): when `need` is set, only the
+    // 32-byte segments of S(r, .) marked in need[(job * strips + strip) *
+    // need_rows + r] (bit = lane) are stored; maps with map_full[map] != 0
+    // store every segment. Padded row / column 0 are not stored.
+    const unsigned* need;
+    int64_t need_rows;
+    const unsigned* map_full;
+    int64_t jobs_per_map; // SAT jobs per map (n_slabs * n_bands)
 };
 
 struct SatJobView {
@@ -160,6 +166,47 @@ struct CfarLaunch {
     int ring_ahead;      // CFAR ring: table groups of look-ahead beyond the window
     int pf_groups;       // CFAR ring: L2 prefetch distance of both streams (groups)
     int64_t col_tiles;
+    const unsigned* map_filter; // non-null: only maps with map_filter[map] != 0 run
+};
+
+// Certified-decision CFAR (cfar_cert.cu): one launch description shared by the
+// certify, mark and resolve kernels.
+struct CertLaunch {
+    const void* maps;
+    int64_t ld, map_stride, cols;
+    JobGeometry geo;     // the CFAR call's geometry (slabs / bands of the tables)
+    int64_t n_maps;
+    int gr, gc, hr, hc;
+    const double* alpha;
+    int n_int;           // interior training count
+    // quantisation q = round(x * 2^s) and the a-priori bound of the reference's rounding
+    int s_bits;
+    double scale, inv_scale_d, xlim, s_bound;
+    float inv_scale, magic;
+    uint32_t bits_magic, xlim_bits, ring_off;
+    const float4* ke;    // per n: {K_n, K_n 2^-(s+1), E_n}
+    // candidates
+    int2* cand;          // per map cand_cap (row, col), global rows
+    unsigned* cand_count;
+    int64_t cand_cap;
+    unsigned* status;    // per map: bit 0 list overflow, bit 1 value outside the certified range
+    unsigned long long* first_bad;
+    int64_t col_ctas, row_chunk, row_chunks;
+    // sparse-table taps
+    unsigned* need;
+    int64_t need_rows, strips;
+    int cpl;
+    const double* table;
+    int64_t table_ld, table_stride;
+    // outputs
+    uint32_t* mask_bits;
+    int64_t words_per_row, mask_map_stride;
+    uwb_detection* dets;
+    int64_t det_cap;
+    unsigned long long* det_counts;
+    unsigned long long* tie_counts;
+    uwb_detection* ties;
+    int64_t tie_cap;
 };
 
 cudaError_t launch_sat(const SatLaunch& L, int dtype, cudaStream_t stream);
@@ -171,6 +218,13 @@ cudaError_t launch_cfar_integral(const CfarLaunch& L, int dtype, cudaStream_t st
 // batches only; cudaErrorNotSupported when the geometry does not qualify.
 cudaError_t launch_cfar_fused(const SatLaunch& S, const CfarLaunch& C, int dtype, cudaStream_t stream);
 cudaError_t launch_cfar_naive(const CfarLaunch& L, int dtype, cudaStream_t stream);
+// certified-decision CFAR (cfar_cert.cu)
+bool cert_supported(int hr, int gr, int hc, int gc);
+void cert_prepare(CertLaunch& L, int range_log2);
+cudaError_t launch_cert_table(const CertLaunch& L, float4* ke, int n_max, cudaStream_t stream);
+cudaError_t launch_cert(const CertLaunch& L, int dtype, cudaStream_t stream);
+cudaError_t launch_cert_mark(const CertLaunch& L, cudaStream_t stream);
+cudaError_t launch_cert_resolve(const CertLaunch& L, int dtype, cudaStream_t stream);
 // Sort each map's detection list: value desc, row asc, col asc (cfar.cpp:170-173).
 cudaError_t launch_sort_detections(uwb_detection* dets, int64_t cap,
                                    const unsigned long long* counts, int64_t n_maps,

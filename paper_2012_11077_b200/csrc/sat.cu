@@ -52,6 +52,7 @@ constexpr int kAhead = 8;               // staging distance in steps (<= kXSlots
 constexpr int kXSlots = 16;             // lane-private source ring (copy steps)
 constexpr int kOSlots = 8;              // lane-private result delay ring (rows)
 constexpr int kPublishEvery = 64;       // steps between edge hand-overs
+constexpr int kL2Ahead = 48;            // sparse mode: L2 prefetch distance (rows)
 constexpr int kSatCtasPerSm = 3;        // occupancy target (registers and shared memory)
 #ifndef UWB_POLL_SLEEP_NS
 #define UWB_POLL_SLEEP_NS 200
@@ -155,12 +156,6 @@ __device__ __forceinline__ double lds_d(unsigned addr) {
 // Zero source for the virtual rows r < 0 of a strip's first block (see step()).
 __device__ __align__(16) double g_sat_zero[4];
 
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-
 __device__ __forceinline__ double canon_edge(double v) {
     return __double_as_longlong(v) == -1LL ? __longlong_as_double(0x7ff8000000000000LL) : v;
 }
@@ -171,7 +166,10 @@ __device__ __noinline__ void publish_rows(unsigned* prog, int rows_done, int lan
     __syncwarp();
 }
 
-template <typename T, int kCpl>
+// kSparse: certified-CFAR mode (see kernels.cuh SatLaunch::need): the same
+// recurrence, but only the table segments marked in the tap bitmap are stored,
+// straight from registers (no delay ring, no zero row / column).
+template <typename T, int kCpl, bool kSparse>
 __global__ void __launch_bounds__(kWarpsPerCta * kWarp, kSatCtasPerSm)
 sat_systolic_kernel(SatLaunch L) {
     constexpr int kStripCols = kCpl * kWarp;
@@ -199,12 +197,6 @@ sat_systolic_kernel(SatLaunch L) {
         tile = __shfl_sync(0xffffffffu, tile, 0);
         if (tile >= n_tiles) return;
 
-        unsigned long long* tr = L.trace ? L.trace + 40 * tile : nullptr;
-        if (tr && lane == 0) {
-            unsigned smid;
-            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-            tr[0] = smid;
-        }
         // strip-major claim order: every job's strip k precedes any job's strip k+1
         const int strip = static_cast<int>(tile / L.n_jobs);
         const int64_t job = tile % L.n_jobs;
@@ -217,8 +209,15 @@ sat_systolic_kernel(SatLaunch L) {
         const int64_t ld = L.ld;
         const T* src = static_cast<const T*>(J.src);
 
-        for (int k = 0; k < nvalid; ++k) table[kTabShift + 1 + c + k] = 0.0; // padded row 0 is zero
-        if (strip == 0 && lane == 0) table[kTabShift] = 0.0;
+        // sparse mode: this strip's tap bitmap (one word per row, bit = lane);
+        // a flagged map stores its whole table (the exact CFAR reads it)
+        const unsigned* need_col = kSparse ? L.need + (job * L.strips + strip) * L.need_rows : nullptr;
+        const bool store_all = kSparse && L.map_full && L.map_full[job / L.jobs_per_map] != 0;
+        const bool dense = !kSparse || store_all;
+        if (dense) {
+            for (int k = 0; k < nvalid; ++k) table[kTabShift + 1 + c + k] = 0.0; // padded row 0 is zero
+            if (strip == 0 && lane == 0) table[kTabShift] = 0.0;
+        }
 
         const unsigned* prog_in = strip > 0 ? L.gprog + job * L.strips + strip - 1 : nullptr;
         unsigned* prog_out = strip + 1 < L.strips ? L.gprog + job * L.strips + strip : nullptr;
@@ -326,7 +325,7 @@ sat_systolic_kernel(SatLaunch L) {
             const int r = s - lane;
             // (1) group g writes back row s - 8g - 8 (slot u mod 8, stored >= 1 step ago)
             const int rf = s - 8 * grp - 8;
-            if (kFirst ? rf >= 0 : (!kChecked || (rf >= 0 && rf < rows))) {
+            if (!kSparse && (kFirst ? rf >= 0 : (!kChecked || (rf >= 0 && rf < rows)))) {
                 double o[kCpl];
                 lds_out<kCpl>(o_lane + static_cast<unsigned>(u & (kOSlots - 1)) * kOSlotBytes, o);
                 if (!kChecked || nvalid == kCpl) {
@@ -343,7 +342,7 @@ sat_systolic_kernel(SatLaunch L) {
                         if (k < nvalid) tflush[k] = o[k];
                 }
             }
-            tflush += tld;
+            if constexpr (!kSparse) tflush += tld;
             // (2) stage source row s + kAhead - 8g into slot u (s0 is a multiple of 32)
             if (kFirst) {
                 const int row = s + kAhead - 8 * grp;
@@ -353,6 +352,10 @@ sat_systolic_kernel(SatLaunch L) {
                 stage(static_cast<unsigned>((u & (kXSlots - 1)) * kXSlotBytes), s + kAhead - 8 * grp, xrow, kChecked);
             }
             cp_async_commit();
+            // sparse mode is read-bound: pull the row kL2Ahead steps later into L2
+            // (the 16-step staging ring alone does not cover the DRAM latency)
+            if (kSparse && kMode == 0 && s + kAhead - 8 * grp + kL2Ahead < rows) // interior steps
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(xrow + kL2Ahead * ld));
             xrow += ld;
             // (3) this step's inputs were loaded one step ahead; load the next step's
             T x[kCpl];
@@ -387,7 +390,24 @@ sat_systolic_kernel(SatLaunch L) {
                 left_prev = left;
 #pragma unroll
                 for (int k = 0; k < kCpl; ++k) prev[k] = last[k] = sv[k];
-                sts_out<kCpl>(o_lane + ((static_cast<unsigned>(u) + o_rbase_lane) & (kOSlots - 1)) * kOSlotBytes, sv);
+                if constexpr (!kSparse) {
+                    sts_out<kCpl>(o_lane + ((static_cast<unsigned>(u) + o_rbase_lane) & (kOSlots - 1)) * kOSlotBytes, sv);
+                } else if (!kFirst || r >= 0) {
+                    // marked taps of row r: S(r, c..c+kCpl-1) = padded (r+1, c+1..)
+                    const unsigned w = store_all ? ~0u : __ldg(need_col + r);
+                    if ((w >> lane) & 1u) {
+                        double* dst = table + static_cast<int64_t>(r + 1) * tld + kTabShift + 1 + c;
+                        if (kCpl >= 2 && nvalid == kCpl) {
+#pragma unroll
+                            for (int q = 0; q < kCpl / 2; ++q)
+                                reinterpret_cast<double2*>(dst)[q] = make_double2(sv[2 * q], sv[2 * q + 1]);
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < kCpl; ++k)
+                                if (k < nvalid) dst[k] = sv[k];
+                        }
+                    }
+                }
             }
         };
 
@@ -402,9 +422,7 @@ sat_systolic_kernel(SatLaunch L) {
         double e_next = low_latency ? 0.0 : fetch_left(kWarp);
         cp_async_wait<kAhead - 1>();
         lds_lane<kCpl>(x_lane + (x_rbase_lane & (kXSlots - 1)) * kXSlotBytes, xn);
-        if (tr && lane == 0) tr[1] = gtimer();
         for (int s0 = 0; s0 < steps; s0 += kWarp) {
-            if (tr && lane == 0 && s0 / kWarp < 5) tr[2 + s0 / kWarp] = gtimer(); // blocks 0..4
             // left-strip edge values for rows [s0, s0 + 32) (lane 0 reads row s at step s)
             __syncwarp();
             asm volatile("st.shared.f64 [%0], %1;" ::"r"(edge_smem + 8u * lane), "d"(e_cur) : "memory");
@@ -417,7 +435,7 @@ sat_systolic_kernel(SatLaunch L) {
                 e_next = fetch_left(s0 + 2 * kWarp);
             }
             // padded column 0 of the rows group 0 writes back in this block
-            if (strip == 0 && s0 - 8 + lane >= 0 && s0 - 8 + lane < rows)
+            if (dense && strip == 0 && s0 - 8 + lane >= 0 && s0 - 8 + lane < rows)
                 table[static_cast<int64_t>(s0 - 8 + lane + 1) * tld + kTabShift] = 0.0;
             const bool fast = s0 >= kWarp && s0 + kWarp + kAhead <= rows && warp_fast;
             if (fast) {
@@ -427,10 +445,7 @@ sat_systolic_kernel(SatLaunch L) {
                 // the first block at interior speed (it is on every later strip's
                 // critical path in a chain)
 #pragma unroll 16
-                for (int u = 0; u < kWarp; ++u) {
-                    step(s0, u, std::integral_constant<int, 2>{});
-                    if (tr && lane == 0) tr[8 + u] = clock64();
-                }
+                for (int u = 0; u < kWarp; ++u) step(s0, u, std::integral_constant<int, 2>{});
             } else {
 #pragma unroll 1
                 for (int u = 0; u < kWarp && s0 + u < steps; ++u) step(s0, u, std::integral_constant<int, 1>{});
@@ -456,21 +471,20 @@ sat_systolic_kernel(SatLaunch L) {
         }
         cp_async_wait<0>();
         __syncwarp();
-        if (tr && lane == 0) tr[7] = gtimer();
     }
 }
 
-template <typename T, int kCpl>
+template <typename T, int kCpl, bool kSparse>
 static cudaError_t launch_sat_t(const SatLaunch& L, cudaStream_t stream) {
     const int64_t n_tiles = L.n_jobs * L.strips;
     const size_t smem = SatSmem<T, kCpl>::bytes();
-    cudaError_t e = cudaFuncSetAttribute(sat_systolic_kernel<T, kCpl>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+    auto kern = sat_systolic_kernel<T, kCpl, kSparse>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sat_systolic_kernel<T, kCpl>, kWarpsPerCta * kWarp, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarpsPerCta * kWarp, smem);
     // leave room for a concurrent CFAR on another stream (UWB_SAT_CTAS_PER_SM)
     if (const char* e = getenv("UWB_SAT_CTAS_PER_SM")) per_sm = std::min(per_sm, std::max(1, atoi(e)));
     const int64_t ctas = (n_tiles + kWarpsPerCta - 1) / kWarpsPerCta;
@@ -490,36 +504,24 @@ static cudaError_t launch_sat_t(const SatLaunch& L, cudaStream_t stream) {
         const cudaError_t me = cudaMemsetAsync(L.gedge, 0xff, sizeof(double) * L.n_jobs * L.strips * L.edge_stride, stream);
         if (me != cudaSuccess) return me;
     }
-    static unsigned long long* trace = nullptr;
-    const char* trace_file = getenv("UWB_SAT_TRACE");
-    if (trace_file) {
-        if (!trace) cudaMalloc(&trace, sizeof(unsigned long long) * 40 * 65536);
-        if (n_tiles <= 65536) L2.trace = trace;
-    }
     ++g_kernel_launches;
-    sat_systolic_kernel<T, kCpl><<<static_cast<unsigned>(grid), kWarpsPerCta * kWarp, smem, stream>>>(L2);
-    if (L2.trace) { // debug dump: tile, 8 timestamps (ns)
-        std::vector<unsigned long long> h(40 * n_tiles);
-        cudaMemcpyAsync(h.data(), trace, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, stream);
-        cudaStreamSynchronize(stream);
-        if (FILE* f = fopen(trace_file, "w")) {
-            for (int64_t t = 0; t < n_tiles; ++t) {
-                fprintf(f, "%lld", static_cast<long long>(t));
-                for (int k = 0; k < 40; ++k) fprintf(f, " %llu", h[40 * t + k]);
-                fprintf(f, "\n");
-            }
-            fclose(f);
-        }
-    }
+    kern<<<static_cast<unsigned>(grid), kWarpsPerCta * kWarp, smem, stream>>>(L2);
     return cudaGetLastError();
 }
 
 template <typename T>
 static cudaError_t launch_sat_cpl(const SatLaunch& L, cudaStream_t stream) {
+    if (L.need) {
+        switch (L.cpl) {
+            case 1: return launch_sat_t<T, 1, true>(L, stream);
+            case 2: return launch_sat_t<T, 2, true>(L, stream);
+            default: return launch_sat_t<T, 4, true>(L, stream);
+        }
+    }
     switch (L.cpl) {
-        case 1: return launch_sat_t<T, 1>(L, stream);
-        case 2: return launch_sat_t<T, 2>(L, stream);
-        default: return launch_sat_t<T, 4>(L, stream);
+        case 1: return launch_sat_t<T, 1, false>(L, stream);
+        case 2: return launch_sat_t<T, 2, false>(L, stream);
+        default: return launch_sat_t<T, 4, false>(L, stream);
     }
 }
 
