@@ -17,7 +17,7 @@ def _run(uwb, maps, p, per_cell, fused, cap=1 << 14):
     n, R, C = maps.shape
     b = BatchCfar(n, R, C, p, maps.dtype, det_capacity=cap, want_mask_u8=per_cell, want_thresholds=per_cell)
     k0 = kernel_launches()
-    b(maps, fused=fused)
+    b(maps, fused=fused, exact=not fused)  # the exact two-kernel path, not the certified one
     torch.cuda.synchronize()
     return b, kernel_launches() - k0
 
