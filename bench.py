@@ -46,6 +46,9 @@ WORKLOAD = ("cfg3: 4096 fp32 maps 1024x1024, Exp(1) + 32 targets/map at U(8,20) 
 SAT_BYTES_PER_CELL = 4 + 8        # read fp32 cell, write fp64 table entry
 CFAR_BYTES_PER_CELL = 8 + 4 + 1 / 8  # read table entry + CUT, write mask bit
 FUSED_BYTES_PER_CELL = 4 + 1 / 8     # fused SAT+CFAR: read fp32 cell once, write mask bit
+CERT_BYTES_PER_CELL = 4              # certify: read fp32 cell once (candidates ~1e-4 of cells)
+SPARSE_SAT_BYTES_PER_CELL = 4        # sparse SAT: read fp32 cell once (writes ~8 taps x 32 B per candidate)
+RESOLVE_BYTES_PER_CELL = 1 / 8       # resolve: mask bit per cell (taps and lists ~Pfa of the cells)
 
 
 def _peaks():
@@ -146,13 +149,10 @@ def _init_rank(world: int, local: int):
 
 
 def _shard(world: int, rank: int):
-    """Contiguous blocks of 64-map chunks per rank (maps are independent units)."""
-    chunks = N_MAPS // CHUNK
-    per = chunks // world
-    extra = chunks % world
-    c0 = rank * per + min(rank, extra)
-    c1 = c0 + per + (1 if rank < extra else 0)
-    return c0 * CHUNK, c1 * CHUNK
+    """Contiguous blocks of 64-map chunks per rank (maps are independent units;
+    shard.map_shard)."""
+    from paper_2012_11077_b200.shard import map_shard
+    return map_shard(N_MAPS, world, rank, block=CHUNK)
 
 
 def _generate(m0: int, m1: int, device):
@@ -200,35 +200,63 @@ def reference_cells_per_s(maps_host, budget_s: float = 12.0, max_maps: int = 512
                           "detections": int(counts.sum())}
 
 
+def _load_synth():
+    """The seeded generators (paper_2012_11077_b200/synth.py, torch only) loaded
+    by path, so the reference arm never imports the product package (whose
+    __init__ loads libuwbvital_b200.so)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_uwb_synth_standalone", os.path.join(ROOT, "paper_2012_11077_b200", "synth.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+REF_MAPS_PER_STEP = 512
+
+
 def run_reference(args):
+    """The reference's own CPU path (oracle/_ref = /root/reference/proj/src
+    compiled unchanged): cfar2d_integral per map, map-parallel on every host
+    thread (SURVEY 8d way ii), on a bounded sample of config 3 per step. Also
+    reports, once, way (i): one map at a time with the reference's own row
+    split over all threads (cfar.cpp:142-161)."""
     world, rank, _ = _dist()
     if rank != 0:
         return 0
     import numpy as np
-    import torch
-    from paper_2012_11077_b200 import synth
-    cores = _cpu_threads()
-    # bounded sample per step: ~2 maps per host thread (whole maps, threads=1 each)
-    n = max(8, min(N_MAPS, 2 * cores))
-    maps = synth.cfg3_maps(n, seed=SEED, device="cpu").numpy()
+    synth = _load_synth()
     from oracle.pyoracle import RefLib
+    cores = _cpu_threads()
+    n = max(cores, min(N_MAPS, REF_MAPS_PER_STEP))
+    maps = np.empty((n, ROWS, COLS), dtype=np.float32)
+    for c in range(0, n, CHUNK):  # the same generator blocks as the device arm's first maps
+        k = min(CHUNK, n - c)
+        maps[c:c + k] = synth.cfg3_maps(CHUNK, seed=SEED * 1_000_003 + c // CHUNK, device="cpu")[:k].numpy()
     ref = RefLib()
     for _ in range(args.warmup):
         ref.time_cfar_batch(maps[:cores], GUARD, TRAIN, PFA, cores)
     times = []
     for _ in range(args.steps):
-        secs, _ = ref.time_cfar_batch(maps, GUARD, TRAIN, PFA, cores)
+        secs, counts = ref.time_cfar_batch(maps, GUARD, TRAIN, PFA, cores)
         times.append(secs)
     step = statistics.mean(times)
     value = n * ROWS * COLS / step / 1e9
+    k_rows = min(8, n)
+    secs_rows, _ = ref.time_cfar_batch(maps[:k_rows], GUARD, TRAIN, PFA, 1, cores)
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": max(world, args.gpus),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, config 3)",
-        "config": {"workload": WORKLOAD, "sample_maps_per_step": n, "parallelism": f"{cores} host threads"},
+        "config": {"workload": WORKLOAD, "sample_maps_per_step": n, "parallelism": f"{cores} host threads",
+                   "detections_per_step": int(counts.sum())},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
-                         "sample": f"{n} config-3 maps per step, uwbvital_ref::cfar2d_integral(map, params, 1) "
-                                   f"map-parallel on {cores} threads ({_cpu_name()})"},
+                         "sample": f"{n} config-3 maps per step (the device arm's maps 0..{n - 1}), "
+                                   f"uwbvital_ref::cfar2d_integral(map, params, 1) map-parallel on {cores} threads "
+                                   f"({_cpu_name()})",
+                         "row_split_value": k_rows * ROWS * COLS / secs_rows / 1e9,
+                         "row_split_sample": f"{k_rows} maps one at a time, cfar2d_integral(map, params, {cores}) "
+                                             f"(the reference's own row split, cfar.cpp:142-161)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -250,7 +278,7 @@ def run_b200(args):
     import torch
     import torch.distributed as dist
     import paper_2012_11077_b200 as uwb
-    from paper_2012_11077_b200.batch import BatchCfar, host_cfar2d_batch, kernel_launches, phase_ms
+    from paper_2012_11077_b200.batch import BatchCfar, host_cfar2d_batch, kernel_launches, phase_ms4
 
     world, rank, local = _dist()
     dev = _init_rank(world, local)
@@ -263,7 +291,7 @@ def run_b200(args):
     total_count = torch.zeros(1, dtype=torch.int64, device=dev)
 
     def step(phase=False):
-        runner(maps, phase_events=phase, fused=args.fused)
+        runner(maps, phase_events=phase, fused=args.fused, exact=args.exact)
         total_count.copy_(runner.counts.sum().view(1))
         if world > 1:
             dist.all_reduce(total_count)  # final detection-count reduce (NCCL)
@@ -276,7 +304,7 @@ def run_b200(args):
         step(phase=(i == args.warmup - 1))  # the last warm-up also creates the phase events
     torch.cuda.synchronize()
     runner.check_inputs()
-    phase_ms(1024)  # clear the ring
+    phase_ms4(1024)  # clear the ring
 
     sampler = ClockSampler(dev.index)
     sampler.start()
@@ -303,15 +331,26 @@ def run_b200(args):
     cells_total = N_MAPS * ROWS * COLS
     value = cells_total / (ms_per_step / 1e3) / 1e9
 
-    ph = phase_ms(1024)
-    sat_ms, cfar_ms, sort_ms = (float(np.mean(ph[:, i])) for i in range(3)) if len(ph) else (0.0, 0.0, 0.0)
+    ph = phase_ms4(1024)
+    cert_ms, sat_ms, cfar_ms, sort_ms = (float(np.mean(ph[:, i])) for i in range(4)) if len(ph) else (0.0,) * 4
     peak, peak_src = _peaks()
     cells_local = n_local * ROWS * COLS
+    certified = cert_ms > 0.02 * (sat_ms + cfar_ms + 1e-9) and not args.exact and not args.fused
     # whole-map batches run SAT + CFAR as one kernel (cfar_fused.cu); its phase
     # is "cfar" and the "sat" phase is empty
-    fused = cfar_ms > 0 and sat_ms < 0.02 * cfar_ms
+    fused = args.fused and cfar_ms > 0 and sat_ms < 0.02 * cfar_ms
     if fused:
         kernels = {"cfar_fused_kernel": (cfar_ms, FUSED_BYTES_PER_CELL * cells_local)}
+    elif certified:
+        # certified-decision path (DESIGN 4c): cert_kernel reads the map once
+        # (window sums of quantised cells -> candidate list), the SAT reads it
+        # again and stores only the candidates' taps, the resolve reads ~Pfa of
+        # the cells' taps; algorithmic bytes per cell = one map read per pass
+        kernels = {
+            "cert_kernel": (cert_ms, CERT_BYTES_PER_CELL * cells_local),
+            "sat_systolic_kernel(sparse)": (sat_ms, SPARSE_SAT_BYTES_PER_CELL * cells_local),
+            "cert_resolve_kernel": (cfar_ms, RESOLVE_BYTES_PER_CELL * cells_local),
+        }
     else:
         kernels = {
             "sat_systolic_kernel": (sat_ms, SAT_BYTES_PER_CELL * cells_local),
@@ -320,9 +359,11 @@ def run_b200(args):
     dom = max(kernels, key=lambda k: kernels[k][0])
     dom_ms, dom_bytes = kernels[dom]
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
+    step_bytes = sum(v[1] for v in kernels.values())
     ncu = _ncu_traffic() or {}
     traffic = ncu.get(dom, {}).get("dram_bytes_per_launch_per_map")
     traffic = traffic * n_local if traffic else None
+    traffic_src = ncu.get(dom, {}).get("source") if traffic else None
 
     # ---- end to end through the public host API: pinned host maps -> H2D -> SAT+CFAR+sort -> D2H
     e2e = None
@@ -370,24 +411,30 @@ def run_b200(args):
             "config": {"workload": WORKLOAD, "n_maps": N_MAPS, "rows": ROWS, "cols": COLS,
                        "input_dtype": "f32", "sat_mode": "global (bit-identical to the reference)",
                        "kernels": ("fused SAT+CFAR (flags bit 4)" if args.fused else
+                                   "certify (cert_kernel + cert_mark_kernel) + sparse SAT (sat_systolic_kernel) "
+                                   "+ resolve (cert_resolve_kernel) + sort" if certified else
                                    "SAT (sat_systolic_kernel) + CFAR (cfar_ws_kernel) + sort"),
+                       "decision": ("certified: cells whose exact-arithmetic lower bound of T exceeds the CUT "
+                                    "are decided without the table; the rest are resolved from exact fp64 SAT "
+                                    "taps (bit-identical to the reference)" if certified else "exact"),
                        "l2": "inputs 16 GiB per pass >> 126 MB L2 (no flush needed)",
                        "parallelism": f"dp{world} (maps sharded in 64-map blocks)",
                        "detections_per_step": int(total_count.item()) if world > 1 else
                        int(runner.counts.sum().item())},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "bytes_per_cell": (FUSED_BYTES_PER_CELL if fused else
-                                            SAT_BYTES_PER_CELL if dom.startswith("sat") else CFAR_BYTES_PER_CELL),
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "bytes_per_cell": dom_bytes / cells_local,
                          "launch_ms": dom_ms, "peak_source": peak_src,
                          **({"note": "fused SAT+CFAR: the table stays in shared memory, so HBM carries only "
                                      "the map read and the mask; the kernel is bound by the SAT wavefront "
                                      "(one dependent fp64 chain per 128-column band, 3 bands per SM), see "
                                      "DESIGN.md 4(e)"} if fused else {})},
-            "phases_ms": {"sat": sat_ms, "cfar": cfar_ms, "sort": sort_ms},
+            "phases_ms": {"certify": cert_ms, "sat": sat_ms, "cfar": cfar_ms, "sort": sort_ms},
+            # whole-step HBM fraction against the algorithmic bytes of the kernels above
+            "step_hbm_frac": step_bytes / (ms_per_step / 1e3) / 1e9 / peak,
             # HBM fraction the two-pass algorithm (table written and read back) would need for this time
-            "two_pass_hbm_frac": (SAT_BYTES_PER_CELL + CFAR_BYTES_PER_CELL) * cells_local
-                                 / ((sat_ms + cfar_ms) / 1e3) / 1e9 / peak if sat_ms + cfar_ms > 0 else None,
+            "two_pass_equiv_hbm_frac": (SAT_BYTES_PER_CELL + CFAR_BYTES_PER_CELL) * cells_local
+                                       / (ms_per_step / 1e3) / 1e9 / peak,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
@@ -397,6 +444,35 @@ def run_b200(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def _ensure_world(args):
+    """--gpus N is honoured: under torch.distributed.run WORLD_SIZE must equal N;
+    without it, N > 1 re-executes this command under torch.distributed.run (one
+    rank per GPU), after checking that N devices are visible. The reference arm
+    runs on the host cores (rank 0 only) and needs no ranks."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus < 1:
+        print(json.dumps({"error": f"--gpus {args.gpus} < 1"}), flush=True)
+        return 2
+    if args.impl == "reference" or world == args.gpus:
+        return None
+    if world != 1:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}), flush=True)
+        return 2
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus and os.environ.get("UWB_DIST_BACKEND", "nccl") == "nccl":
+        print(json.dumps({"error": f"--gpus {args.gpus} but only {have} CUDA device(s) visible"}), flush=True)
+        return 2
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
 
 
 def main():
@@ -411,12 +487,17 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--fused", action="store_true",
                     help="device path through the fused SAT+CFAR kernel (flags bit 4) instead of SAT + ring CFAR")
+    ap.add_argument("--exact", action="store_true",
+                    help="device path through the exact two-kernel path (full fp64 table + ring CFAR)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5, 6],
                     help="BASELINE.json configuration (3 = the headline line; 6 = the paper's Table I; "
                          "see bench_configs.py)")
     args = ap.parse_args()
     globals()["N_MAPS"] = args.maps
+    rc = _ensure_world(args)
+    if rc is not None:
+        return rc
     if args.config != 3:
         import bench_configs
         return bench_configs.run(args)

@@ -277,7 +277,10 @@ uint64_t uwb_dev_build_sat_workspace(const uwb_map_batch* batch);
 
 /* Host-buffer batched CFAR for the end-to-end path: maps in (pinned) host
  * memory are streamed through the device in chunks with copy/compute overlap;
- * mask bits, detection lists and counts come back to host buffers. */
+ * mask bits, detection lists and counts come back to host buffers. A map with
+ * a non-finite or negative cell fails the call with UWB_INPUT_ERROR and the
+ * message cfar2d_integral raises on that map (the first such map in batch
+ * order; sat.cpp:28-32 before cfar.cpp:85-92). */
 uwb_status uwb_host_cfar2d_batch(const uwb_map_batch* host_batch, const uwb_cfar_params* params,
                                  int32_t sat_mode, uint64_t slab_rows, uint32_t* mask_bits,
                                  uwb_detection* dets, uint64_t det_capacity,

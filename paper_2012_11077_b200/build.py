@@ -32,6 +32,10 @@ NVCC_FLAGS = [
     "-I" + INCLUDE,
 ]
 
+# tuning build for the scripts/ probes only: environment knobs (common.cuh UWB_KNOB)
+if os.environ.get("UWB_TUNING_KNOBS") == "1":
+    NVCC_FLAGS.append("-DUWB_TUNING_KNOBS")
+
 CAPI_SO = os.path.join(LIB, "libuwbvital_b200.so")
 DROPIN_SO = os.path.join(LIB, "libuwbvital.so")
 

@@ -195,7 +195,7 @@ Plan make_plan(const uwb_map_batch& b, const uwb_cfar_params* p, int sat_mode, u
     P.sat_cols = P.cols;
     if (((sat_mode == UWB_SAT_TILE && !win) || (win && win->col_bands)) && p && P.cols % 32 == 0) {
         int64_t bc = win ? static_cast<int64_t>(win->col_bands) : 1024;
-        if (const char* e = getenv("UWB_TILE_COLS"); e && !win) bc = atoll(e);
+        if (const char* e = UWB_KNOB("UWB_TILE_COLS"); e && !win) bc = atoll(e);
         bc = round_up(bc < 128 ? 128 : bc, 128);
         const int64_t hp = round_up(p->guard_cols + p->background_cols, 32);
         if (bc + 2 * hp < P.cols) {
@@ -371,7 +371,7 @@ CertLaunch cert_launch(const Plan& P, const uwb_map_batch& b, const uwb_cfar_par
     L.ties = o.ties;
     L.tie_cap = static_cast<int64_t>(o.tie_capacity);
     int range = 9; // certified values lie in [0, 2^range)
-    if (const char* e = getenv("UWB_CERT_RANGE_LOG2")) range = std::max(0, std::min(20, atoi(e)));
+    if (const char* e = UWB_KNOB("UWB_CERT_RANGE_LOG2")) range = std::max(0, std::min(20, atoi(e)));
     cert_prepare(L, range);
     return L;
 }
@@ -1261,6 +1261,15 @@ uwb_status uwb_host_cfar2d_batch(const uwb_map_batch* hb, const uwb_cfar_params*
         UWB_CUDA_TRY(sl.cnt.alloc(sizeof(uint64_t) * chunk, S.comp));
         UWB_CUDA_TRY(sl.bad.alloc(sizeof(uint64_t) * 2 * chunk, S.comp));
     }
+    // per-map first bad cells {non-finite, negative} (row-major index), read back
+    // with the counts and reported as the reference's InputError below
+    struct PinnedBad {
+        uint64_t* p = nullptr;
+        ~PinnedBad() {
+            if (p) cudaFreeHost(p);
+        }
+    } bad;
+    UWB_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&bad.p), sizeof(uint64_t) * 2 * hb->n_maps));
     UWB_CUDA_TRY(cudaStreamSynchronize(S.comp)); // allocations visible to the other streams
     uwb_status result = UWB_OK;
     for (uint64_t m0 = 0, k = 0; m0 < hb->n_maps; m0 += chunk, ++k) {
@@ -1296,10 +1305,24 @@ uwb_status uwb_host_cfar2d_batch(const uwb_map_batch* hb, const uwb_cfar_params*
             UWB_CUDA_TRY(cudaMemcpyAsync(dets + det_capacity * m0, sl.dets.p, sizeof(uwb_detection) * det_capacity * nm,
                                          cudaMemcpyDeviceToHost, S.out));
         UWB_CUDA_TRY(cudaMemcpyAsync(det_counts + m0, sl.cnt.p, sizeof(uint64_t) * nm, cudaMemcpyDeviceToHost, S.out));
+        UWB_CUDA_TRY(cudaMemcpyAsync(bad.p + 2 * m0, sl.bad.p, sizeof(uint64_t) * 2 * nm, cudaMemcpyDeviceToHost, S.out));
         UWB_CUDA_TRY(cudaEventRecord(S.drained[i], S.out));
     }
     UWB_CUDA_TRY(cudaStreamSynchronize(S.out));
     UWB_CUDA_TRY(cudaStreamSynchronize(S.comp));
+    // the first map with a bad cell raises what cfar2d_integral raises on it:
+    // build_sat's non-finite check first (sat.cpp:28-32), then run_cfar's
+    // power-map check (cfar.cpp:85-92); its outputs are not meaningful
+    for (uint64_t i = 0; i < hb->n_maps; ++i) {
+        const uint64_t nf = bad.p[2 * i], neg = bad.p[2 * i + 1];
+        if (nf == ~0ull && neg == ~0ull) continue;
+        const uint64_t idx = nf != ~0ull ? nf : neg;
+        const int64_t r = static_cast<int64_t>(idx / hb->cols), c = static_cast<int64_t>(idx % hb->cols);
+        if (nf != ~0ull)
+            return fail(UWB_INPUT_ERROR, "build_sat: non-finite entry at (" + S(r) + ", " + S(c) + ")", r, c);
+        return fail(UWB_INPUT_ERROR, "cfar2d: cell (" + S(r) + ", " + S(c) + ") is not a finite non-negative power",
+                    r, c);
+    }
     for (uint64_t i = 0; i < hb->n_maps; ++i)
         if (det_counts[i] > det_capacity) result = fail(UWB_CAPACITY_ERROR, "uwb_host_cfar2d_batch: detection buffer too small");
     return result ? result : ok();

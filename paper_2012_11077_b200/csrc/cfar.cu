@@ -358,7 +358,7 @@ cudaError_t launch_sort_detections(uwb_detection* dets, int64_t cap, const unsig
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (n_maps < sms && !getenv("UWB_SORT_ONE_CTA")) {
+        if (n_maps < sms && !UWB_KNOB("UWB_SORT_ONE_CTA")) {
             // few long lists (single large maps): every merge pass spreads each
             // list over many CTAs; an even number of passes ends in `dets`
             const int64_t tiles = (cap + kMergeTile - 1) / kMergeTile;

@@ -644,14 +644,14 @@ cudaError_t go_fused_occ(FusedLaunch F, cudaStream_t stream) {
     const int span_lanes = (kWarp + 2 * F.c.hc + 1 + kCpl - 1) / kCpl + 2;
     const int need = ((2 * F.c.hr + span_lanes + 14 + kRs - 1) / kRs + 1) * kRs;
     int pinned = 0;
-    if (const char* e = getenv("UWB_FUSED_OCC")) pinned = atoi(e);
+    if (const char* e = UWB_KNOB("UWB_FUSED_OCC")) pinned = atoi(e);
     for (int occ : {3, 2, 1}) {
         if (pinned && occ != pinned) continue;
         const size_t budget = static_cast<size_t>(233472 / occ - 1024);
         int nr = need;
         if (FusedSmem<T, kCpl>::bytes(nr) > budget) continue;
         while (FusedSmem<T, kCpl>::bytes(nr + kRs) <= budget && nr + kRs <= need + 64) nr += kRs;
-        if (const char* e = getenv("UWB_FUSED_RING")) nr = std::max(need, atoi(e) / kRs * kRs);
+        if (const char* e = UWB_KNOB("UWB_FUSED_RING")) nr = std::max(need, atoi(e) / kRs * kRs);
         F.nr = nr;
         switch (occ) {
             case 3: return go_fused<T, kCpl, 3>(F, stream);
@@ -676,7 +676,7 @@ cudaError_t go_fused_cpl(const FusedLaunch& F, cudaStream_t stream) {
 // Whole-map batches only (no row window / slabs). Returns cudaErrorNotSupported
 // when the geometry does not qualify (the caller runs SAT + CFAR instead).
 cudaError_t launch_cfar_fused(const SatLaunch& S, const CfarLaunch& C, int dtype, cudaStream_t stream) {
-    if (const char* e = getenv("UWB_FUSED"))
+    if (const char* e = UWB_KNOB("UWB_FUSED"))
         if (atoi(e) == 0) return cudaErrorNotSupported;
     const JobGeometry& g = C.geo;
     if (g.n_slabs != 1 || g.n_bands != 1 || g.row_lo != 0 || g.row_hi != g.rows || g.buf_row0 != 0 || g.buf_rows != g.rows)
@@ -697,7 +697,7 @@ cudaError_t launch_cfar_fused(const SatLaunch& S, const CfarLaunch& C, int dtype
     F.unit_counter = S.tile_counter;
     F.c.debug = 0;
 #ifdef UWB_PROBE_BUILD // timing probes only: skip the arithmetic (never in the release library)
-    if (const char* e = getenv("UWB_FUSED_DEBUG")) F.c.debug = static_cast<unsigned>(atoi(e));
+    if (const char* e = UWB_KNOB("UWB_FUSED_DEBUG")) F.c.debug = static_cast<unsigned>(atoi(e));
 #endif
     return dtype == UWB_F32 ? go_fused_cpl<float>(F, stream) : go_fused_cpl<double>(F, stream);
 }

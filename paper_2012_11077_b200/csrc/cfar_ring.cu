@@ -624,12 +624,12 @@ template <typename T, int NCW, int CPT, int BOXC, int SG, int OCC, int NGRP = 1>
 cudaError_t go(const CfarLaunch& L0, cudaStream_t stream) {
     CfarLaunch L = L0;
     L.sleep_ns = 20000;
-    if (const char* e = getenv("UWB_RING_SLEEP_NS")) L.sleep_ns = static_cast<unsigned>(atoi(e));
+    if (const char* e = UWB_KNOB("UWB_RING_SLEEP_NS")) L.sleep_ns = static_cast<unsigned>(atoi(e));
     L.pf_groups = kPfGroups;
-    if (const char* e = getenv("UWB_RING_PF")) L.pf_groups = atoi(e) > 0 ? atoi(e) : kPfGroups;
+    if (const char* e = UWB_KNOB("UWB_RING_PF")) L.pf_groups = atoi(e) > 0 ? atoi(e) : kPfGroups;
     L.debug = 0;
 #ifdef UWB_PROBE_BUILD // timing probes only: skip the arithmetic (never in the release library)
-    if (const char* e = getenv("UWB_RING_DEBUG")) L.debug = static_cast<unsigned>(atoi(e));
+    if (const char* e = UWB_KNOB("UWB_RING_DEBUG")) L.debug = static_cast<unsigned>(atoi(e));
 #endif
     L.col_tiles = (L.cols + kW - 1) / kW;
     // row chunks of kRingRows; a batch too small to give every SM two CTAs
@@ -643,8 +643,8 @@ cudaError_t go(const CfarLaunch& L0, cudaStream_t stream) {
     // (cfg 4: 1.62 -> 1.48 ms)
     L.ring_rows = 2 * L.hr + 1 > 48 ? 2 * kRingRows : kRingRows;
     auto ctas = [&](int64_t rr) { return L.col_tiles * ((L.geo.slab_rows + rr - 1) / rr) * L.n_jobs; };
-    if (const char* e = getenv("UWB_RING_ROWS")) L.ring_rows = atoi(e) > 0 ? atoi(e) : kRingRows;
-    while (L.ring_rows > 32 && ctas(L.ring_rows) < 2 * sms && !getenv("UWB_RING_FIXED_ROWS")) L.ring_rows /= 2;
+    if (const char* e = UWB_KNOB("UWB_RING_ROWS")) L.ring_rows = atoi(e) > 0 ? atoi(e) : kRingRows;
+    while (L.ring_rows > 32 && ctas(L.ring_rows) < 2 * sms && !UWB_KNOB("UWB_RING_FIXED_ROWS")) L.ring_rows /= 2;
     L.row_chunks = (L.geo.slab_rows + L.ring_rows - 1) / L.ring_rows;
     const int64_t n_maps = L.n_jobs / L.geo.n_slabs;
     CUtensorMap tmap_tab, tmap_cut;
@@ -674,7 +674,7 @@ cudaError_t go_occ(const CfarLaunch& L, cudaStream_t stream) {
     // the deepest look-ahead that still fits at that occupancy (measured: CTAs
     // per SM matter more than look-ahead). UWB_RING_OCC pins the occupancy.
     int occ = 0;
-    const int pinned = getenv("UWB_RING_OCC") ? atoi(getenv("UWB_RING_OCC")) : 0;
+    const int pinned = UWB_KNOB("UWB_RING_OCC") ? atoi(UWB_KNOB("UWB_RING_OCC")) : 0;
     auto fits = [&](int o, int ahead) {
         return ring_smem_bytes<T>(L.hr, BOXC, 1, ahead, cut_groups_for(o, sizeof(T))) <= static_cast<size_t>(233472 / o - 1024);
     };
@@ -696,7 +696,7 @@ cudaError_t go_occ(const CfarLaunch& L, cudaStream_t stream) {
         default:
             // one CTA per SM (tall windows): two consumer warp groups on alternate steps
             {
-                const char* e = getenv("UWB_RING_GROUPS");
+                const char* e = UWB_KNOB("UWB_RING_GROUPS");
                 const int ngrp = e ? atoi(e) : 2;
                 if (ngrp == 4) return go<T, 4, 1, BOXC, 1, 1, 4>(La, stream);
                 if (ngrp == 1) return go<T, 4, 1, BOXC, 1, 1>(La, stream);
@@ -720,7 +720,7 @@ cudaError_t go_cfg(const CfarLaunch& L, int boxc, cudaStream_t stream) {
 // Returns cudaErrorNotSupported when the rings do not fit or the layout does
 // not allow tensor copies (caller falls back to the simple kernel).
 cudaError_t launch_cfar_ring(const CfarLaunch& L, int dtype, cudaStream_t stream) {
-    if (getenv("UWB_CFAR_SIMPLE")) return cudaErrorNotSupported;
+    if (UWB_KNOB("UWB_CFAR_SIMPLE")) return cudaErrorNotSupported;
     if (L.geo.rows >= (int64_t(1) << 31) || L.cols >= (int64_t(1) << 30)) return cudaErrorNotSupported;
     const bool f32 = dtype == UWB_F32;
     const size_t esz = f32 ? 4 : 8;

@@ -12,6 +12,17 @@
 
 #include "uwbvital_b200.h"
 
+// Tuning knobs (ring depth, occupancy, chunking ...) read from the environment
+// exist only in a tuning build (-DUWB_TUNING_KNOBS, scripts/ probes); the
+// release library reads no environment variable, so nothing outside the call
+// arguments can change what a call computes or how.
+#ifdef UWB_TUNING_KNOBS
+#include <cstdlib>
+#define UWB_KNOB(name) std::getenv(name)
+#else
+#define UWB_KNOB(name) (static_cast<const char*>(nullptr))
+#endif
+
 namespace uwb {
 
 constexpr int kWarp = 32;

@@ -569,7 +569,7 @@ cudaError_t launch_fft_half(const FrontendLaunch& F, int half, dim3 grid, cudaSt
 // The fused front end (stats + fft1024) for the whole detect() front end;
 // cudaErrorNotSupported when the configuration needs the general kernels.
 cudaError_t launch_frontend_fused(const FrontendLaunch& F, cudaStream_t stream) {
-    if (const char* e = getenv("UWB_FE_FUSED"))
+    if (const char* e = UWB_KNOB("UWB_FE_FUSED"))
         if (atoi(e) == 0) return cudaErrorNotSupported;
     if (F.L != 1024 || F.n < 2 || F.n > 1024 || F.m < 3 || F.mode != 0 || F.full_power || !F.band || F.kept < 1 ||
         F.first_bin < 0 || F.first_bin + F.kept > F.L / 2 + 1 || F.window < 1 || (F.window & 1) == 0 ||

@@ -147,6 +147,16 @@ __device__ __forceinline__ void lds_out(unsigned addr, double (&v)[kCpl]) {
                          : "memory");
     }
 }
+// Edge hand-over stores: strong (relaxed, gpu scope) so that the next strip's
+// ld.relaxed.gpu polling is a race-free morally-strong pair under the PTX
+// memory model; each 8-byte element is single-copy atomic.
+__device__ __forceinline__ void st_edge(double* p, double v) {
+    asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_edge2(double* p, double a, double b) {
+    asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+}
+
 __device__ __forceinline__ double lds_d(unsigned addr) {
     double v;
     asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
@@ -381,10 +391,10 @@ sat_systolic_kernel(SatLaunch L) {
                     // a non-finite input, which the call reports as an error
                     const double e_new = canon_edge(sv[kCpl - 1]), e_prev = canon_edge(prev[kCpl - 1]);
                     if (kChecked) {
-                        ge_out[r] = e_new;
-                        if (u == 0 && r >= 1) ge_out[r - 1] = e_prev; // row a fast block left unstored
+                        st_edge(ge_out + r, e_new);
+                        if (u == 0 && r >= 1) st_edge(ge_out + r - 1, e_prev); // row a fast block left unstored
                     } else if ((u & 1) == 0 && (!kFirst || r >= 1)) { // r = s - 31 is odd
-                        *reinterpret_cast<double2*>(ge_out + r - 1) = make_double2(e_prev, e_new);
+                        st_edge2(ge_out + r - 1, e_prev, e_new);
                     }
                 }
                 left_prev = left;
@@ -486,7 +496,7 @@ static cudaError_t launch_sat_t(const SatLaunch& L, cudaStream_t stream) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarpsPerCta * kWarp, smem);
     // leave room for a concurrent CFAR on another stream (UWB_SAT_CTAS_PER_SM)
-    if (const char* e = getenv("UWB_SAT_CTAS_PER_SM")) per_sm = std::min(per_sm, std::max(1, atoi(e)));
+    if (const char* e = UWB_KNOB("UWB_SAT_CTAS_PER_SM")) per_sm = std::min(per_sm, std::max(1, atoi(e)));
     const int64_t ctas = (n_tiles + kWarpsPerCta - 1) / kWarpsPerCta;
     int64_t grid = imin(ctas, static_cast<int64_t>(sms) * (per_sm > 0 ? per_sm : 1));
     SatLaunch L2 = L;
@@ -494,11 +504,11 @@ static cudaError_t launch_sat_t(const SatLaunch& L, cudaStream_t stream) {
     if (n_tiles < 2LL * sms * (per_sm > 0 ? per_sm : 1) * kWarpsPerCta) L2.flags |= 2u;
     // at most one strip per SM: each strip gets an SM to itself
     if (n_tiles <= sms) L2.flags |= 8u;
-    if (const char* f = getenv("UWB_SAT_FLAGS")) L2.flags = static_cast<unsigned>(atoi(f));
+    if (const char* f = UWB_KNOB("UWB_SAT_FLAGS")) L2.flags = static_cast<unsigned>(atoi(f));
     // low-latency chains hand edges over through sentinel-initialised values
     // (and, one strip per SM, fetch each block's left edge at the end of the
     // previous block: 32 steps less lag per strip, measured 6% faster on 128 strips)
-    if ((L2.flags & 2u) && L.strips > 1 && !getenv("UWB_SAT_FLAGS")) L2.flags |= (L2.flags & 8u) ? 48u : 16u;
+    if ((L2.flags & 2u) && L.strips > 1 && !UWB_KNOB("UWB_SAT_FLAGS")) L2.flags |= (L2.flags & 8u) ? 48u : 16u;
     if (L2.flags & 8u) grid = imin(n_tiles, sms);
     if ((L2.flags & 16u) && L.strips > 1) {
         const cudaError_t me = cudaMemsetAsync(L.gedge, 0xff, sizeof(double) * L.n_jobs * L.strips * L.edge_stride, stream);
@@ -543,7 +553,7 @@ cudaError_t launch_sat(const SatLaunch& L, int dtype, cudaStream_t stream) {
 int sat_cpl_for(int64_t n_jobs, int64_t cols) {
     (void)n_jobs;
     (void)cols;
-    if (const char* e = getenv("UWB_SAT_CPL")) {
+    if (const char* e = UWB_KNOB("UWB_SAT_CPL")) {
         const int c = atoi(e);
         if (c == 1 || c == 2 || c == 4) return c;
     }

@@ -171,6 +171,38 @@ def test_host_batch_e2e_matches_device_batch(uwb, cuda):
         assert torch.equal(dets[i, :k], b.dets[i, :k].cpu())
 
 
+@pytest.mark.parametrize("bad", ["nan", "inf", "neg", "nan_after_neg"])
+def test_host_batch_rejects_bad_cells(uwb, cuda, bad):
+    """uwb_host_cfar2d_batch raises what cfar2d_integral raises on the first bad
+    map: build_sat's non-finite check (sat.cpp:28-32) before run_cfar's
+    negative-power check (cfar.cpp:85-92), at the first row-major cell."""
+    from paper_2012_11077_b200.batch import host_cfar2d_batch
+    n, R, Cc = 5, 64, 96
+    maps = torch.rand((n, R, Cc), dtype=torch.float32) + 0.1
+    if bad == "nan":
+        maps[3, 10, 11] = float("nan")
+        maps[4, 1, 1] = float("nan")
+        msg = "build_sat: non-finite entry at (10, 11)"
+    elif bad == "inf":
+        maps[2, 0, 95] = float("inf")
+        msg = "build_sat: non-finite entry at (0, 95)"
+    elif bad == "neg":
+        maps[1, 63, 2] = -1.0
+        maps[1, 63, 5] = -2.0
+        msg = "cfar2d: cell (63, 2) is not a finite non-negative power"
+    else:
+        maps[2, 0, 0] = -1.0
+        maps[2, 9, 9] = float("nan")
+        msg = "build_sat: non-finite entry at (9, 9)"
+    host_in = maps.pin_memory()
+    bits = torch.zeros((n, R, 3), dtype=torch.int32).pin_memory()
+    dets = torch.zeros((n, 64, 32), dtype=torch.uint8).pin_memory()
+    counts = torch.zeros(n, dtype=torch.int64).pin_memory()
+    with pytest.raises(uwb.InputError) as e:
+        host_cfar2d_batch(host_in, uwb.CfarParams(1, 4, 1e-3), bits, dets, counts, 64, maps_per_chunk=2)
+    assert str(e.value) == msg
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_row_window_ranks_vs_restatement(uwb, oracle, cuda, world):
     """Config 4 sharded by rows: each "rank" holds only its owned rows
