@@ -233,7 +233,10 @@ uint64_t uwb_dev_cfar2d_workspace(const uwb_map_batch* batch, const uwb_cfar_par
  *   every cell below T against an a-priori bound of the reference's table
  *   rounding, the SAT stores only the taps of the remaining candidates, and
  *   those are decided exactly. Results are identical to the exact path; a call
- *   that should leave its tables for a later bit-2 call must set bit 6. */
+ *   that should leave its tables for a later bit-2 call must set bit 6.
+ * flags bit 7 (test hook): the certified path's SAT writes whole tables.
+ * flags bit 8 (test hook): the exact ring CFAR keeps 256-row chunks for small
+ *   batches. Bits 7 and 8 change the schedule only, never the results. */
 uwb_status uwb_dev_cfar2d(const uwb_map_batch* batch, const uwb_cfar_params* params,
                           const double* alpha_dev, int32_t sat_mode, uint64_t slab_rows,
                           const uwb_cfar_outputs* out, void* workspace, uint64_t workspace_bytes,
@@ -295,7 +298,9 @@ uwb_status uwb_host_cfar2d_batch(const uwb_map_batch* host_batch, const uwb_cfar
  * the reference's messages before any work; per-record input errors go to
  * out->first_bad (entry 0: first non-finite frame sample, row-major). Query the
  * band width and workspace first (uwb_dev_detect_batch_workspace returns 0 for
- * a configuration error). */
+ * a configuration error). `flags` as uwb_dev_cfar2d for the CFAR (bits 2 and 8
+ * ignored there); bit 8 (test hook) runs the per-stage front-end kernels
+ * instead of the fused two-kernel front end (same results). */
 uint64_t uwb_dev_detect_batch_workspace(uint64_t n_records, uint64_t m, uint64_t n, double prf,
                                         const uwb_pipeline_config* cfg, uint64_t det_capacity);
 uwb_status uwb_dev_detect_batch(const void* records, int32_t dtype, uint64_t n_records, uint64_t m, uint64_t n,

@@ -132,26 +132,32 @@ class RefLib:
         return {"outer": tuple(o[0:4]), "guard": tuple(o[4:8]), "n_train": o[8]}
 
     def cfar2d(self, power_map, g: int, b: int, pfa: float, backend: str = "integral",
-               threads: int = 1) -> CfarResult:
+               threads: int = 1, det_cap: int | None = None, thresholds: bool = True) -> CfarResult:
+        """cfar2d_naive / cfar2d_integral (cfar.cpp:200-227). ``det_cap`` bounds
+        the exported list (default: every cell); ``thresholds=False`` skips the
+        threshold-map export (``threshold_map`` is then None)."""
         m = _f64(power_map)
         if m.ndim != 2:
             raise ValueError("2-D map required")
         rows, cols = m.shape
         cells = rows * cols
         mask = np.zeros((rows, cols), dtype=np.uint8)
-        thr = np.zeros((rows, cols), dtype=np.float64)
+        thr = np.zeros((rows, cols), dtype=np.float64) if thresholds else None
         n_det = C.c_uint64()
-        cap = cells
+        cap = cells if det_cap is None else int(det_cap)
         dr = np.zeros(max(cap, 1), np.uint64)
         dc = np.zeros(max(cap, 1), np.uint64)
         dv = np.zeros(max(cap, 1), np.float64)
         dt = np.zeros(max(cap, 1), np.float64)
         self._check(self.lib.uwbref_cfar2d(
             C.c_int(0 if backend == "naive" else 1), _p(m), C.c_uint64(rows), C.c_uint64(cols),
-            C.c_int(g), C.c_int(b), C.c_double(pfa), C.c_uint(threads), _p(mask), _p(thr),
+            C.c_int(g), C.c_int(b), C.c_double(pfa), C.c_uint(threads), _p(mask),
+            _p(thr) if thr is not None else None,
             C.byref(n_det), C.c_uint64(cap), _p(dr), _p(dc), _p(dv), _p(dt), self.err,
             C.c_uint64(1024)))
         n = n_det.value
+        if n > cap:
+            raise OracleError(9, f"{n} detections > det_cap {cap}")
         dets = np.zeros(n, dtype=DET_DTYPE)
         dets["row"], dets["col"], dets["value"], dets["threshold"] = dr[:n], dc[:n], dv[:n], dt[:n]
         return CfarResult(mask, thr, dets)
@@ -322,14 +328,15 @@ class OracleLib:
         return int(self.lib.uwbo_interior_train_count(C.byref(p)))
 
     def cfar(self, power_map, guard_rows, guard_cols, background_rows, background_cols, pfa,
-             backend="integral", row_begin=0, row_end=None, slab_local=False) -> CfarResult:
+             backend="integral", row_begin=0, row_end=None, slab_local=False,
+             det_cap: int | None = None) -> CfarResult:
         m = _f64(power_map)
         rows, cols = m.shape
         row_end = rows if row_end is None else row_end
         p = _Params(guard_rows, guard_cols, background_rows, background_cols, pfa)
         mask = np.zeros((rows, cols), np.uint8)
         thr = np.zeros((rows, cols))
-        cap = max(rows * cols, 1)
+        cap = max(rows * cols, 1) if det_cap is None else int(det_cap)
         dets = (_Det * cap)()
         n_det = C.c_size_t()
         br, bc = C.c_int64(-1), C.c_int64(-1)
@@ -341,6 +348,8 @@ class OracleLib:
         if code:
             raise OracleError(code, f"cell ({br.value}, {bc.value})")
         n = n_det.value
+        if n > cap:
+            raise OracleError(9, f"{n} detections > det_cap {cap}")
         arr = np.frombuffer(dets, dtype=DET_DTYPE, count=n).copy()
         return CfarResult(mask, thr, arr)
 

@@ -87,7 +87,7 @@ class BatchCfar:
 
     def __call__(self, maps: torch.Tensor, sort: bool = True, stream=None, phase_events: bool = False,
                  reuse_tables: bool = False, naive: bool = False, fused: bool = False,
-                 exact: bool = False, dense_tables: bool = False) -> None:
+                 exact: bool = False, dense_tables: bool = False, fixed_ring_rows: bool = False) -> None:
         """Launch SAT + CFAR (+ sort) for ``maps`` of shape (n_maps, rows, cols).
         ``phase_events`` records per-phase CUDA events (read with :func:`phase_ms`).
         ``reuse_tables`` skips the SAT: the (shared) workspace already holds the
@@ -97,7 +97,9 @@ class BatchCfar:
         (whole-map batches; no table is left for ``reuse_tables``).
         ``exact`` forces the two-kernel path (full table, then the ring CFAR)
         instead of the default certified-decision path; a call whose tables a
-        later ``reuse_tables`` call reads must pass it."""
+        later ``reuse_tables`` call reads must pass it. ``dense_tables`` and
+        ``fixed_ring_rows`` are test hooks that change the schedule, not the
+        results (full tables on the certified path; 256-row ring chunks)."""
         if maps.dtype != self.dtype or tuple(maps.shape) != (self.n_maps, self.rows, self.cols):
             raise ValueError(f"expected {(self.n_maps, self.rows, self.cols)} {self.dtype}, got "
                              f"{tuple(maps.shape)} {maps.dtype}")
@@ -105,7 +107,7 @@ class BatchCfar:
             raise ValueError("maps must be a contiguous CUDA tensor")
         self._batch.maps = maps.data_ptr()
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
-        flags = (0 if sort else 1) | (2 if phase_events else 0) | (4 if reuse_tables else 0) | (8 if naive else 0) | (16 if fused else 0) | (64 if exact else 0) | (128 if dense_tables else 0)
+        flags = (0 if sort else 1) | (2 if phase_events else 0) | (4 if reuse_tables else 0) | (8 if naive else 0) | (16 if fused else 0) | (64 if exact else 0) | (128 if dense_tables else 0) | (256 if fixed_ring_rows else 0)
         if self.window is None:
             st = N.lib.uwb_dev_cfar2d(C.byref(self._batch), C.byref(self._cparams), self.alpha.data_ptr(),
                                       self.sat_mode, C.c_uint64(self.slab_rows), C.byref(self._out),
@@ -194,7 +196,9 @@ class DetectBatch:
             self.mask_bits.data_ptr(), self.words_per_row, self.m * self.words_per_row, None, None,
             self.dets.data_ptr(), self.det_capacity, self.counts.data_ptr(), self.first_bad.data_ptr())
 
-    def __call__(self, records: torch.Tensor, stream=None) -> None:
+    def __call__(self, records: torch.Tensor, stream=None, general_kernels: bool = False) -> None:
+        """``general_kernels`` (test hook): the per-stage front-end kernels instead
+        of the fused two-kernel front end (same results)."""
         if records.dtype != self.dtype or tuple(records.shape) != (self.n_records, self.m, self.n):
             raise ValueError(f"expected {(self.n_records, self.m, self.n)} {self.dtype}")
         if not records.is_cuda or not records.is_contiguous():
@@ -204,7 +208,8 @@ class DetectBatch:
         raise_for(N.lib.uwb_dev_detect_batch(records.data_ptr(), _DT[self.dtype], self.n_records, self.m, self.n,
                                              C.c_double(self.fast_rate), C.c_double(self.prf), C.byref(self._cfg),
                                              self.band.data_ptr(), C.byref(kept), C.byref(self._out),
-                                             self.workspace.data_ptr(), C.c_uint64(self.workspace.numel()), 0,
+                                             self.workspace.data_ptr(), C.c_uint64(self.workspace.numel()),
+                                             256 if general_kernels else 0,
                                              C.c_void_p(s.cuda_stream)))
 
     def check_inputs(self) -> None:

@@ -467,7 +467,9 @@ uwb_status dev_cfar(const uwb_map_batch& b, const uwb_cfar_params& p, const doub
                 UWB_CUDA_TRY(run_sat(P, SL, b.dtype, s));
             }
             if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[2], s));
-            UWB_CUDA_TRY(launch_cfar_integral(cfar_launch(P, b, p, alpha, ws, o), b.dtype, s));
+            CfarLaunch FL = cfar_launch(P, b, p, alpha, ws, o);
+            FL.fixed_rows = (flags & 256u) != 0; // bit 8 (test hook): 256-row ring chunks, same results
+            UWB_CUDA_TRY(launch_cfar_integral(FL, b.dtype, s));
         }
     } else {
         if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[1], s));
@@ -1318,10 +1320,9 @@ uwb_status uwb_host_cfar2d_batch(const uwb_map_batch* hb, const uwb_cfar_params*
         if (nf == ~0ull && neg == ~0ull) continue;
         const uint64_t idx = nf != ~0ull ? nf : neg;
         const int64_t r = static_cast<int64_t>(idx / hb->cols), c = static_cast<int64_t>(idx % hb->cols);
-        if (nf != ~0ull)
-            return fail(UWB_INPUT_ERROR, "build_sat: non-finite entry at (" + S(r) + ", " + S(c) + ")", r, c);
-        return fail(UWB_INPUT_ERROR, "cfar2d: cell (" + S(r) + ", " + S(c) + ") is not a finite non-negative power",
-                    r, c);
+        const std::string at = "(" + std::to_string(r) + ", " + std::to_string(c) + ")";
+        if (nf != ~0ull) return fail(UWB_INPUT_ERROR, "build_sat: non-finite entry at " + at, r, c);
+        return fail(UWB_INPUT_ERROR, "cfar2d: cell " + at + " is not a finite non-negative power", r, c);
     }
     for (uint64_t i = 0; i < hb->n_maps; ++i)
         if (det_counts[i] > det_capacity) result = fail(UWB_CAPACITY_ERROR, "uwb_host_cfar2d_batch: detection buffer too small");
@@ -1424,7 +1425,8 @@ uwb_status uwb_dev_detect_batch(const void* records, int32_t dtype, uint64_t n_r
     F.first_bin = static_cast<int64_t>(D.first);
     F.kept = static_cast<int64_t>(D.kept);
     F.band = band;
-    const cudaError_t fused = launch_frontend_fused(F, s);
+    // flags bit 8 (test hook): the general front-end kernels (same results)
+    const cudaError_t fused = (flags & 256u) ? cudaErrorNotSupported : launch_frontend_fused(F, s);
     if (fused == cudaErrorNotSupported) {
         F.stage_mask = 3;
         UWB_CUDA_TRY(launch_frontend_columns(F, s));
@@ -1436,7 +1438,7 @@ uwb_status uwb_dev_detect_batch(const void* records, int32_t dtype, uint64_t n_r
     // CFAR over the band maps (pipeline.cpp:269-273)
     const int backend = cfg->backend == UWB_NAIVE ? UWB_NAIVE : UWB_INTEGRAL;
     if (uwb_status st = dev_cfar(b, cfg->cfar, d_alpha.as<double>(), backend, UWB_SAT_GLOBAL, 0, *out,
-                                 ws + off_cfar, P.total, flags & ~4u, s))
+                                 ws + off_cfar, P.total, flags & ~(4u | 256u), s))
         return st;
     // a record's first non-finite sample (row-major over its m x n frame) is its
     // entry 0 of first_bad (RadarFrame::validate, pipeline.cpp:27-38)

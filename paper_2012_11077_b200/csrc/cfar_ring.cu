@@ -644,7 +644,7 @@ cudaError_t go(const CfarLaunch& L0, cudaStream_t stream) {
     L.ring_rows = 2 * L.hr + 1 > 48 ? 2 * kRingRows : kRingRows;
     auto ctas = [&](int64_t rr) { return L.col_tiles * ((L.geo.slab_rows + rr - 1) / rr) * L.n_jobs; };
     if (const char* e = UWB_KNOB("UWB_RING_ROWS")) L.ring_rows = atoi(e) > 0 ? atoi(e) : kRingRows;
-    while (L.ring_rows > 32 && ctas(L.ring_rows) < 2 * sms && !UWB_KNOB("UWB_RING_FIXED_ROWS")) L.ring_rows /= 2;
+    while (L.ring_rows > 32 && ctas(L.ring_rows) < 2 * sms && !L.fixed_rows && !UWB_KNOB("UWB_RING_FIXED_ROWS")) L.ring_rows /= 2;
     L.row_chunks = (L.geo.slab_rows + L.ring_rows - 1) / L.ring_rows;
     const int64_t n_maps = L.n_jobs / L.geo.n_slabs;
     CUtensorMap tmap_tab, tmap_cut;
@@ -674,7 +674,8 @@ cudaError_t go_occ(const CfarLaunch& L, cudaStream_t stream) {
     // the deepest look-ahead that still fits at that occupancy (measured: CTAs
     // per SM matter more than look-ahead). UWB_RING_OCC pins the occupancy.
     int occ = 0;
-    const int pinned = UWB_KNOB("UWB_RING_OCC") ? atoi(UWB_KNOB("UWB_RING_OCC")) : 0;
+    const char* occ_knob = UWB_KNOB("UWB_RING_OCC");
+    const int pinned = occ_knob ? atoi(occ_knob) : 0;
     auto fits = [&](int o, int ahead) {
         return ring_smem_bytes<T>(L.hr, BOXC, 1, ahead, cut_groups_for(o, sizeof(T))) <= static_cast<size_t>(233472 / o - 1024);
     };

@@ -162,7 +162,8 @@ struct CfarLaunch {
     int64_t row_chunks;  // row chunks per job
     int64_t ring_rows;   // CFAR ring kernel: output rows per CTA (row chunk height)
     unsigned sleep_ns;   // barrier-wait suspend hint of the CFAR ring kernel (ns)
-    unsigned debug;      // bit 0: consumers skip the cell arithmetic (data-movement probe)
+    unsigned debug;      // bit 0: consumers skip the cell arithmetic (data-movement probe; tuning build only)
+    bool fixed_rows;     // CFAR ring: keep 256-row chunks for small batches (test hook, same results)
     int ring_ahead;      // CFAR ring: table groups of look-ahead beyond the window
     int pf_groups;       // CFAR ring: L2 prefetch distance of both streams (groups)
     int64_t col_tiles;

@@ -292,22 +292,16 @@ def test_ring_row_chunk_edges_bits_only(uwb, ref, cuda, rows, fixed):
     """The ring kernel's steady loop (taken only without per-cell outputs) on row
     counts whose last row chunk ends within the window of the bottom edge, with
     the adaptive (short) row chunks of small batches and with 256-row chunks
-    (UWB_RING_FIXED_ROWS): masks and detection lists equal the reference."""
-    import os
+    (flags bit 8): masks and detection lists equal the reference."""
     from paper_2012_11077_b200.batch import BatchCfar
     gen = torch.Generator(device="cuda").manual_seed(rows)
     n, C = 3, 520
     maps = torch.empty((n, rows, C), device=cuda, dtype=torch.float32).exponential_(1.0, generator=gen)
     maps[:, ::9, ::7] *= 30.0
     p = uwb.CfarParams(2, 8, 1e-2)
-    if fixed:
-        os.environ["UWB_RING_FIXED_ROWS"] = "1"
-    try:
-        b = BatchCfar(n, rows, C, p, torch.float32, det_capacity=1 << 14)
-        b(maps)
-        torch.cuda.synchronize()
-    finally:
-        os.environ.pop("UWB_RING_FIXED_ROWS", None)
+    b = BatchCfar(n, rows, C, p, torch.float32, det_capacity=1 << 14)
+    b(maps, exact=True, fixed_ring_rows=fixed)
+    torch.cuda.synchronize()
     host = maps.double().cpu().numpy()
     for i in range(n):
         exp = ref.cfar2d(host[i], 2, 8, 1e-2, "integral")

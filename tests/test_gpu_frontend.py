@@ -261,8 +261,7 @@ def test_detect_batch_reports_nonfinite_record(uwb, cuda):
 def test_fused_front_end_matches_reference(uwb, ref, cuda, m, n, window, band, dtype):
     """The fused L = 1024 front end (column statistics + one-warp-per-row FFT,
     csrc/frontend.cu) against the reference detect() per record, bit for bit,
-    and against the general kernels (UWB_FE_FUSED=0)."""
-    import os
+    and against the general kernels (flags bit 8)."""
     import torch
     from paper_2012_11077_b200.batch import DetectBatch
     g = torch.Generator(device="cuda").manual_seed(m * 1000 + n)
@@ -274,16 +273,12 @@ def test_fused_front_end_matches_reference(uwb, ref, cuda, m, n, window, band, d
     config = uwb.PipelineConfig(mean_filter_window=window, fft_length=1024, band_low_hz=band[0],
                                 band_high_hz=band[1], cfar=cfar)
     outs = []
-    for fused in ("1", "0"):
-        os.environ["UWB_FE_FUSED"] = fused
-        try:
-            db = DetectBatch(3, m, n, config, prf=20.0, dtype=recs.dtype, det_capacity=1 << 14)
-            db(recs)
-            torch.cuda.synchronize()
-            db.check_inputs()
-            outs.append((db.band.cpu().numpy().copy(), [db.mask(i) for i in range(3)]))
-        finally:
-            os.environ.pop("UWB_FE_FUSED", None)
+    for general in (False, True):
+        db = DetectBatch(3, m, n, config, prf=20.0, dtype=recs.dtype, det_capacity=1 << 14)
+        db(recs, general_kernels=general)
+        torch.cuda.synchronize()
+        db.check_inputs()
+        outs.append((db.band.cpu().numpy().copy(), [db.mask(i) for i in range(3)]))
     assert_bitwise(outs[0][0], outs[1][0], "fused vs general band maps")
     host = recs.double().cpu().numpy()
     for i in range(3):
