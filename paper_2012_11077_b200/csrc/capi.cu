@@ -337,6 +337,7 @@ CertLaunch cert_launch(const Plan& P, const uwb_map_batch& b, const uwb_cfar_par
                        char* ws, const uwb_cfar_outputs& o) {
     CertLaunch L{};
     L.maps = b.maps;
+    L.elem_bytes = b.dtype == UWB_F32 ? 4 : 8;
     L.ld = static_cast<int64_t>(b.ld);
     L.map_stride = static_cast<int64_t>(b.map_stride);
     L.cols = P.cols;
@@ -422,14 +423,14 @@ uwb_status dev_cfar(const uwb_map_batch& b, const uwb_cfar_params& p, const doub
         UWB_CUDA_TRY(cudaMemset2DAsync(o.mask_bits, sizeof(uint32_t) * o.mask_map_stride, 0,
                                        sizeof(uint32_t) * o.words_per_row * P.geo.out_rows(), b.n_maps, s));
         UWB_CUDA_TRY(launch_cert_table(CL, const_cast<float4*>(CL.ke), static_cast<int>(P.n_int), s));
-        UWB_CUDA_TRY(launch_cert(CL, b.dtype, s));
-        UWB_CUDA_TRY(launch_cert_mark(CL, s));
-        if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[1], s));
         SatLaunch SL = sat_launch(P, b, ws, reinterpret_cast<unsigned long long*>(o.first_bad));
         SL.need = (flags & 128u) ? nullptr : CL.need; // bit 7 (test hook): full tables, same results
         SL.need_rows = P.need_rows;
         SL.map_full = CL.status;
         SL.jobs_per_map = P.geo.n_slabs * P.geo.n_bands;
+        UWB_CUDA_TRY(launch_cert(CL, b.dtype, s));
+        UWB_CUDA_TRY(launch_cert_mark(CL, s));
+        if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[1], s));
         UWB_CUDA_TRY(run_sat(P, SL, b.dtype, s));
         if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[2], s));
         UWB_CUDA_TRY(launch_cert_resolve(CL, b.dtype, s));

@@ -174,6 +174,7 @@ struct CfarLaunch {
 // certify, mark and resolve kernels.
 struct CertLaunch {
     const void* maps;
+    int elem_bytes;
     int64_t ld, map_stride, cols;
     JobGeometry geo;     // the CFAR call's geometry (slabs / bands of the tables)
     int64_t n_maps;

@@ -54,6 +54,8 @@ constexpr int kOSlots = 8;              // lane-private result delay ring (rows)
 constexpr int kPublishEvery = 64;       // steps between edge hand-overs
 constexpr int kL2Ahead = 48;            // sparse mode: L2 prefetch distance (rows)
 constexpr int kSatCtasPerSm = 3;        // occupancy target (registers and shared memory)
+constexpr int kSatCtasPerSmSparse = 4;  // sparse mode: no result ring, <= 128 registers
+constexpr int kSatCtasPerSmSparseRun = 3; // ... of which 3 resident: measured 3.5% faster than 4 (cfg 3)
 #ifndef UWB_POLL_SLEEP_NS
 #define UWB_POLL_SLEEP_NS 200
 #endif
@@ -61,14 +63,14 @@ constexpr unsigned kPollSleepNs = UWB_POLL_SLEEP_NS; // back-off between edge po
 
 // Shared memory per CTA: the warps' source rings, the result rings and the
 // edge staging.
-template <typename T, int kCpl>
+template <typename T, int kCpl, bool kSparse = false>
 struct SatSmem {
     static constexpr unsigned kXLane = kCpl * sizeof(T);              // source bytes per lane and row
     static constexpr unsigned kXSlotBytes = kWarp * kXLane;
     static constexpr unsigned kXRing = kXSlots * kXSlotBytes;        // 8 KB (f32) / 16 KB (f64)
     static constexpr unsigned kOLane = kCpl * sizeof(double);
     static constexpr unsigned kOSlotBytes = kWarp * kOLane;
-    static constexpr unsigned kORing = kOSlots * kOSlotBytes;        // 8 KB
+    static constexpr unsigned kORing = kSparse ? 0u : kOSlots * kOSlotBytes; // 8 KB (none when sparse)
     static constexpr size_t bytes() {
         return 16 /* alignment slack */ + kWarpsPerCta * (kXRing + kORing + kWarp * sizeof(double));
     }
@@ -180,11 +182,11 @@ __device__ __noinline__ void publish_rows(unsigned* prog, int rows_done, int lan
 // recurrence, but only the table segments marked in the tap bitmap are stored,
 // straight from registers (no delay ring, no zero row / column).
 template <typename T, int kCpl, bool kSparse>
-__global__ void __launch_bounds__(kWarpsPerCta * kWarp, kSatCtasPerSm)
+__global__ void __launch_bounds__(kWarpsPerCta * kWarp, kSparse ? kSatCtasPerSmSparse : kSatCtasPerSm)
 sat_systolic_kernel(SatLaunch L) {
     constexpr int kStripCols = kCpl * kWarp;
     extern __shared__ __align__(16) unsigned char sat_smem_raw[];
-    using SM = SatSmem<T, kCpl>;
+    using SM = SatSmem<T, kCpl, kSparse>;
     constexpr unsigned kXSlotBytes = SM::kXSlotBytes;
     constexpr unsigned kOSlotBytes = SM::kOSlotBytes;
     const int warp = threadIdx.x / kWarp;
@@ -224,6 +226,10 @@ sat_systolic_kernel(SatLaunch L) {
         const unsigned* need_col = kSparse ? L.need + (job * L.strips + strip) * L.need_rows : nullptr;
         const bool store_all = kSparse && L.map_full && L.map_full[job / L.jobs_per_map] != 0;
         const bool dense = !kSparse || store_all;
+        // sparse mode: need words of the previous / current / next block of rows
+        // (lane j: row base + j), fetched one block ahead so no step waits on them
+        unsigned need_prev = 0u, need_cur = 0u, need_next = 0u;
+        if (kSparse && !store_all && lane < J.rows) need_next = __ldg(need_col + lane);
         if (dense) {
             for (int k = 0; k < nvalid; ++k) table[kTabShift + 1 + c + k] = 0.0; // padded row 0 is zero
             if (strip == 0 && lane == 0) table[kTabShift] = 0.0;
@@ -383,6 +389,13 @@ sat_systolic_kernel(SatLaunch L) {
             sv[0] = dsub(dadd(dadd(widen(x[0]), prev[0]), left), left_prev);
 #pragma unroll
             for (int k = 1; k < kCpl; ++k) sv[k] = dsub(dadd(dadd(widen(x[k]), prev[k]), sv[k - 1]), prev[k - 1]);
+            // sparse mode: need word of row r = s0 + u - lane from the block's words
+            // (lane j holds rows s0 + j and s0 - 32 + j; see the block loop),
+            // shuffled while the warp is converged
+            unsigned w_need = 0u;
+            (void)w_need;
+            if constexpr (kSparse)
+                w_need = __shfl_sync(0xffffffffu, lane <= u ? need_cur : need_prev, (u - lane) & (kWarp - 1));
             const bool act = !kChecked || (r >= 0 && r < rows);
             if (act) {
                 // (6) edge column for the strip to the right (two rows per 16-byte store)
@@ -404,7 +417,7 @@ sat_systolic_kernel(SatLaunch L) {
                     sts_out<kCpl>(o_lane + ((static_cast<unsigned>(u) + o_rbase_lane) & (kOSlots - 1)) * kOSlotBytes, sv);
                 } else if (!kFirst || r >= 0) {
                     // marked taps of row r: S(r, c..c+kCpl-1) = padded (r+1, c+1..)
-                    const unsigned w = store_all ? ~0u : __ldg(need_col + r);
+                    const unsigned w = store_all ? ~0u : w_need;
                     if ((w >> lane) & 1u) {
                         double* dst = table + static_cast<int64_t>(r + 1) * tld + kTabShift + 1 + c;
                         if (kCpl >= 2 && nvalid == kCpl) {
@@ -433,6 +446,12 @@ sat_systolic_kernel(SatLaunch L) {
         cp_async_wait<kAhead - 1>();
         lds_lane<kCpl>(x_lane + (x_rbase_lane & (kXSlots - 1)) * kXSlotBytes, xn);
         for (int s0 = 0; s0 < steps; s0 += kWarp) {
+            if constexpr (kSparse) {
+                need_prev = need_cur;
+                need_cur = need_next;
+                const int rn = s0 + kWarp + lane;
+                need_next = (!store_all && rn < rows) ? __ldg(need_col + rn) : 0u;
+            }
             // left-strip edge values for rows [s0, s0 + 32) (lane 0 reads row s at step s)
             __syncwarp();
             asm volatile("st.shared.f64 [%0], %1;" ::"r"(edge_smem + 8u * lane), "d"(e_cur) : "memory");
@@ -487,7 +506,7 @@ sat_systolic_kernel(SatLaunch L) {
 template <typename T, int kCpl, bool kSparse>
 static cudaError_t launch_sat_t(const SatLaunch& L, cudaStream_t stream) {
     const int64_t n_tiles = L.n_jobs * L.strips;
-    const size_t smem = SatSmem<T, kCpl>::bytes();
+    const size_t smem = SatSmem<T, kCpl, kSparse>::bytes();
     auto kern = sat_systolic_kernel<T, kCpl, kSparse>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
@@ -496,6 +515,7 @@ static cudaError_t launch_sat_t(const SatLaunch& L, cudaStream_t stream) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarpsPerCta * kWarp, smem);
     // leave room for a concurrent CFAR on another stream (UWB_SAT_CTAS_PER_SM)
+    if (kSparse) per_sm = std::min(per_sm, kSatCtasPerSmSparseRun);
     if (const char* e = UWB_KNOB("UWB_SAT_CTAS_PER_SM")) per_sm = std::min(per_sm, std::max(1, atoi(e)));
     const int64_t ctas = (n_tiles + kWarpsPerCta - 1) / kWarpsPerCta;
     int64_t grid = imin(ctas, static_cast<int64_t>(sms) * (per_sm > 0 ? per_sm : 1));

@@ -190,3 +190,31 @@ def test_odd_width_runs_exact_path(uwb, cuda):
     exact(maps, exact=True)
     torch.cuda.synchronize()
     _same(cert, exact, 3, "odd width", expect_status=-1)
+
+
+def test_large_batch_with_fallback_maps_equals_exact(uwb, cuda):
+    """A 1200-map batch gives exactly the exact path's results, with a map the
+    certificate cannot cover (a value >= 2^9: exact fallback inside the same
+    call) in the middle of the batch, and reports a non-finite cell of a later
+    map as the reference's InputError."""
+    from paper_2012_11077_b200 import synth
+    n, R, C = 1200, 256, 1024
+    gen = torch.Generator(device="cuda").manual_seed(77)
+    maps = torch.empty((n, R, C), device=cuda, dtype=torch.float32).exponential_(1.0, generator=gen)
+    maps[:, 100, 500] += 40.0
+    maps[700, 10, 10] = 1000.0        # outside the certified range: exact fallback for map 700
+    p = uwb.CfarParams(2, 8, 1e-4)
+    cert, exact = _pair(n, R, C, p, det_capacity=256)
+    cert(maps)
+    exact(maps, exact=True)
+    torch.cuda.synchronize()
+    st = cert.cert_status.cpu().numpy()
+    assert st[700] != 0 and (np.delete(st, 700) == 0).all()
+    _same(cert, exact, n, "large batch", expect_status=None)
+    maps[1100, 3, 4] = float("nan")
+    cert(maps)
+    torch.cuda.synchronize()
+    fb = cert.first_bad.cpu().numpy().astype(np.uint64)
+    assert fb[1100, 0] == 3 * C + 4
+    with pytest.raises(uwb.InputError):
+        cert.check_inputs()
