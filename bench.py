@@ -263,6 +263,34 @@ def run_reference(args):
     return 0
 
 
+def step_kernels(cert_ms: float, sat_ms: float, cfar_ms: float, cells: float, certified: bool, fused: bool = False):
+    """{kernel: (ms per launch, algorithmic bytes per launch)} of one CFAR call
+    from its phase times (batch.phase_ms4). Certified path: cert_kernel and the
+    sparse SAT each read the map once; the resolve writes the mask bits (its
+    taps and lists are ~Pfa of the cells). Exact path: the SAT writes the fp64
+    table, the ring CFAR reads it back with the CUT. Fused: one map read."""
+    if fused:
+        return {"cfar_fused_kernel": (cfar_ms, FUSED_BYTES_PER_CELL * cells)}
+    if certified:
+        return {"cert_kernel": (cert_ms, CERT_BYTES_PER_CELL * cells),
+                "sat_systolic_kernel(sparse)": (sat_ms, SPARSE_SAT_BYTES_PER_CELL * cells),
+                "cert_resolve_kernel": (cfar_ms, RESOLVE_BYTES_PER_CELL * cells)}
+    return {"sat_systolic_kernel": (sat_ms, SAT_BYTES_PER_CELL * cells),
+            "cfar_ws_kernel": (cfar_ms, CFAR_BYTES_PER_CELL * cells)}
+
+
+def roofline_of(kernels: dict, peak: float, peak_src: str) -> dict:
+    """Roofline entry of the dominant (longest) kernel of `kernels`."""
+    dom = max(kernels, key=lambda k: kernels[k][0])
+    ms, by = kernels[dom]
+    ach = by / (ms / 1e3) / 1e9 if ms > 0 else 0.0
+    ncu = _ncu_traffic() or {}
+    return {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "traffic": None, "traffic_source": None, "bytes_per_cell": None, "launch_ms": ms,
+            "launch_bytes": by, "peak_source": peak_src,
+            "ncu_kernels_known": sorted(ncu.keys())}
+
+
 def _ncu_traffic():
     """dram bytes per launch of the dominant kernel from the committed ncu summary."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")

@@ -62,20 +62,31 @@ def _events_time(fn, steps, warmup, world, dist):
 
 
 def _phases(n):
-    from paper_2012_11077_b200.batch import phase_ms
-    ph = phase_ms(1024)[:n]
-    return {k: float(np.mean(ph[:, i])) for i, k in enumerate(("sat", "cfar", "sort"))} if len(ph) else {}
+    """Mean {certify, sat, cfar, sort} ms of the last n phase-timed calls."""
+    from paper_2012_11077_b200.batch import phase_ms4
+    ph = phase_ms4(1024)[-n:]
+    return {k: float(np.mean(ph[:, i])) for i, k in enumerate(("certify", "sat", "cfar", "sort"))} if len(ph) else {}
 
 
-def _roof(phases, cells, peak, peak_src):
-    kernels = {"sat_systolic_kernel": (phases.get("sat", 0.0), B.SAT_BYTES_PER_CELL * cells),
-               "cfar_ws_kernel": (phases.get("cfar", 0.0), B.CFAR_BYTES_PER_CELL * cells)}
-    dom = max(kernels, key=lambda k: kernels[k][0])
-    ms, by = kernels[dom]
-    ach = by / (ms / 1e3) / 1e9 if ms > 0 else 0.0
-    return {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-            "traffic": None, "bytes_per_cell": B.SAT_BYTES_PER_CELL if dom.startswith("sat") else
-            B.CFAR_BYTES_PER_CELL, "launch_ms": ms, "peak_source": peak_src}
+def _roof(phases, cells, peak, peak_src, certified=True):
+    """Roofline of the dominant kernel (bench.step_kernels), plus the whole
+    step's HBM fraction over the algorithmic bytes of all its kernels."""
+    ks = B.step_kernels(phases.get("certify", 0.0), phases.get("sat", 0.0), phases.get("cfar", 0.0), cells,
+                        certified)
+    r = B.roofline_of(ks, peak, peak_src)
+    r["bytes_per_cell"] = r["launch_bytes"] / cells
+    return r
+
+
+def _step_frac(phases, cells, ms, peak, certified=True):
+    """Whole-step HBM fraction over the algorithmic bytes of the step's kernels."""
+    ks = B.step_kernels(phases.get("certify", 0.0), phases.get("sat", 0.0), phases.get("cfar", 0.0), cells,
+                        certified)
+    return sum(v[1] for v in ks.values()) / (ms / 1e3) / 1e9 / peak
+
+
+def _certified(runner) -> bool:
+    return bool((runner.cert_status.cpu().numpy() == 0).all())
 
 
 def _init_dist():
@@ -109,7 +120,7 @@ def run_cfg4(args):
     # table per tile (UWB_SAT_TILE semantics): the map runs as a batch of short
     # SAT strip chains instead of one 128-strip chain (DESIGN 4(c))
     runner = BatchCfar(1, s.load_end - s.load_begin, C, p, torch.float32, det_capacity=1 << 16,
-                       slab_rows=CFG4_SLAB_ROWS,
+                       slab_rows=CFG4_SLAB_ROWS, tie_capacity=1 << 12,
                        window=(R, s.load_begin, s.owned_begin, s.owned_end, CFG4_BAND_COLS))
     count = torch.zeros(1, dtype=torch.int64, device="cuda")
 
@@ -119,8 +130,8 @@ def run_cfg4(args):
         reduce_count(count)
 
     step(phase=True)
-    from paper_2012_11077_b200.batch import phase_ms
-    phase_ms(1024)
+    from paper_2012_11077_b200.batch import phase_ms4
+    phase_ms4(1024)
     sampler = B.ClockSampler(torch.cuda.current_device())
     sampler.start()
     l0 = kernel_launches()
@@ -157,9 +168,10 @@ def run_cfg4(args):
     e_ms = float(e_ms.item())
 
     exact = None
+    tie_check = {"tie_band_cells_tile": int(runner.tie_counts[0].item()), "tie_band": "|cut - T| <= 1e-6 T"}
     if world == 1:
         # the reference-exact global table (one 128-strip SAT chain) on the same map
-        g_runner = BatchCfar(1, R, C, p, torch.float32, det_capacity=1 << 16)
+        g_runner = BatchCfar(1, R, C, p, torch.float32, det_capacity=1 << 16, tie_capacity=1 << 12)
         g_count = torch.zeros(1, dtype=torch.int64, device="cuda")
 
         def g_step(phase=False):
@@ -170,7 +182,21 @@ def run_cfg4(args):
         g_ms = _events_time(lambda: g_step(phase=True), max(3, args.steps // 2), 1, world, dist)
         g_ph = _phases(max(3, args.steps // 2) + 1)
         exact = {"value": R * C / (g_ms / 1e3) / 1e9, "unit": B.UNIT, "ms_per_step": g_ms, "phases_ms": g_ph,
-                 "sat": "one global table (bit-identical to the reference)", "detections": int(g_count.item())}
+                 "sat": "one global table (bit-identical to the reference)", "detections": int(g_count.item()),
+                 "certified": _certified(g_runner)}
+        # the tile path against the reference-exact global table on this map:
+        # cells whose decision differs must all lie in the tie band
+        runner(local)
+        torch.cuda.synchronize()
+        tb, gb = runner.mask_bits[0].cpu().numpy().view(np.uint32), g_runner.mask_bits[0].cpu().numpy().view(np.uint32)
+        diff = np.argwhere(np.unpackbits((tb ^ gb).view(np.uint8), axis=1, bitorder="little")[:, :C])
+        t_ties, g_ties = runner.tie_band(0), g_runner.tie_band(0)
+        band = set(zip(t_ties["row"].tolist(), t_ties["col"].tolist())) | \
+            set(zip(g_ties["row"].tolist(), g_ties["col"].tolist()))
+        tie_check = {"tile_vs_global_differing_cells": int(len(diff)),
+                     "differing_outside_tie_band": int(sum(1 for x in diff.tolist() if tuple(x) not in band)),
+                     "tie_band_cells_tile": int(len(t_ties)), "tie_band_cells_global": int(len(g_ties)),
+                     "tie_band": "|cut - T| <= 1e-6 T"}
         del g_runner
 
     cpu = None
@@ -189,11 +215,13 @@ def run_cfg4(args):
                       "parallelism": f"row slabs over {world} GPU(s), halo {g + b} rows, global clamps "
                                      "(uwb_dev_cfar2d_window)",
                       "sat": f"tile-local tables ({CFG4_SLAB_ROWS}-row slabs x {CFG4_BAND_COLS}-column bands, "
-                             "halo 36 rows / 64 columns): masks equal the reference's global table outside the "
-                             "1e-6 tie band and are bit-identical to the reference run on each tile's buffer",
+                             "halo 36 rows / 64 columns): bit-identical to the reference run on each tile's "
+                             "buffer; against the global table see tie_check (measured in this run at N=1)",
                       "l2": "1 GiB input + 2.1 GiB table per pass >> 126 MB L2",
                       "detections_per_step": int(count.item())},
-              roofline=_roof(ph, owned_cells, peak, src), phases_ms=ph, global_exact=exact, cpu_baseline=cpu,
+              roofline=_roof(ph, owned_cells, peak, src, _certified(runner)), phases_ms=ph,
+              step_hbm_frac=_step_frac(ph, owned_cells, ms, peak, _certified(runner)),
+              global_exact=exact, tie_check=tie_check, cpu_baseline=cpu,
               e2e={"value": R * C / (e_ms / 1e3) / 1e9, "unit": B.UNIT,
                    "h2d_bytes_per_step": int(host.numel() * 4) * world,
                    "d2h_bytes_per_step": int(mask_host.numel() * 4 + 8) * world, "ms_per_step": e_ms,
@@ -220,8 +248,10 @@ def run_cfg5(args):
     maps = torch.empty((m1 - m0, R, C), dtype=torch.float32, device="cuda")
     for blk in range(m0 // 8, m1 // 8):
         maps[blk * 8 - m0:(blk + 1) * 8 - m0] = synth.cfg5_maps(8, seed=5_000 + blk, device="cuda", rows=R, cols=C)
-    # the four runs share one workspace: the integral image of each map is built
-    # once per step and read by the four parameter sets (flags bit 2)
+    # the four runs share one workspace and run one after another; each is a
+    # certified-path call (its own window-sum pass, sparse SAT and resolve:
+    # 8 B/cell per run, against 12 + 4 x 12.125 B/cell for one full table read
+    # back by the four parameter sets)
     runners = []
     for (gr, gc, br, bc), pfa in CFG5_RUNS:
         p = uwb.CfarParams(guard_radius=gr, background_radius=br, pfa=pfa, guard_cols=gc, background_cols=bc)
@@ -232,21 +262,21 @@ def run_cfg5(args):
     def step(phase=False):
         count.zero_()
         for i, rn in enumerate(runners):
-            rn(maps, phase_events=phase, reuse_tables=i > 0)
+            rn(maps, phase_events=phase)
             count.add_(rn.counts.sum())
         reduce_count(count)
 
     step(phase=True)
-    from paper_2012_11077_b200.batch import phase_ms
-    phase_ms(1024)
+    from paper_2012_11077_b200.batch import phase_ms4
+    phase_ms4(1024)
     sampler = B.ClockSampler(torch.cuda.current_device())
     sampler.start()
     l0 = kernel_launches()
     ms = _events_time(lambda: step(phase=True), args.steps, max(args.warmup - 1, 0), world, dist)
     launches = kernel_launches() - l0
     clocks = sampler.stop()
-    ph = _phases(4 * (args.steps + max(args.warmup - 1, 0)))
-    ph["sat"] = ph.get("sat", 0.0) * 4  # the SAT phase is recorded by the first run only (others ~0)
+    ph = _phases(4 * (args.steps + max(args.warmup - 1, 0)))  # per run (call)
+    certified = all(_certified(rn) for rn in runners)
     cells_local = (m1 - m0) * R * C
     peak, src = B._peaks()
 
@@ -290,11 +320,12 @@ def run_cfg5(args):
               warmup=args.warmup, ms_per_step=ms,
               config={"workload": "cfg5: 64 K-clutter fp32 maps 8192x2048 (Gamma(0.5) texture, 16x16 box, "
                                   "x Exp(1) speckle) + 64 clusters/map at U(10,25) dB; windows (g_r,g_c,b_r,b_c) "
-                                  "(1,3,4,16),(3,1,16,4) x Pfa 1e-3,1e-5; one step = the 4 runs (one SAT per "
-                                  "map, reused by the 4 parameter sets; the e2e leg runs 4 independent calls)",
+                                  "(1,3,4,16),(3,1,16,4) x Pfa 1e-3,1e-5; one step = the 4 runs, each a full "
+                                  "certified-path call (the e2e leg runs the same 4 calls from host buffers)",
                       "parallelism": f"dp{world} (maps sharded in 8-map blocks)",
                       "l2": "4 GiB input per run >> 126 MB L2", "detections_per_step": int(count.item())},
-              roofline=_roof(ph, cells_local, peak, src), phases_ms=ph, cpu_baseline=cpu,
+              roofline=_roof(ph, cells_local, peak, src, certified), phases_ms_per_run=ph,
+              step_hbm_frac=_step_frac(ph, cells_local, ms / 4, peak, certified), cpu_baseline=cpu,
               e2e={"value": total_cells / (e_ms / 1e3) / 1e9, "unit": B.UNIT,
                    "h2d_bytes_per_step": int(4 * host.numel() * 4) * world,
                    "d2h_bytes_per_step": int(sum(o[0].numel() * 4 + o[1].numel() + o[2].numel() * 8

@@ -390,6 +390,9 @@ bool cert_applies(const Plan& P, const uwb_map_batch& b, const uwb_cfar_params& 
         reinterpret_cast<uintptr_t>(b.maps) % (2 * esz))
         return false;
     if (P.cand_cap == 0 || P.geo.rows >= (int64_t(1) << 30) || P.cols >= (int64_t(1) << 30)) return false;
+    // small batches are latency-bound: the one-CTA-per-table exact SAT and the
+    // ring CFAR take fewer dependent steps than certify + sparse SAT + resolve
+    if (!(flags & 512u) && sat_cta_eligible(P.sat_jobs, P.strips, P.cpl, b.dtype)) return false;
     return cert_supported(p.guard_rows + p.background_rows, p.guard_rows, p.guard_cols + p.background_cols,
                           p.guard_cols);
 }

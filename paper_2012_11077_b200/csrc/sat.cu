@@ -503,6 +503,141 @@ sat_systolic_kernel(SatLaunch L) {
     }
 }
 
+// ---- small batches: one CTA per table, strips hand over through shared memory
+//
+// A batch of a few maps cannot fill the GPU, and the strip chain of the kernel
+// above (one warp per strip, edges handed over through global memory 32 rows at
+// a time, one warp per SM) is latency-bound: ~500 cycles per row step. Here one
+// CTA owns a whole table: warp w runs strip w of the same systolic schedule
+// (lane l: row t - kCtaSkew w - l at step t), lane 31 of warp w leaves
+// S(r, last column) in a shared-memory ring and lane 0 of warp w+1 reads it
+// kCtaSync + 1 steps later; one __syncthreads every kCtaSync steps orders the
+// ring. The same three additions per cell in the same order (sat.cpp:33), so
+// the table is bit-identical to the other kernel's (and the reference's).
+constexpr int kCtaSync = 8;                      // steps between CTA barriers
+constexpr int kCtaSkew = kWarp + kCtaSync;       // steps between adjacent strips
+constexpr int kCtaEdgeRing = 64;                 // edge ring rows (>= kCtaSkew + kCtaSync, power of 2)
+static_assert(kCtaEdgeRing >= kCtaSkew + kCtaSync && kCtaSync < kWarp, "edge ring / barrier spacing");
+
+template <typename T, int kCpl>
+constexpr int cta_sat_max_warps() { // the staging rings fit the shared memory
+    return sizeof(T) * kCpl >= 32 ? 8 : 16;
+}
+
+template <typename T, int kCpl>
+__global__ void __launch_bounds__(16 * kWarp, 1) sat_cta_kernel(SatLaunch L) {
+    extern __shared__ __align__(16) unsigned char cta_smem_raw[];
+    constexpr unsigned kXLane = kCpl * sizeof(T);
+    constexpr unsigned kXSlotBytes = kWarp * kXLane;
+    const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+    const int n_warps = blockDim.x / kWarp; // == strips of this table
+    const unsigned base = (smem_u32(cta_smem_raw) + 15u) & ~15u;
+    const unsigned x_lane = base + static_cast<unsigned>(warp) * kXSlots * kXSlotBytes + lane * kXLane;
+    double* edge = reinterpret_cast<double*>(cta_smem_raw + ((base - smem_u32(cta_smem_raw)) +
+                                                             static_cast<unsigned>(n_warps) * kXSlots * kXSlotBytes));
+    const SatJobView J = sat_job(L, blockIdx.x);
+    const int rows = static_cast<int>(J.rows);
+    const int cols = static_cast<int>(L.cols);
+    const int c = warp * kWarp * kCpl + kCpl * lane;
+    const int nvalid = max(0, min(kCpl, cols - c));
+    const T* src = static_cast<const T*>(J.src);
+    const int64_t ld = L.ld, tld = L.table_ld;
+    double* table = J.table;
+    for (int k = 0; k < nvalid; ++k) table[kTabShift + 1 + c + k] = 0.0; // padded row 0
+    if (warp == 0 && lane == 0) table[kTabShift] = 0.0;
+    const bool vec = nvalid == kCpl && L.vec_ok;
+    // a lane's source values of row r go to slot (its step of row r) mod kXSlots
+    auto stage = [&](int t_of_row, int r) {
+        if (r < 0 || r >= rows || nvalid == 0) return;
+        const unsigned dst = x_lane + static_cast<unsigned>(t_of_row & (kXSlots - 1)) * kXSlotBytes;
+        const T* p = src + static_cast<int64_t>(r) * ld + c;
+        if (vec) {
+            cp_async_lane<T, kCpl>(dst, p);
+        } else {
+            for (int k = 0; k < nvalid; ++k) cp_async_one(dst + k * sizeof(T), p + k);
+        }
+    };
+    const int lag = kCtaSkew * warp + lane; // row r is handled at step r + lag
+#pragma unroll 1
+    for (int t = 0; t < kAhead; ++t) {
+        stage(t, t - lag);
+        cp_async_commit();
+    }
+    double prev[kCpl], last[kCpl];
+#pragma unroll
+    for (int k = 0; k < kCpl; ++k) prev[k] = last[k] = 0.0;
+    double left_prev = 0.0;
+    const int steps = rows + kCtaSkew * (n_warps - 1) + kWarp;
+#pragma unroll 1
+    for (int t = 0; t < steps; ++t) {
+        const int r = t - lag;
+        stage(t + kAhead, r + kAhead);
+        cp_async_commit();
+        cp_async_wait<kAhead>();
+        T x[kCpl];
+        lds_lane<kCpl>(x_lane + static_cast<unsigned>(t & (kXSlots - 1)) * kXSlotBytes, x);
+        double left = __shfl_up_sync(0xffffffffu, last[kCpl - 1], 1);
+        const bool act = r >= 0 && r < rows;
+        if (lane == 0) left = (warp > 0 && act) ? edge[(warp - 1) * kCtaEdgeRing + (r & (kCtaEdgeRing - 1))] : 0.0;
+        if (act) {
+            double sv[kCpl];
+            sv[0] = dsub(dadd(dadd(widen(x[0]), prev[0]), left), left_prev);
+#pragma unroll
+            for (int k = 1; k < kCpl; ++k) sv[k] = dsub(dadd(dadd(widen(x[k]), prev[k]), sv[k - 1]), prev[k - 1]);
+            double* dst = table + static_cast<int64_t>(r + 1) * tld + kTabShift + 1 + c;
+#pragma unroll
+            for (int k = 0; k < kCpl; ++k)
+                if (k < nvalid) dst[k] = sv[k];
+            if (warp == 0 && lane == 0) table[static_cast<int64_t>(r + 1) * tld + kTabShift] = 0.0;
+            if (lane == kWarp - 1 && warp + 1 < n_warps)
+                edge[warp * kCtaEdgeRing + (r & (kCtaEdgeRing - 1))] = sv[kCpl - 1];
+            left_prev = left;
+#pragma unroll
+            for (int k = 0; k < kCpl; ++k) prev[k] = last[k] = sv[k];
+        }
+        if ((t + 1) % kCtaSync == 0) __syncthreads();
+    }
+    cp_async_wait<0>();
+    // non-finite inputs poison every later S of their column (see the header)
+    bool finite = true;
+#pragma unroll
+    for (int k = 0; k < kCpl; ++k) finite &= k >= nvalid || isfinite(last[k]);
+    if (!finite && J.nonfinite) {
+        int col = c;
+        const int bad = first_nonfinite<T>(src, ld, c, nvalid, rows, &col);
+        if (bad != INT_MAX)
+            report_min(J.nonfinite, static_cast<unsigned long long>((J.row0 + bad) * L.geo.map_cols + J.col0 + col));
+    }
+}
+
+} // namespace
+bool sat_cta_eligible(int64_t n_jobs, int64_t strips, int cpl, int dtype);
+namespace {
+
+template <typename T, int kCpl>
+size_t cta_sat_smem(int warps) {
+    return 16 + static_cast<size_t>(warps) * (kXSlots * kWarp * kCpl * sizeof(T) + kCtaEdgeRing * sizeof(double));
+}
+
+// One CTA per table when the batch is too small to fill the GPU and every
+// table's strips fit one CTA (dense tables only).
+template <typename T, int kCpl>
+static bool launch_sat_cta(const SatLaunch& L, cudaStream_t stream, cudaError_t* err) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (L.need || !sat_cta_eligible(L.n_jobs, L.strips, kCpl, sizeof(T) == 4 ? UWB_F32 : UWB_F64)) return false;
+    const int warps = static_cast<int>(L.strips);
+    const size_t smem = cta_sat_smem<T, kCpl>(warps);
+    auto kern = sat_cta_kernel<T, kCpl>;
+    *err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (*err != cudaSuccess) return true;
+    ++g_kernel_launches;
+    kern<<<static_cast<unsigned>(L.n_jobs), warps * kWarp, smem, stream>>>(L);
+    *err = cudaGetLastError();
+    return true;
+}
+
 template <typename T, int kCpl, bool kSparse>
 static cudaError_t launch_sat_t(const SatLaunch& L, cudaStream_t stream) {
     const int64_t n_tiles = L.n_jobs * L.strips;
@@ -541,6 +676,8 @@ static cudaError_t launch_sat_t(const SatLaunch& L, cudaStream_t stream) {
 
 template <typename T>
 static cudaError_t launch_sat_cpl(const SatLaunch& L, cudaStream_t stream) {
+    cudaError_t e = cudaSuccess;
+    if (L.cpl == 4 && launch_sat_cta<T, 4>(L, stream, &e)) return e;
     if (L.need) {
         switch (L.cpl) {
             case 1: return launch_sat_t<T, 1, true>(L, stream);
@@ -578,6 +715,14 @@ int sat_cpl_for(int64_t n_jobs, int64_t cols) {
         if (c == 1 || c == 2 || c == 4) return c;
     }
     return 4;
+}
+
+bool sat_cta_eligible(int64_t n_jobs, int64_t strips, int cpl, int dtype) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int max_warps = dtype == UWB_F32 ? cta_sat_max_warps<float, 4>() : cta_sat_max_warps<double, 4>();
+    return cpl == 4 && n_jobs >= 1 && n_jobs <= sms && strips <= max_warps;
 }
 
 int64_t sat_strips(int64_t cols, int cpl) { return (cols + kWarp * cpl - 1) / (kWarp * cpl); }

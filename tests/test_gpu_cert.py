@@ -42,7 +42,7 @@ def test_cfg3_shape_certified_equals_exact_and_reference(uwb, ref, cuda):
     maps = synth.cfg3_maps(n, seed=11, device=cuda)
     p = uwb.CfarParams(2, 8, 1e-4)
     cert, exact = _pair(n, 1024, 1024, p, det_capacity=1024)
-    cert(maps)
+    cert(maps, certify=True)
     exact(maps, exact=True)
     torch.cuda.synchronize()
     cert.check_inputs()
@@ -79,7 +79,7 @@ def test_tie_band_matches_exact_thresholds(uwb, cuda):
         maps[i, rr, cc] = thr[i, rr, cc] * (1.0 + d)
     full(maps)
     cert = BatchCfar(n, R, C, p, torch.float64, det_capacity=4096, tie_capacity=4096)
-    cert(maps)
+    cert(maps, certify=True)
     torch.cuda.synchronize()
     # placed cells keep their T up to the table rounding (every cell enters every later table entry)
     assert torch.allclose(full.thresholds[:, rr, cc], thr[:, rr, cc], rtol=1e-9, atol=0)
@@ -112,7 +112,7 @@ def test_instantiated_windows_equal_exact(uwb, cuda, shape):
     synth.add_point_targets(maps, 5, 10.0, 20.0, seed=22)
     p = uwb.CfarParams(guard_radius=gr, background_radius=br, pfa=pfa, guard_cols=gc, background_cols=bc)
     cert, exact = _pair(n, R, C, p, dt, det_capacity=1 << 14)
-    cert(maps)
+    cert(maps, certify=True)
     exact(maps, exact=True)
     torch.cuda.synchronize()
     _same(cert, exact, n, f"window {(gr, gc, br, bc)}")
@@ -129,7 +129,7 @@ def test_out_of_range_and_overflow_maps_run_exact(uwb, cuda):
     maps[2].zero_()
     p = uwb.CfarParams(2, 8, 1e-4)
     cert, exact = _pair(n, 1024, 1024, p, det_capacity=2048)
-    cert(maps)
+    cert(maps, certify=True)
     exact(maps, exact=True)
     torch.cuda.synchronize()
     st = cert.cert_status.cpu().numpy()
@@ -149,7 +149,7 @@ def test_input_errors_reported_like_exact_path(uwb, cuda):
     maps[2, 0, 0] = -0.0      # a valid zero
     p = uwb.CfarParams(2, 8, 1e-4)
     cert, exact = _pair(n, 1024, 1024, p, det_capacity=1024)
-    cert(maps)
+    cert(maps, certify=True)
     exact(maps, exact=True)
     torch.cuda.synchronize()
     assert torch.equal(cert.first_bad, exact.first_bad)
@@ -174,7 +174,7 @@ def test_row_window_tiles_equal_exact(uwb, cuda):
         win = (R, b0, r0, r1, 1024)
         cert = BatchCfar(1, b1 - b0, C, p, torch.float32, det_capacity=1 << 15, window=win, slab_rows=512)
         exact = BatchCfar(1, b1 - b0, C, p, torch.float32, det_capacity=1 << 15, window=win, slab_rows=512)
-        cert(buf)
+        cert(buf, certify=True)
         exact(buf, exact=True)
         torch.cuda.synchronize()
         _same(cert, exact, 1, f"rows [{r0}, {r1})")
@@ -186,7 +186,7 @@ def test_odd_width_runs_exact_path(uwb, cuda):
     maps = synth.exponential_maps(3, 512, 25, seed=61, dtype=torch.float64, device=cuda)
     p = uwb.CfarParams(1, 4, 1e-3)
     cert, exact = _pair(3, 512, 25, p, torch.float64, det_capacity=1024)
-    cert(maps)
+    cert(maps, certify=True)
     exact(maps, exact=True)
     torch.cuda.synchronize()
     _same(cert, exact, 3, "odd width", expect_status=-1)
@@ -205,14 +205,14 @@ def test_large_batch_with_fallback_maps_equals_exact(uwb, cuda):
     maps[700, 10, 10] = 1000.0        # outside the certified range: exact fallback for map 700
     p = uwb.CfarParams(2, 8, 1e-4)
     cert, exact = _pair(n, R, C, p, det_capacity=256)
-    cert(maps)
+    cert(maps, certify=True)
     exact(maps, exact=True)
     torch.cuda.synchronize()
     st = cert.cert_status.cpu().numpy()
     assert st[700] != 0 and (np.delete(st, 700) == 0).all()
     _same(cert, exact, n, "large batch", expect_status=None)
     maps[1100, 3, 4] = float("nan")
-    cert(maps)
+    cert(maps, certify=True)
     torch.cuda.synchronize()
     fb = cert.first_bad.cpu().numpy().astype(np.uint64)
     assert fb[1100, 0] == 3 * C + 4
