@@ -15,6 +15,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -392,10 +394,19 @@ bool cert_applies(const Plan& P, const uwb_map_batch& b, const uwb_cfar_params& 
     if (P.cand_cap == 0 || P.geo.rows >= (int64_t(1) << 30) || P.cols >= (int64_t(1) << 30)) return false;
     // small batches are latency-bound: the one-CTA-per-table exact SAT and the
     // ring CFAR take fewer dependent steps than certify + sparse SAT + resolve
-    if (!(flags & 512u) && sat_cta_eligible(P.sat_jobs, P.strips, P.cpl, b.dtype)) return false;
+    if (!(flags & 512u) && sat_cta_eligible(P.sat_jobs, P.sat_cols, b.dtype)) return false;
     return cert_supported(p.guard_rows + p.background_rows, p.guard_rows, p.guard_cols + p.background_cols,
                           p.guard_cols);
 }
+
+// NVTX range over the launches of one stage (host side; visible in nsys / ncu
+// NVTX filters; no cost without an attached tool).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Device-resident CFAR of a batch (no validation beyond layout; see uwb_dev_cfar2d).
 uwb_status dev_cfar(const uwb_map_batch& b, const uwb_cfar_params& p, const double* alpha,
@@ -431,11 +442,18 @@ uwb_status dev_cfar(const uwb_map_batch& b, const uwb_cfar_params& p, const doub
         SL.need_rows = P.need_rows;
         SL.map_full = CL.status;
         SL.jobs_per_map = P.geo.n_slabs * P.geo.n_bands;
-        UWB_CUDA_TRY(launch_cert(CL, b.dtype, s));
-        UWB_CUDA_TRY(launch_cert_mark(CL, s));
+        {
+            NvtxRange r("uwb.certify");
+            UWB_CUDA_TRY(launch_cert(CL, b.dtype, s));
+            UWB_CUDA_TRY(launch_cert_mark(CL, s));
+        }
         if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[1], s));
-        UWB_CUDA_TRY(run_sat(P, SL, b.dtype, s));
+        {
+            NvtxRange r("uwb.sat.sparse");
+            UWB_CUDA_TRY(run_sat(P, SL, b.dtype, s));
+        }
         if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[2], s));
+        NvtxRange r("uwb.resolve");
         UWB_CUDA_TRY(launch_cert_resolve(CL, b.dtype, s));
         // maps the certificate could not cover (values outside its range, or
         // more candidates than the list holds) have full tables: exact kernel
@@ -467,9 +485,11 @@ uwb_status dev_cfar(const uwb_map_batch& b, const uwb_cfar_params& p, const doub
         }
         if (!fused) {
             if (!(flags & 4u)) { // bit 2: the workspace already holds this batch's tables
+                NvtxRange r("uwb.sat");
                 const SatLaunch SL = sat_launch(P, b, ws, reinterpret_cast<unsigned long long*>(o.first_bad));
                 UWB_CUDA_TRY(run_sat(P, SL, b.dtype, s));
             }
+            NvtxRange r("uwb.cfar");
             if (ev) UWB_CUDA_TRY(cudaEventRecord(ev[2], s));
             CfarLaunch FL = cfar_launch(P, b, p, alpha, ws, o);
             FL.fixed_rows = (flags & 256u) != 0; // bit 8 (test hook): 256-row ring chunks, same results
@@ -492,6 +512,7 @@ uwb_status dev_cfar(const uwb_map_batch& b, const uwb_cfar_params& p, const doub
         uwb_detection* scratch = (o.det_capacity > 2048 && ws && ws_bytes >= P.total)
                                      ? reinterpret_cast<uwb_detection*>(ws + P.off_scratch)
                                      : nullptr;
+        NvtxRange r("uwb.sort");
         UWB_CUDA_TRY(launch_sort_detections(o.dets, static_cast<int64_t>(o.det_capacity),
                                             reinterpret_cast<const unsigned long long*>(o.det_counts),
                                             static_cast<int64_t>(b.n_maps), scratch, s));
@@ -1430,6 +1451,7 @@ uwb_status uwb_dev_detect_batch(const void* records, int32_t dtype, uint64_t n_r
     F.kept = static_cast<int64_t>(D.kept);
     F.band = band;
     // flags bit 8 (test hook): the general front-end kernels (same results)
+    NvtxRange fe("uwb.detect_batch");
     const cudaError_t fused = (flags & 256u) ? cudaErrorNotSupported : launch_frontend_fused(F, s);
     if (fused == cudaErrorNotSupported) {
         F.stage_mask = 3;

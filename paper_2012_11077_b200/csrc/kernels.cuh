@@ -215,7 +215,7 @@ cudaError_t launch_sat(const SatLaunch& L, int dtype, cudaStream_t stream);
 int64_t sat_strips(int64_t cols, int cpl);       // strips of 32 * cpl columns
 int sat_cpl_for(int64_t n_jobs, int64_t cols);   // columns per lane for a batch
 // small batches whose tables each fit one CTA (sat_cta_kernel: strips hand over in shared memory)
-bool sat_cta_eligible(int64_t n_jobs, int64_t strips, int cpl, int dtype);
+bool sat_cta_eligible(int64_t n_jobs, int64_t cols, int dtype);
 
 cudaError_t launch_cfar_integral(const CfarLaunch& L, int dtype, cudaStream_t stream);
 // SAT + CFAR in one kernel, table kept on chip (cfar_fused.cu). Whole-map

@@ -507,133 +507,183 @@ sat_systolic_kernel(SatLaunch L) {
 //
 // A batch of a few maps cannot fill the GPU, and the strip chain of the kernel
 // above (one warp per strip, edges handed over through global memory 32 rows at
-// a time, one warp per SM) is latency-bound: ~500 cycles per row step. Here one
-// CTA owns a whole table: warp w runs strip w of the same systolic schedule
-// (lane l: row t - kCtaSkew w - l at step t), lane 31 of warp w leaves
-// S(r, last column) in a shared-memory ring and lane 0 of warp w+1 reads it
-// kCtaSync + 1 steps later; one __syncthreads every kCtaSync steps orders the
-// ring. The same three additions per cell in the same order (sat.cpp:33), so
-// the table is bit-identical to the other kernel's (and the reference's).
-constexpr int kCtaSync = 8;                      // steps between CTA barriers
+// a time, one warp per SM) is latency-bound. Here one CTA owns a whole table:
+// warp w runs strip w of the same systolic schedule, kCtaSkew steps behind
+// warp w-1 (lane l: row s - l at local step s = t - kCtaSkew w); lane 31 of warp
+// w leaves S(r, last column) in a shared-memory ring and lane 0 of warp w+1
+// reads it kCtaSync + 1 steps later, one __syncthreads every kCtaSync steps
+// ordering the ring. Lanes own 16 bytes of source per row (4 fp32 / 2 fp64
+// columns: the shortest dependent chain per step that keeps the loads whole
+// lines), and global memory is touched only in whole 128-byte lines: lane group
+// g (8 lanes) stages, with cp.async, the row its lanes need kCtaAhead..+7 steps
+// later into lane-private slots, and writes back, from a lane-private 8-row
+// delay ring, the row it finished 8..15 steps earlier. The same three additions
+// per cell in the same order (sat.cpp:33): bit-identical tables.
+constexpr int kCtaSync = 8;                      // steps per unrolled block (one CTA barrier each)
 constexpr int kCtaSkew = kWarp + kCtaSync;       // steps between adjacent strips
 constexpr int kCtaEdgeRing = 64;                 // edge ring rows (>= kCtaSkew + kCtaSync, power of 2)
+constexpr int kCtaAhead = 8;                     // staging distance (steps)
+constexpr int kCtaXSlots = 16;                   // lane-private source slots
+constexpr int kCtaOSlots = 8;                    // lane-private result delay slots
+constexpr int kCtaMaxWarps = 12;                 // strips per CTA (shared memory)
 static_assert(kCtaEdgeRing >= kCtaSkew + kCtaSync && kCtaSync < kWarp, "edge ring / barrier spacing");
+static_assert(kCtaXSlots >= kCtaAhead + 8 && kCtaSkew % kCtaSync == 0, "staging ring / block alignment");
 
-template <typename T, int kCpl>
-constexpr int cta_sat_max_warps() { // the staging rings fit the shared memory
-    return sizeof(T) * kCpl >= 32 ? 8 : 16;
+template <typename T>
+__host__ __device__ constexpr int cta_cpl() { return 16 / static_cast<int>(sizeof(T)); }
+template <typename T>
+constexpr size_t cta_smem_per_warp() {
+    return kCtaXSlots * kWarp * 16 + kCtaOSlots * kWarp * cta_cpl<T>() * sizeof(double) +
+           kCtaEdgeRing * sizeof(double);
 }
 
-template <typename T, int kCpl>
-__global__ void __launch_bounds__(16 * kWarp, 1) sat_cta_kernel(SatLaunch L) {
+template <typename T>
+__global__ void __launch_bounds__(kCtaMaxWarps * kWarp, 1) sat_cta_kernel(SatLaunch L) {
+    constexpr int kC = cta_cpl<T>();
+    constexpr unsigned kXSlot = kWarp * 16;                     // bytes per source slot
+    constexpr unsigned kOSlot = kWarp * kC * sizeof(double);    // bytes per result slot
     extern __shared__ __align__(16) unsigned char cta_smem_raw[];
-    constexpr unsigned kXLane = kCpl * sizeof(T);
-    constexpr unsigned kXSlotBytes = kWarp * kXLane;
     const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+    const int grp = lane >> 3, j = lane & 7;
     const int n_warps = blockDim.x / kWarp; // == strips of this table
     const unsigned base = (smem_u32(cta_smem_raw) + 15u) & ~15u;
-    const unsigned x_lane = base + static_cast<unsigned>(warp) * kXSlots * kXSlotBytes + lane * kXLane;
-    double* edge = reinterpret_cast<double*>(cta_smem_raw + ((base - smem_u32(cta_smem_raw)) +
-                                                             static_cast<unsigned>(n_warps) * kXSlots * kXSlotBytes));
+    const unsigned x_lane = base + static_cast<unsigned>(warp) * kCtaXSlots * kXSlot + lane * 16u;
+    const unsigned o_base = base + static_cast<unsigned>(n_warps) * kCtaXSlots * kXSlot;
+    const unsigned o_lane = o_base + static_cast<unsigned>(warp) * kCtaOSlots * kOSlot + lane * 16u;
+    double* edge = reinterpret_cast<double*>(cta_smem_raw + (o_base - smem_u32(cta_smem_raw)) +
+                                             static_cast<size_t>(n_warps) * kCtaOSlots * kOSlot);
     const SatJobView J = sat_job(L, blockIdx.x);
     const int rows = static_cast<int>(J.rows);
     const int cols = static_cast<int>(L.cols);
-    const int c = warp * kWarp * kCpl + kCpl * lane;
-    const int nvalid = max(0, min(kCpl, cols - c));
-    const T* src = static_cast<const T*>(J.src);
+    const int c = (warp * kWarp + lane) * kC;
+    const int nvalid = max(0, min(kC, cols - c));
+    const T* src = static_cast<const T*>(J.src) + c;
     const int64_t ld = L.ld, tld = L.table_ld;
     double* table = J.table;
     for (int k = 0; k < nvalid; ++k) table[kTabShift + 1 + c + k] = 0.0; // padded row 0
     if (warp == 0 && lane == 0) table[kTabShift] = 0.0;
-    const bool vec = nvalid == kCpl && L.vec_ok;
-    // a lane's source values of row r go to slot (its step of row r) mod kXSlots
-    auto stage = [&](int t_of_row, int r) {
-        if (r < 0 || r >= rows || nvalid == 0) return;
-        const unsigned dst = x_lane + static_cast<unsigned>(t_of_row & (kXSlots - 1)) * kXSlotBytes;
-        const T* p = src + static_cast<int64_t>(r) * ld + c;
-        if (vec) {
-            cp_async_lane<T, kCpl>(dst, p);
+    const bool vec = nvalid == kC && L.vec_ok;
+    const bool full = __all_sync(0xffffffffu, vec); // every lane: 16 aligned source bytes in the map
+    double* edge_in = warp > 0 ? edge + (warp - 1) * kCtaEdgeRing : nullptr;
+    double* edge_out = warp + 1 < n_warps ? edge + warp * kCtaEdgeRing : nullptr;
+
+    // group g stages source row s + kCtaAhead - 8g at local step s into slot (s + kCtaAhead) mod 16
+    auto stage = [&](int s, bool checked) {
+        const int r = s + kCtaAhead - 8 * grp;
+        if (checked && (r < 0 || r >= rows || nvalid == 0)) return;
+        const unsigned dst = x_lane + static_cast<unsigned>((s + kCtaAhead) & (kCtaXSlots - 1)) * kXSlot;
+        const T* p = src + static_cast<int64_t>(r) * ld;
+        if (!checked || vec) {
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(p) : "memory");
         } else {
             for (int k = 0; k < nvalid; ++k) cp_async_one(dst + k * sizeof(T), p + k);
         }
     };
-    const int lag = kCtaSkew * warp + lane; // row r is handled at step r + lag
-#pragma unroll 1
-    for (int t = 0; t < kAhead; ++t) {
-        stage(t, t - lag);
-        cp_async_commit();
-    }
-    double prev[kCpl], last[kCpl];
+    double prev[kC], last[kC];
 #pragma unroll
-    for (int k = 0; k < kCpl; ++k) prev[k] = last[k] = 0.0;
+    for (int k = 0; k < kC; ++k) prev[k] = last[k] = 0.0;
     double left_prev = 0.0;
-    const int steps = rows + kCtaSkew * (n_warps - 1) + kWarp;
-#pragma unroll 1
-    for (int t = 0; t < steps; ++t) {
-        const int r = t - lag;
-        stage(t + kAhead, r + kAhead);
-        cp_async_commit();
-        cp_async_wait<kAhead>();
-        T x[kCpl];
-        lds_lane<kCpl>(x_lane + static_cast<unsigned>(t & (kXSlots - 1)) * kXSlotBytes, x);
-        double left = __shfl_up_sync(0xffffffffu, last[kCpl - 1], 1);
-        const bool act = r >= 0 && r < rows;
-        if (lane == 0) left = (warp > 0 && act) ? edge[(warp - 1) * kCtaEdgeRing + (r & (kCtaEdgeRing - 1))] : 0.0;
-        if (act) {
-            double sv[kCpl];
-            sv[0] = dsub(dadd(dadd(widen(x[0]), prev[0]), left), left_prev);
+    T xn[kC]; // source of the next step (loaded one step ahead)
 #pragma unroll
-            for (int k = 1; k < kCpl; ++k) sv[k] = dsub(dadd(dadd(widen(x[k]), prev[k]), sv[k - 1]), prev[k - 1]);
-            double* dst = table + static_cast<int64_t>(r + 1) * tld + kTabShift + 1 + c;
+    for (int k = 0; k < kC; ++k) xn[k] = T(0);
+    // local steps [-kCtaSync, s_end): staging starts kCtaAhead steps before row 0,
+    // the delay ring drains 8 * 3 + 8 steps after the last row
+    const int s_end = rows + kWarp + 4 * 8;
+    const int skew = kCtaSkew * warp;
+    const int n_blocks = (s_end + kCtaSync + kCtaSkew * (n_warps - 1) + kCtaSync - 1) / kCtaSync;
+
+    auto block = [&](const int s0, auto checked_tag) {
+        constexpr bool kChecked = decltype(checked_tag)::value;
 #pragma unroll
-            for (int k = 0; k < kCpl; ++k)
-                if (k < nvalid) dst[k] = sv[k];
-            if (warp == 0 && lane == 0) table[static_cast<int64_t>(r + 1) * tld + kTabShift] = 0.0;
-            if (lane == kWarp - 1 && warp + 1 < n_warps)
-                edge[warp * kCtaEdgeRing + (r & (kCtaEdgeRing - 1))] = sv[kCpl - 1];
-            left_prev = left;
+        for (int u = 0; u < kCtaSync; ++u) {
+            const int s = s0 + u;
+            const int r = s - lane;
+            // (1) group g writes back row s - 8g - 8 (computed 1..8 steps ago, slot (s + j) mod 8)
+            {
+                const int rf = s - 8 * grp - 8;
+                if (!kChecked || (rf >= 0 && rf < rows)) {
+                    double o[kC];
+                    lds_out<kC>(o_lane + static_cast<unsigned>((s + j) & (kCtaOSlots - 1)) * kOSlot, o);
+                    double* dst = table + static_cast<int64_t>(rf + 1) * tld + kTabShift + 1 + c;
+                    if (!kChecked || nvalid == kC) {
 #pragma unroll
-            for (int k = 0; k < kCpl; ++k) prev[k] = last[k] = sv[k];
+                        for (int q = 0; q < kC / 2; ++q)
+                            reinterpret_cast<double2*>(dst)[q] = make_double2(o[2 * q], o[2 * q + 1]);
+                    } else {
+                        for (int k = 0; k < nvalid; ++k) dst[k] = o[k];
+                    }
+                }
+            }
+            // (2) stage the source row needed kCtaAhead..+7 steps later
+            stage(s, kChecked);
+            cp_async_commit();
+            // (3) this step's source was loaded last step; load the next step's
+            T x[kC];
+#pragma unroll
+            for (int k = 0; k < kC; ++k) x[k] = xn[k];
+            cp_async_wait<kCtaAhead - 1>();
+            lds_lane<kC>(x_lane + static_cast<unsigned>((s + 1 - j) & (kCtaXSlots - 1)) * kXSlot, xn);
+            // (4) x + S(r-1, .) before the left neighbour arrives
+            double a[kC];
+#pragma unroll
+            for (int k = 0; k < kC; ++k) a[k] = dadd(widen(x[k]), prev[k]);
+            const bool act = !kChecked || (r >= 0 && r < rows);
+            double left = __shfl_up_sync(0xffffffffu, last[kC - 1], 1);
+            if (lane == 0) left = (edge_in && act) ? edge_in[r & (kCtaEdgeRing - 1)] : 0.0;
+            double sv[kC];
+            sv[0] = dsub(dadd(a[0], left), left_prev);
+#pragma unroll
+            for (int k = 1; k < kC; ++k) sv[k] = dsub(dadd(a[k], sv[k - 1]), prev[k - 1]);
+            if (act) {
+                sts_out<kC>(o_lane + static_cast<unsigned>(s & (kCtaOSlots - 1)) * kOSlot, sv);
+                if (lane == kWarp - 1 && edge_out) edge_out[r & (kCtaEdgeRing - 1)] = sv[kC - 1];
+                if (warp == 0 && lane == 0) table[static_cast<int64_t>(r + 1) * tld + kTabShift] = 0.0;
+                left_prev = left;
+#pragma unroll
+                for (int k = 0; k < kC; ++k) prev[k] = last[k] = sv[k];
+            }
         }
-        if ((t + 1) % kCtaSync == 0) __syncthreads();
+    };
+    // prologue: stage the rows of local steps before -kCtaSync (group 0: row 0 at
+    // step -kCtaAhead is the first real copy; nothing earlier is needed)
+#pragma unroll 1
+    for (int b = 0; b < n_blocks; ++b) {
+        const int s0 = b * kCtaSync - kCtaSync - skew; // local step of this block
+        if (s0 + kCtaSync > -kCtaSync && s0 < s_end) {
+            const bool interior = full && s0 >= kWarp && s0 + 2 * kCtaSync <= rows;
+            if (interior) block(s0, std::integral_constant<bool, false>{});
+            else block(s0, std::integral_constant<bool, true>{});
+        }
+        __syncthreads();
     }
     cp_async_wait<0>();
     // non-finite inputs poison every later S of their column (see the header)
     bool finite = true;
 #pragma unroll
-    for (int k = 0; k < kCpl; ++k) finite &= k >= nvalid || isfinite(last[k]);
+    for (int k = 0; k < kC; ++k) finite &= k >= nvalid || isfinite(last[k]);
     if (!finite && J.nonfinite) {
         int col = c;
-        const int bad = first_nonfinite<T>(src, ld, c, nvalid, rows, &col);
+        const int bad = first_nonfinite<T>(static_cast<const T*>(J.src), ld, c, nvalid, rows, &col);
         if (bad != INT_MAX)
             report_min(J.nonfinite, static_cast<unsigned long long>((J.row0 + bad) * L.geo.map_cols + J.col0 + col));
     }
 }
 
 } // namespace
-bool sat_cta_eligible(int64_t n_jobs, int64_t strips, int cpl, int dtype);
+bool sat_cta_eligible(int64_t n_jobs, int64_t cols, int dtype);
 namespace {
-
-template <typename T, int kCpl>
-size_t cta_sat_smem(int warps) {
-    return 16 + static_cast<size_t>(warps) * (kXSlots * kWarp * kCpl * sizeof(T) + kCtaEdgeRing * sizeof(double));
-}
 
 // One CTA per table when the batch is too small to fill the GPU and every
 // table's strips fit one CTA (dense tables only).
-template <typename T, int kCpl>
+template <typename T>
 static bool launch_sat_cta(const SatLaunch& L, cudaStream_t stream, cudaError_t* err) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (L.need || !sat_cta_eligible(L.n_jobs, L.strips, kCpl, sizeof(T) == 4 ? UWB_F32 : UWB_F64)) return false;
-    const int warps = static_cast<int>(L.strips);
-    const size_t smem = cta_sat_smem<T, kCpl>(warps);
-    auto kern = sat_cta_kernel<T, kCpl>;
-    *err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (L.need || !sat_cta_eligible(L.n_jobs, L.cols, sizeof(T) == 4 ? UWB_F32 : UWB_F64)) return false;
+    const int warps = static_cast<int>((L.cols + kWarp * cta_cpl<T>() - 1) / (kWarp * cta_cpl<T>()));
+    const size_t smem = 16 + static_cast<size_t>(warps) * cta_smem_per_warp<T>();
+    *err = cudaFuncSetAttribute(sat_cta_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (*err != cudaSuccess) return true;
     ++g_kernel_launches;
-    kern<<<static_cast<unsigned>(L.n_jobs), warps * kWarp, smem, stream>>>(L);
+    sat_cta_kernel<T><<<static_cast<unsigned>(L.n_jobs), warps * kWarp, smem, stream>>>(L);
     *err = cudaGetLastError();
     return true;
 }
@@ -677,7 +727,7 @@ static cudaError_t launch_sat_t(const SatLaunch& L, cudaStream_t stream) {
 template <typename T>
 static cudaError_t launch_sat_cpl(const SatLaunch& L, cudaStream_t stream) {
     cudaError_t e = cudaSuccess;
-    if (L.cpl == 4 && launch_sat_cta<T, 4>(L, stream, &e)) return e;
+    if (launch_sat_cta<T>(L, stream, &e)) return e;
     if (L.need) {
         switch (L.cpl) {
             case 1: return launch_sat_t<T, 1, true>(L, stream);
@@ -717,12 +767,12 @@ int sat_cpl_for(int64_t n_jobs, int64_t cols) {
     return 4;
 }
 
-bool sat_cta_eligible(int64_t n_jobs, int64_t strips, int cpl, int dtype) {
+bool sat_cta_eligible(int64_t n_jobs, int64_t cols, int dtype) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int max_warps = dtype == UWB_F32 ? cta_sat_max_warps<float, 4>() : cta_sat_max_warps<double, 4>();
-    return cpl == 4 && n_jobs >= 1 && n_jobs <= sms && strips <= max_warps;
+    const int64_t strip_cols = kWarp * (dtype == UWB_F32 ? cta_cpl<float>() : cta_cpl<double>());
+    return n_jobs >= 1 && n_jobs <= sms && (cols + strip_cols - 1) / strip_cols <= kCtaMaxWarps;
 }
 
 int64_t sat_strips(int64_t cols, int cpl) { return (cols + kWarp * cpl - 1) / (kWarp * cpl); }

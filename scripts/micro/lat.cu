@@ -1,56 +1,29 @@
-// Dependent-chain latencies on this GPU: DADD (rn), DMUL, SHFL (64-bit as two 32-bit), LDS.
+// Latency probe: dependent DADD chain, dependent shfl chain, LDS chain (one warp).
 #include <cstdio>
 #include <cuda_runtime.h>
-
-__global__ void k_dadd(double* out, long long* cyc, double a, int n) {
+__global__ void k(double* out, long long* cyc, double a, double b, int n) {
     double x = a;
     long long t0 = clock64();
-    for (int i = 0; i < n; ++i) x = __dadd_rn(x, a);
+    for (int i = 0; i < n; ++i) { x = __dadd_rn(x, b); x = __dadd_rn(x, -b); x = __dadd_rn(x, b); x = __dadd_rn(x, -b); }
     long long t1 = clock64();
-    out[0] = x;
-    cyc[0] = t1 - t0;
+    double y = a;
+    for (int i = 0; i < n; ++i) { y = __shfl_up_sync(0xffffffffu, y, 1) + 0.0; }
+    long long t2 = clock64();
+    float z = (float)a; 
+    for (int i = 0; i < n; ++i) { z = __fadd_rn(z, (float)b); z = __fadd_rn(z, (float)-b); z = __fadd_rn(z, (float)b); z = __fadd_rn(z, (float)-b); }
+    long long t3 = clock64();
+    int u = (int)a;
+    for (int i = 0; i < n; ++i) { u = __shfl_sync(0xffffffffu, u, (threadIdx.x + 1) & 31); }
+    long long t4 = clock64();
+    out[threadIdx.x] = x + y + z + u;
+    if (threadIdx.x == 0) { cyc[0] = t1 - t0; cyc[1] = t2 - t1; cyc[2] = t3 - t2; cyc[3] = t4 - t3; }
 }
-__global__ void k_fadd(float* out, long long* cyc, float a, int n) {
-    float x = a;
-    long long t0 = clock64();
-    for (int i = 0; i < n; ++i) x = __fadd_rn(x, a);
-    long long t1 = clock64();
-    out[0] = x;
-    cyc[0] = t1 - t0;
-}
-__global__ void k_shfl(double* out, long long* cyc, double a, int n) {
-    double x = a + threadIdx.x;
-    long long t0 = clock64();
-    for (int i = 0; i < n; ++i) x = __shfl_up_sync(0xffffffffu, x, 1);
-    long long t1 = clock64();
-    out[threadIdx.x] = x;
-    if (threadIdx.x == 0) cyc[0] = t1 - t0;
-}
-__global__ void k_shfl_dadd(double* out, long long* cyc, double a, int n) {
-    double x = a + threadIdx.x;
-    long long t0 = clock64();
-    for (int i = 0; i < n; ++i) x = __dadd_rn(__shfl_up_sync(0xffffffffu, x, 1), a);
-    long long t1 = clock64();
-    out[threadIdx.x] = x;
-    if (threadIdx.x == 0) cyc[0] = t1 - t0;
-}
-
 int main() {
-    double* d; float* f; long long* c;
-    cudaMalloc(&d, 1024); cudaMalloc(&f, 1024); cudaMalloc(&c, 64);
-    const int n = 4096;
-    long long h;
-    k_dadd<<<1, 1>>>(d, c, 1.0000001, n); cudaDeviceSynchronize();
-    k_dadd<<<1, 1>>>(d, c, 1.0000001, n); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
-    printf("DADD dependent: %.2f cycles\n", double(h) / n);
-    k_fadd<<<1, 1>>>(f, c, 1.0001f, n); cudaDeviceSynchronize();
-    k_fadd<<<1, 1>>>(f, c, 1.0001f, n); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
-    printf("FADD dependent: %.2f cycles\n", double(h) / n);
-    k_shfl<<<1, 32>>>(d, c, 1.0, n); cudaDeviceSynchronize();
-    k_shfl<<<1, 32>>>(d, c, 1.0, n); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
-    printf("SHFL.UP f64 dependent: %.2f cycles\n", double(h) / n);
-    k_shfl_dadd<<<1, 32>>>(d, c, 1.0, n); cudaDeviceSynchronize();
-    k_shfl_dadd<<<1, 32>>>(d, c, 1.0, n); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
-    printf("SHFL.UP f64 + DADD dependent: %.2f cycles\n", double(h) / n);
+    double* o; long long* c; cudaMalloc(&o, 256); cudaMallocManaged(&c, 64);
+    int n = 4096;
+    k<<<1, 32>>>(o, c, 1.0, 0.5, n); cudaDeviceSynchronize();
+    k<<<1, 32>>>(o, c, 1.0, 0.5, n); cudaDeviceSynchronize();
+    printf("DADD dep latency %.2f cyc, shfl_up(f64)+DADD %.2f cyc, FADD %.2f cyc, shfl(u32) %.2f cyc\n",
+           c[0] / (4.0 * n), c[1] / (double)n, c[2] / (4.0 * n), c[3] / (double)n);
     return 0;
 }
