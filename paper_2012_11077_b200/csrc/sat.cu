@@ -519,15 +519,15 @@ sat_systolic_kernel(SatLaunch L) {
 // later into lane-private slots, and writes back, from a lane-private 8-row
 // delay ring, the row it finished 8..15 steps earlier. The same three additions
 // per cell in the same order (sat.cpp:33): bit-identical tables.
-constexpr int kCtaSync = 8;                      // steps per unrolled block (one CTA barrier each)
+constexpr int kCtaSync = 8;                      // steps per block (one CTA barrier each)
 constexpr int kCtaSkew = kWarp + kCtaSync;       // steps between adjacent strips
 constexpr int kCtaEdgeRing = 64;                 // edge ring rows (>= kCtaSkew + kCtaSync, power of 2)
-constexpr int kCtaAhead = 8;                     // staging distance (steps)
-constexpr int kCtaXSlots = 16;                   // lane-private source slots
-constexpr int kCtaOSlots = 8;                    // lane-private result delay slots
-constexpr int kCtaMaxWarps = 12;                 // strips per CTA (shared memory)
+constexpr int kCtaXSlots = 24;                   // lane-private source slots (copy index mod 24)
+constexpr int kCtaOSlots = 16;                   // lane-private result slots (step mod 16)
+constexpr int kCtaMaxWarps = 12;                 // launch bound; the shared memory caps fp64 / fp32 at 11 / 7
+constexpr size_t kCtaSmemCap = 227 * 1024;
 static_assert(kCtaEdgeRing >= kCtaSkew + kCtaSync && kCtaSync < kWarp, "edge ring / barrier spacing");
-static_assert(kCtaXSlots >= kCtaAhead + 8 && kCtaSkew % kCtaSync == 0, "staging ring / block alignment");
+static_assert(kCtaSkew % kCtaSync == 0, "block alignment");
 
 template <typename T>
 __host__ __device__ constexpr int cta_cpl() { return 16 / static_cast<int>(sizeof(T)); }
@@ -536,22 +536,38 @@ constexpr size_t cta_smem_per_warp() {
     return kCtaXSlots * kWarp * 16 + kCtaOSlots * kWarp * cta_cpl<T>() * sizeof(double) +
            kCtaEdgeRing * sizeof(double);
 }
+constexpr size_t kCtaSmemExtra = 16 + 2 * kCtaEdgeRing * sizeof(double); // alignment, zero and scratch edge rows
+template <typename T>
+constexpr int cta_max_warps() {
+    return static_cast<int>((kCtaSmemCap - kCtaSmemExtra) / cta_smem_per_warp<T>()) < kCtaMaxWarps
+               ? static_cast<int>((kCtaSmemCap - kCtaSmemExtra) / cta_smem_per_warp<T>())
+               : kCtaMaxWarps;
+}
 
+// Per block of kCtaSync steps a warp (i) issues, per lane group g, the cp.async
+// copies of the 8 rows it needs in the next block (copy index q: group g copies
+// row q - 8g into slot q mod 24; lane j of the group reads index s - j at step
+// s; indices s0 - 7 .. s0 + 15 are live during a block), (ii) runs 8 systolic steps whose only shared-memory traffic is plain
+// loads / stores of lane-private slots, so the compiler is free to overlap
+// consecutive steps (no asm memory clobber inside), and (iii) writes back the 8
+// rows its groups finished (group g: rows s0 - 8g - 7 .. s0 - 8g), 128-byte
+// lines per group.
 template <typename T>
 __global__ void __launch_bounds__(kCtaMaxWarps * kWarp, 1) sat_cta_kernel(SatLaunch L) {
     constexpr int kC = cta_cpl<T>();
-    constexpr unsigned kXSlot = kWarp * 16;                     // bytes per source slot
-    constexpr unsigned kOSlot = kWarp * kC * sizeof(double);    // bytes per result slot
     extern __shared__ __align__(16) unsigned char cta_smem_raw[];
     const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
     const int grp = lane >> 3, j = lane & 7;
     const int n_warps = blockDim.x / kWarp; // == strips of this table
-    const unsigned base = (smem_u32(cta_smem_raw) + 15u) & ~15u;
-    const unsigned x_lane = base + static_cast<unsigned>(warp) * kCtaXSlots * kXSlot + lane * 16u;
-    const unsigned o_base = base + static_cast<unsigned>(n_warps) * kCtaXSlots * kXSlot;
-    const unsigned o_lane = o_base + static_cast<unsigned>(warp) * kCtaOSlots * kOSlot + lane * 16u;
-    double* edge = reinterpret_cast<double*>(cta_smem_raw + (o_base - smem_u32(cta_smem_raw)) +
-                                             static_cast<size_t>(n_warps) * kCtaOSlots * kOSlot);
+    unsigned char* sm = cta_smem_raw + ((16u - (smem_u32(cta_smem_raw) & 15u)) & 15u);
+    // x ring [warp][slot][lane] of 16 bytes; o ring [warp][slot][lane] of kC doubles; edge ring [warp][row]
+    T* xr = reinterpret_cast<T*>(sm) + (static_cast<size_t>(warp) * kCtaXSlots * kWarp + lane) * kC;
+    double* orr = reinterpret_cast<double*>(sm + static_cast<size_t>(n_warps) * kCtaXSlots * kWarp * 16) +
+                  (static_cast<size_t>(warp) * kCtaOSlots * kWarp + lane) * kC;
+    double* edge = reinterpret_cast<double*>(sm + static_cast<size_t>(n_warps) *
+                                                      (kCtaXSlots * kWarp * 16 + kCtaOSlots * kWarp * kC * 8));
+    constexpr int kXStride = kWarp * kC; // elements between x slots of a lane
+    constexpr int kOStride = kWarp * kC; // doubles between o slots of a lane
     const SatJobView J = sat_job(L, blockIdx.x);
     const int rows = static_cast<int>(J.rows);
     const int cols = static_cast<int>(L.cols);
@@ -563,96 +579,126 @@ __global__ void __launch_bounds__(kCtaMaxWarps * kWarp, 1) sat_cta_kernel(SatLau
     for (int k = 0; k < nvalid; ++k) table[kTabShift + 1 + c + k] = 0.0; // padded row 0
     if (warp == 0 && lane == 0) table[kTabShift] = 0.0;
     const bool vec = nvalid == kC && L.vec_ok;
-    const bool full = __all_sync(0xffffffffu, vec); // every lane: 16 aligned source bytes in the map
-    double* edge_in = warp > 0 ? edge + (warp - 1) * kCtaEdgeRing : nullptr;
-    double* edge_out = warp + 1 < n_warps ? edge + warp * kCtaEdgeRing : nullptr;
-
-    // group g stages source row s + kCtaAhead - 8g at local step s into slot (s + kCtaAhead) mod 16
-    auto stage = [&](int s, bool checked) {
-        const int r = s + kCtaAhead - 8 * grp;
-        if (checked && (r < 0 || r >= rows || nvalid == 0)) return;
-        const unsigned dst = x_lane + static_cast<unsigned>((s + kCtaAhead) & (kCtaXSlots - 1)) * kXSlot;
-        const T* p = src + static_cast<int64_t>(r) * ld;
-        if (!checked || vec) {
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(p) : "memory");
-        } else {
-            for (int k = 0; k < nvalid; ++k) cp_async_one(dst + k * sizeof(T), p + k);
-        }
+    // edge rings: row r of strip w at edge[w][r mod 64]; strip 0 reads the zero
+    // row (slot n_warps), the last strip writes a scratch row (slot n_warps + 1)
+    double* zero_row = edge + n_warps * kCtaEdgeRing;
+    const double* edge_in = warp > 0 ? edge + (warp - 1) * kCtaEdgeRing : zero_row;
+    double* edge_out = warp + 1 < n_warps ? edge + warp * kCtaEdgeRing : zero_row + kCtaEdgeRing;
+    for (int i = threadIdx.x; i < kCtaEdgeRing; i += blockDim.x) zero_row[i] = 0.0;
+    __syncthreads();
+    const unsigned x_smem = smem_u32(xr);
+    auto mod_x = [](int q) { // q mod kCtaXSlots for q >= -kCtaXSlots
+        const int m = q % kCtaXSlots;
+        return m < 0 ? m + kCtaXSlots : m;
     };
-    double prev[kC], last[kC];
-#pragma unroll
-    for (int k = 0; k < kC; ++k) prev[k] = last[k] = 0.0;
-    double left_prev = 0.0;
-    T xn[kC]; // source of the next step (loaded one step ahead)
-#pragma unroll
-    for (int k = 0; k < kC; ++k) xn[k] = T(0);
-    // local steps [-kCtaSync, s_end): staging starts kCtaAhead steps before row 0,
-    // the delay ring drains 8 * 3 + 8 steps after the last row
-    const int s_end = rows + kWarp + 4 * 8;
-    const int skew = kCtaSkew * warp;
-    const int n_blocks = (s_end + kCtaSync + kCtaSkew * (n_warps - 1) + kCtaSync - 1) / kCtaSync;
-
-    auto block = [&](const int s0, auto checked_tag) {
+    // copies of indices [q0, q0 + 8) by my group: row q - 8g, slot q mod 24
+    // (checked: rows outside the map are skipped; a lane with fewer than kC
+    // columns inside the map copies element by element)
+    auto stage8 = [&](int q0, auto checked_tag) {
         constexpr bool kChecked = decltype(checked_tag)::value;
+        const int slot0 = mod_x(q0);
+        const int r0 = q0 - 8 * grp;
+        const T* p = src + static_cast<int64_t>(r0) * ld;
+        unsigned dst = x_smem + static_cast<unsigned>(slot0) * kXStride * sizeof(T);
+        constexpr unsigned kSlotBytes = kXStride * sizeof(T);
+#pragma unroll
+        for (int u = 0; u < kCtaSync; ++u) {
+            const bool row_ok = !kChecked || (r0 + u >= 0 && r0 + u < rows);
+            if (row_ok && vec) {
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(p) : "memory");
+            } else if (row_ok) {
+                for (int k = 0; k < nvalid; ++k) cp_async_one(dst + k * sizeof(T), p + k);
+            }
+            p += ld;
+            dst = slot0 + u + 1 == kCtaXSlots ? dst + kSlotBytes - kCtaXSlots * kSlotBytes : dst + kSlotBytes;
+        }
+        cp_async_commit();
+    };
+    double prev[kC];
+#pragma unroll
+    for (int k = 0; k < kC; ++k) prev[k] = 0.0;
+    double left_prev = 0.0;
+    // local steps from -8 (the first copies: index 0 = group 0's row 0) to the
+    // last write-back (row rows - 1 of group 3 after step rows - 1 + 31)
+    const int s_first = -kCtaSync;
+    const int s_end = rows + kWarp + kCtaSync;
+    const int skew = kCtaSkew * warp;
+    const int n_blocks = (s_end - s_first + kCtaSkew * (n_warps - 1) + kCtaSync - 1) / kCtaSync;
+
+    // 8 systolic steps: branch-free (state updates by select, stores by
+    // predicate), so the compiler overlaps a step's loads and x + S(r-1, .) adds
+    // with the previous step's dependent chain
+    auto steps8 = [&](const int s0, auto checked_tag) {
+        constexpr bool kChecked = decltype(checked_tag)::value;
+        const int xbase = mod_x(s0 - j); // slot of step s0
 #pragma unroll
         for (int u = 0; u < kCtaSync; ++u) {
             const int s = s0 + u;
             const int r = s - lane;
-            // (1) group g writes back row s - 8g - 8 (computed 1..8 steps ago, slot (s + j) mod 8)
-            {
-                const int rf = s - 8 * grp - 8;
-                if (!kChecked || (rf >= 0 && rf < rows)) {
-                    double o[kC];
-                    lds_out<kC>(o_lane + static_cast<unsigned>((s + j) & (kCtaOSlots - 1)) * kOSlot, o);
-                    double* dst = table + static_cast<int64_t>(rf + 1) * tld + kTabShift + 1 + c;
-                    if (!kChecked || nvalid == kC) {
-#pragma unroll
-                        for (int q = 0; q < kC / 2; ++q)
-                            reinterpret_cast<double2*>(dst)[q] = make_double2(o[2 * q], o[2 * q + 1]);
-                    } else {
-                        for (int k = 0; k < nvalid; ++k) dst[k] = o[k];
-                    }
-                }
-            }
-            // (2) stage the source row needed kCtaAhead..+7 steps later
-            stage(s, kChecked);
-            cp_async_commit();
-            // (3) this step's source was loaded last step; load the next step's
-            T x[kC];
-#pragma unroll
-            for (int k = 0; k < kC; ++k) x[k] = xn[k];
-            cp_async_wait<kCtaAhead - 1>();
-            lds_lane<kC>(x_lane + static_cast<unsigned>((s + 1 - j) & (kCtaXSlots - 1)) * kXSlot, xn);
-            // (4) x + S(r-1, .) before the left neighbour arrives
-            double a[kC];
-#pragma unroll
-            for (int k = 0; k < kC; ++k) a[k] = dadd(widen(x[k]), prev[k]);
             const bool act = !kChecked || (r >= 0 && r < rows);
-            double left = __shfl_up_sync(0xffffffffu, last[kC - 1], 1);
-            if (lane == 0) left = (edge_in && act) ? edge_in[r & (kCtaEdgeRing - 1)] : 0.0;
+            const int xslot = xbase + u < kCtaXSlots ? xbase + u : xbase + u - kCtaXSlots;
+            const T* xs = xr + xslot * kXStride;
+            double a[kC]; // x + S(r-1, .): independent of the left neighbour
+#pragma unroll
+            for (int k = 0; k < kC; ++k) a[k] = dadd(widen(xs[k]), prev[k]);
+            double left = __shfl_up_sync(0xffffffffu, prev[kC - 1], 1);
+            const double e = edge_in[s & (kCtaEdgeRing - 1)]; // lane 0's row is s (broadcast load)
+            if (lane == 0) left = e;
+            if (kChecked && !act) left = 0.0;
             double sv[kC];
             sv[0] = dsub(dadd(a[0], left), left_prev);
 #pragma unroll
             for (int k = 1; k < kC; ++k) sv[k] = dsub(dadd(a[k], sv[k - 1]), prev[k - 1]);
+            double* o = orr + (s & (kCtaOSlots - 1)) * kOStride;
             if (act) {
-                sts_out<kC>(o_lane + static_cast<unsigned>(s & (kCtaOSlots - 1)) * kOSlot, sv);
-                if (lane == kWarp - 1 && edge_out) edge_out[r & (kCtaEdgeRing - 1)] = sv[kC - 1];
-                if (warp == 0 && lane == 0) table[static_cast<int64_t>(r + 1) * tld + kTabShift] = 0.0;
-                left_prev = left;
 #pragma unroll
-                for (int k = 0; k < kC; ++k) prev[k] = last[k] = sv[k];
+                for (int k = 0; k < kC; ++k) o[k] = sv[k];
             }
+            if (lane == kWarp - 1 && act) edge_out[r & (kCtaEdgeRing - 1)] = sv[kC - 1];
+            left_prev = act ? left : left_prev;
+#pragma unroll
+            for (int k = 0; k < kC; ++k) prev[k] = act ? sv[k] : prev[k];
         }
     };
-    // prologue: stage the rows of local steps before -kCtaSync (group 0: row 0 at
-    // step -kCtaAhead is the first real copy; nothing earlier is needed)
+    // write back the rows my group finished: s0 - 8g - 7 .. s0 - 8g (row r of lane
+    // 8g + j sits in slot (r + 8g + j) mod 16)
+    auto flush8 = [&](const int s0, auto checked_tag) {
+        constexpr bool kChecked = decltype(checked_tag)::value;
+        const int rf0 = s0 - 8 * grp - 7;
+        double* dst = table + static_cast<int64_t>(rf0 + 1) * tld + kTabShift + 1 + c;
+#pragma unroll
+        for (int u = 0; u < kCtaSync; ++u) {
+            const int rf = rf0 + u;
+            if (!kChecked || (rf >= 0 && rf < rows)) {
+                const double* o = orr + ((rf + lane) & (kCtaOSlots - 1)) * kOStride;
+                if (nvalid == kC) {
+#pragma unroll
+                    for (int q = 0; q < kC / 2; ++q)
+                        reinterpret_cast<double2*>(dst)[q] = reinterpret_cast<const double2*>(o)[q];
+                } else {
+                    for (int k = 0; k < nvalid; ++k) dst[k] = o[k];
+                }
+                if (warp == 0 && lane == 0) dst[-1] = 0.0; // padded column 0
+            }
+            dst += tld;
+        }
+    };
 #pragma unroll 1
     for (int b = 0; b < n_blocks; ++b) {
-        const int s0 = b * kCtaSync - kCtaSync - skew; // local step of this block
-        if (s0 + kCtaSync > -kCtaSync && s0 < s_end) {
-            const bool interior = full && s0 >= kWarp && s0 + 2 * kCtaSync <= rows;
-            if (interior) block(s0, std::integral_constant<bool, false>{});
-            else block(s0, std::integral_constant<bool, true>{});
+        const int s0 = s_first + b * kCtaSync - skew; // my first local step in this block
+        if (s0 + kCtaSync > s_first && s0 < s_end) {
+            // staged rows s0 + 8 - 24 .. s0 + 15, computed rows s0 - 31 .. s0 + 7,
+            // written-back rows s0 - 31 .. s0 all inside [0, rows)
+            const bool interior = s0 >= kWarp && s0 + 2 * kCtaSync <= rows;
+            if (interior) stage8(s0 + kCtaSync, std::integral_constant<bool, false>{}); // used in the next block
+            else stage8(s0 + kCtaSync, std::integral_constant<bool, true>{});
+            cp_async_wait<1>(); // this block's copies may still fly
+            __syncwarp();
+            if (interior) steps8(s0, std::integral_constant<bool, false>{});
+            else steps8(s0, std::integral_constant<bool, true>{});
+            __syncwarp();
+            if (interior) flush8(s0, std::integral_constant<bool, false>{});
+            else flush8(s0, std::integral_constant<bool, true>{});
         }
         __syncthreads();
     }
@@ -660,7 +706,7 @@ __global__ void __launch_bounds__(kCtaMaxWarps * kWarp, 1) sat_cta_kernel(SatLau
     // non-finite inputs poison every later S of their column (see the header)
     bool finite = true;
 #pragma unroll
-    for (int k = 0; k < kC; ++k) finite &= k >= nvalid || isfinite(last[k]);
+    for (int k = 0; k < kC; ++k) finite &= k >= nvalid || isfinite(prev[k]);
     if (!finite && J.nonfinite) {
         int col = c;
         const int bad = first_nonfinite<T>(static_cast<const T*>(J.src), ld, c, nvalid, rows, &col);
@@ -679,7 +725,7 @@ template <typename T>
 static bool launch_sat_cta(const SatLaunch& L, cudaStream_t stream, cudaError_t* err) {
     if (L.need || !sat_cta_eligible(L.n_jobs, L.cols, sizeof(T) == 4 ? UWB_F32 : UWB_F64)) return false;
     const int warps = static_cast<int>((L.cols + kWarp * cta_cpl<T>() - 1) / (kWarp * cta_cpl<T>()));
-    const size_t smem = 16 + static_cast<size_t>(warps) * cta_smem_per_warp<T>();
+    const size_t smem = kCtaSmemExtra + static_cast<size_t>(warps) * cta_smem_per_warp<T>();
     *err = cudaFuncSetAttribute(sat_cta_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (*err != cudaSuccess) return true;
     ++g_kernel_launches;
@@ -772,7 +818,8 @@ bool sat_cta_eligible(int64_t n_jobs, int64_t cols, int dtype) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t strip_cols = kWarp * (dtype == UWB_F32 ? cta_cpl<float>() : cta_cpl<double>());
-    return n_jobs >= 1 && n_jobs <= sms && (cols + strip_cols - 1) / strip_cols <= kCtaMaxWarps;
+    const int max_warps = dtype == UWB_F32 ? cta_max_warps<float>() : cta_max_warps<double>();
+    return n_jobs >= 1 && n_jobs <= sms && (cols + strip_cols - 1) / strip_cols <= max_warps;
 }
 
 int64_t sat_strips(int64_t cols, int cpl) { return (cols + kWarp * cpl - 1) / (kWarp * cpl); }
