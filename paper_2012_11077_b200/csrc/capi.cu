@@ -157,7 +157,7 @@ struct Plan {
     size_t off_tables, off_edge, off_prog, off_counter, off_scratch;
     // certified-decision CFAR (cfar_cert.cu): candidate lists, status, tap bitmap, K/E table
     int64_t cand_cap, need_rows, n_int;
-    size_t off_cand, off_cand_count, off_status, off_need, off_ke, total;
+    size_t off_cand, off_cand_count, off_status, off_need, off_ke, off_flagged, total;
 };
 
 // win == nullptr: the batch holds whole maps. Otherwise the batch buffer holds
@@ -238,6 +238,7 @@ Plan make_plan(const uwb_map_batch& b, const uwb_cfar_params* p, int sat_mode, u
         P.off_status = take(sizeof(unsigned) * P.n_maps);
         P.off_need = take(sizeof(unsigned) * P.sat_jobs * P.strips * P.need_rows);
         P.off_ke = take(sizeof(float4) * (P.n_int + 1));
+        P.off_flagged = take(sizeof(unsigned) * (P.n_maps + 1)); // [0] count, [1..] maps
     }
     P.total = off;
     return P;
@@ -356,6 +357,8 @@ CertLaunch cert_launch(const Plan& P, const uwb_map_batch& b, const uwb_cfar_par
     L.cand_count = reinterpret_cast<unsigned*>(ws + P.off_cand_count);
     L.cand_cap = P.cand_cap;
     L.status = reinterpret_cast<unsigned*>(ws + P.off_status);
+    L.flagged_count = reinterpret_cast<unsigned*>(ws + P.off_flagged);
+    L.flagged = L.flagged_count + 1;
     L.first_bad = reinterpret_cast<unsigned long long*>(o.first_bad);
     L.need = reinterpret_cast<unsigned*>(ws + P.off_need);
     L.need_rows = P.need_rows;
@@ -433,6 +436,7 @@ uwb_status dev_cfar(const uwb_map_batch& b, const uwb_cfar_params& p, const doub
         const CertLaunch CL = cert_launch(P, b, p, alpha, ws, o);
         UWB_CUDA_TRY(cudaMemsetAsync(CL.cand_count, 0, sizeof(unsigned) * P.n_maps, s));
         UWB_CUDA_TRY(cudaMemsetAsync(CL.status, 0, sizeof(unsigned) * P.n_maps, s));
+        UWB_CUDA_TRY(cudaMemsetAsync(CL.flagged_count, 0, sizeof(unsigned), s));
         UWB_CUDA_TRY(cudaMemsetAsync(CL.need, 0, sizeof(unsigned) * P.sat_jobs * P.strips * P.need_rows, s));
         UWB_CUDA_TRY(cudaMemset2DAsync(o.mask_bits, sizeof(uint32_t) * o.mask_map_stride, 0,
                                        sizeof(uint32_t) * o.words_per_row * P.geo.out_rows(), b.n_maps, s));
@@ -458,8 +462,9 @@ uwb_status dev_cfar(const uwb_map_batch& b, const uwb_cfar_params& p, const doub
         // maps the certificate could not cover (values outside its range, or
         // more candidates than the list holds) have full tables: exact kernel
         CfarLaunch FL = cfar_launch(P, b, p, alpha, ws, o);
-        FL.map_filter = CL.status;
-        UWB_CUDA_TRY(launch_cfar_integral(FL, b.dtype, s));
+        FL.flagged_maps = CL.flagged;
+        FL.flagged_count = CL.flagged_count;
+        UWB_CUDA_TRY(launch_cfar_integral_filtered(FL, b.dtype, s));
         if (o.cert_status)
             UWB_CUDA_TRY(cudaMemcpyAsync(o.cert_status, CL.status, sizeof(uint32_t) * b.n_maps,
                                          cudaMemcpyDeviceToDevice, s));

@@ -36,12 +36,9 @@ __device__ __forceinline__ double tap(const double* t, int64_t ld, int64_t i, in
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kCfarThreads)
-cfar_integral_kernel(CfarLaunch L) {
-    const int64_t job = blockIdx.y;
+__device__ __forceinline__ void cfar_integral_tile(const CfarLaunch& L, const int64_t job) {
     const int64_t map = job / L.geo.n_slabs;
     const int64_t slab = job % L.geo.n_slabs;
-    if (L.map_filter && !L.map_filter[map]) return; // certified path: only flagged maps
     const int col_tile = static_cast<int>(blockIdx.x % L.col_tiles);
     const int chunk = static_cast<int>(blockIdx.x / L.col_tiles);
     const int c = col_tile * kCfarThreads + static_cast<int>(threadIdx.x);
@@ -83,6 +80,22 @@ cfar_integral_kernel(CfarLaunch L) {
         }
         emit_cells(L, map, r, c, col_ok, hit, v, thr);
     }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kCfarThreads)
+cfar_integral_kernel(CfarLaunch L) {
+    if (!L.flagged_count) {
+        cfar_integral_tile<T>(L, blockIdx.y);
+        return;
+    }
+    // certified path's exact fallback: a short grid strides over the jobs of
+    // the maps the certificate flagged (compacted by cert_resolve_kernel;
+    // usually none)
+    const int64_t n = static_cast<int64_t>(*L.flagged_count) * L.geo.n_slabs;
+    for (int64_t i = blockIdx.y; i < n; i += gridDim.y)
+        cfar_integral_tile<T>(L, static_cast<int64_t>(L.flagged_maps[i / L.geo.n_slabs]) * L.geo.n_slabs +
+                                     i % L.geo.n_slabs);
 }
 
 // cfar.cpp:200-216: explicit ring loop, row-major accumulation order.
@@ -322,6 +335,23 @@ cudaError_t launch_cfar_integral(const CfarLaunch& L0, int dtype, cudaStream_t s
     if (e != cudaErrorNotSupported) return e;
     dim3 grid;
     const CfarLaunch L = grid_shape(L0, grid);
+    ++g_kernel_launches;
+    if (dtype == UWB_F32) cfar_integral_kernel<float><<<grid, kCfarThreads, 0, stream>>>(L);
+    else cfar_integral_kernel<double><<<grid, kCfarThreads, 0, stream>>>(L);
+    return cudaGetLastError();
+}
+
+// The certified path's exact fallback over the flagged maps (L.flagged_maps,
+// *L.flagged_count, written on the device): a grid of at most kFilteredJobs job
+// rows striding over them, so a batch with nothing flagged costs one small
+// launch (the ring kernel's full grid of early-exiting CTAs took ~0.13 ms for
+// 4096 maps).
+cudaError_t launch_cfar_integral_filtered(const CfarLaunch& L0, int dtype, cudaStream_t stream) {
+    if (L0.n_jobs == 0 || L0.cols == 0 || L0.geo.rows == 0) return cudaSuccess;
+    constexpr int64_t kFilteredJobs = 8;
+    dim3 grid;
+    const CfarLaunch L = grid_shape(L0, grid);
+    grid.y = static_cast<unsigned>(L.n_jobs < kFilteredJobs ? L.n_jobs : kFilteredJobs);
     ++g_kernel_launches;
     if (dtype == UWB_F32) cfar_integral_kernel<float><<<grid, kCfarThreads, 0, stream>>>(L);
     else cfar_integral_kernel<double><<<grid, kCfarThreads, 0, stream>>>(L);

@@ -306,6 +306,7 @@ cert_kernel(const __grid_constant__ CertLaunch L) {
     uint32_t vo = LO * 4u * L.bits_magic, vg = LG * 4u * L.bits_magic;
     Raw mx = 0; // largest raw value: out-of-range values compare >= bits(X_lim)
     const float4 kin = __ldg(L.ke + L.n_int); // interior constants (the largest K_n and E_n)
+    const int l2t = L.l2_ahead_t;             // L2 prefetch distance (tile-rows)
     const char* pnext = row_ptr(2 * (K0 + kPT)); // the tile-row the next step prefetches
     const int n_items = I_e - I_s;
     const int n_phases = LAG + (n_items + kTB - 1) / kTB;
@@ -336,8 +337,8 @@ cert_kernel(const __grid_constant__ CertLaunch L) {
                 if (safe) {
                     ra[u] = IO::load2(pu);
                     rb[u] = IO::load2(pu + ld_t);
-                    if ((u & 3) == 0 && col_ok && r0 + 2 * kL2AheadT < rb_hi)
-                        asm volatile("prefetch.global.L2 [%0];" ::"l"(pu + 2 * kL2AheadT * ld_t));
+                    if ((u & 3) == 0 && col_ok && l2t > 0 && r0 + 2 * l2t < rb_hi)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(pu + 2 * l2t * ld_t));
                 } else {
                     ra[u] = (r0 >= rb_lo && r0 < rb_hi) ? IO::load2(pu) : IO::zero2();
                     rb[u] = (r0 + 1 >= rb_lo && r0 + 1 < rb_hi) ? IO::load2(pu + ld_t) : IO::zero2();
@@ -525,8 +526,11 @@ __global__ void cert_mark_kernel(const __grid_constant__ CertLaunch L) {
 template <typename T>
 __global__ void cert_resolve_kernel(const __grid_constant__ CertLaunch L) {
     const int64_t map = blockIdx.x;
-    if (L.status[map]) {
-        if (blockIdx.y == 0 && threadIdx.x == 0 && L.tie_counts) L.tie_counts[map] = ~0ull;
+    if (L.status[map]) { // the exact path decides this map (launch_cfar_integral_filtered)
+        if (blockIdx.y == 0 && threadIdx.x == 0) {
+            if (L.tie_counts) L.tie_counts[map] = ~0ull;
+            L.flagged[atomicAdd(L.flagged_count, 1u)] = static_cast<unsigned>(map);
+        }
         return;
     }
     const unsigned n_c = min(L.cand_count[map], static_cast<unsigned>(L.cand_cap));
@@ -597,6 +601,8 @@ cudaError_t go_cert(CertLaunch L, cudaStream_t stream) {
     L.ring_off = static_cast<uint32_t>(static_cast<uint64_t>(Geo::R.lo * Geo::C.lo - Geo::R.lg * Geo::C.lg) * 4u *
                                        L.bits_magic);
     chunk_rows(L);
+    L.l2_ahead_t = kL2AheadT;
+    if (const char* e = UWB_KNOB("UWB_CERT_L2AHEAD")) L.l2_ahead_t = atoi(e);
     auto kern = cert_kernel<T, HR, GR, HC, GC>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Geo::smem));
     if (e != cudaSuccess) return e;

@@ -155,7 +155,6 @@ cfar_ws_kernel(const __grid_constant__ CfarLaunch L, const __grid_constant__ CUt
     const int64_t job = blockIdx.y;
     const int64_t map = job / L.geo.n_slabs;
     const int64_t slab = job % L.geo.n_slabs;
-    if (L.map_filter && !L.map_filter[map]) return; // certified path: only flagged maps
     const int col_tile = static_cast<int>(blockIdx.x % L.col_tiles);
     const int chunk = static_cast<int>(blockIdx.x / L.col_tiles);
     const int rows = static_cast<int>(L.geo.rows), cols = static_cast<int>(L.cols);

@@ -108,6 +108,7 @@ struct SatLaunch {
     int64_t need_rows;
     const unsigned* map_full;
     int64_t jobs_per_map; // SAT jobs per map (n_slabs * n_bands)
+    int l2_ahead;         // sparse mode: L2 prefetch distance in rows (set by the launcher)
 };
 
 struct SatJobView {
@@ -167,7 +168,9 @@ struct CfarLaunch {
     int ring_ahead;      // CFAR ring: table groups of look-ahead beyond the window
     int pf_groups;       // CFAR ring: L2 prefetch distance of both streams (groups)
     int64_t col_tiles;
-    const unsigned* map_filter; // non-null: only maps with map_filter[map] != 0 run
+    // launch_cfar_integral_filtered: the flagged maps, compacted on the device
+    const unsigned* flagged_maps;
+    const unsigned* flagged_count;
 };
 
 // Certified-decision CFAR (cfar_cert.cu): one launch description shared by the
@@ -192,8 +195,11 @@ struct CertLaunch {
     unsigned* cand_count;
     int64_t cand_cap;
     unsigned* status;    // per map: bit 0 list overflow, bit 1 value outside the certified range
+    unsigned* flagged;   // the maps with status != 0, compacted by cert_resolve_kernel
+    unsigned* flagged_count;
     unsigned long long* first_bad;
     int64_t col_ctas, row_chunk, row_chunks;
+    int l2_ahead_t;      // L2 prefetch distance of the certify pass (tile-rows; set by the launcher)
     // sparse-table taps
     unsigned* need;
     int64_t need_rows, strips;
@@ -218,6 +224,8 @@ int sat_cpl_for(int64_t n_jobs, int64_t cols);   // columns per lane for a batch
 bool sat_cta_eligible(int64_t n_jobs, int64_t cols, int dtype);
 
 cudaError_t launch_cfar_integral(const CfarLaunch& L, int dtype, cudaStream_t stream);
+// the same over the flagged maps L.flagged_maps[0 .. *L.flagged_count) only (certified path's exact fallback)
+cudaError_t launch_cfar_integral_filtered(const CfarLaunch& L, int dtype, cudaStream_t stream);
 // SAT + CFAR in one kernel, table kept on chip (cfar_fused.cu). Whole-map
 // batches only; cudaErrorNotSupported when the geometry does not qualify.
 cudaError_t launch_cfar_fused(const SatLaunch& S, const CfarLaunch& C, int dtype, cudaStream_t stream);

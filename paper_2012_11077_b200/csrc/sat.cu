@@ -52,7 +52,7 @@ constexpr int kAhead = 8;               // staging distance in steps (<= kXSlots
 constexpr int kXSlots = 16;             // lane-private source ring (copy steps)
 constexpr int kOSlots = 8;              // lane-private result delay ring (rows)
 constexpr int kPublishEvery = 64;       // steps between edge hand-overs
-constexpr int kL2Ahead = 48;            // sparse mode: L2 prefetch distance (rows)
+constexpr int kL2Ahead = 0;             // sparse mode: L2 prefetch distance (rows); measured: 0 best (48: +3%, 96: +26%)
 constexpr int kSatCtasPerSm = 3;        // occupancy target (registers and shared memory)
 constexpr int kSatCtasPerSmSparse = 4;  // sparse mode: no result ring, <= 128 registers
 constexpr int kSatCtasPerSmSparseRun = 3; // ... of which 3 resident: measured 3.5% faster than 4 (cfg 3)
@@ -102,10 +102,12 @@ template <int kCpl>
 __device__ __forceinline__ void lds_lane(unsigned addr, float (&x)[kCpl]) {
     if constexpr (kCpl == 1) {
         asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x[0]) : "r"(addr));
-    } else if constexpr (kCpl == 4) {
-        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                     : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3])
-                     : "r"(addr));
+    } else if constexpr (kCpl % 4 == 0) {
+#pragma unroll
+        for (int q = 0; q < kCpl / 4; ++q)
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(x[4 * q]), "=f"(x[4 * q + 1]), "=f"(x[4 * q + 2]), "=f"(x[4 * q + 3])
+                         : "r"(addr + 16u * q));
     } else {
 #pragma unroll
         for (int q = 0; q < kCpl / 2; ++q)
@@ -224,6 +226,7 @@ sat_systolic_kernel(SatLaunch L) {
         // sparse mode: this strip's tap bitmap (one word per row, bit = lane);
         // a flagged map stores its whole table (the exact CFAR reads it)
         const unsigned* need_col = kSparse ? L.need + (job * L.strips + strip) * L.need_rows : nullptr;
+        const int l2_ahead = L.l2_ahead;
         const bool store_all = kSparse && L.map_full && L.map_full[job / L.jobs_per_map] != 0;
         const bool dense = !kSparse || store_all;
         // sparse mode: need words of the previous / current / next block of rows
@@ -370,8 +373,8 @@ sat_systolic_kernel(SatLaunch L) {
             cp_async_commit();
             // sparse mode is read-bound: pull the row kL2Ahead steps later into L2
             // (the 16-step staging ring alone does not cover the DRAM latency)
-            if (kSparse && kMode == 0 && s + kAhead - 8 * grp + kL2Ahead < rows) // interior steps
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(xrow + kL2Ahead * ld));
+            if (kSparse && kMode == 0 && l2_ahead > 0 && s + kAhead - 8 * grp + l2_ahead < rows) // interior steps
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(xrow + l2_ahead * ld));
             xrow += ld;
             // (3) this step's inputs were loaded one step ahead; load the next step's
             T x[kCpl];
@@ -747,10 +750,13 @@ static cudaError_t launch_sat_t(const SatLaunch& L, cudaStream_t stream) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarpsPerCta * kWarp, smem);
     // leave room for a concurrent CFAR on another stream (UWB_SAT_CTAS_PER_SM)
     if (kSparse) per_sm = std::min(per_sm, kSatCtasPerSmSparseRun);
+    SatLaunch Lp = L;
+    Lp.l2_ahead = kL2Ahead;
+    if (const char* e = UWB_KNOB("UWB_SAT_L2AHEAD")) Lp.l2_ahead = atoi(e);
     if (const char* e = UWB_KNOB("UWB_SAT_CTAS_PER_SM")) per_sm = std::min(per_sm, std::max(1, atoi(e)));
     const int64_t ctas = (n_tiles + kWarpsPerCta - 1) / kWarpsPerCta;
     int64_t grid = imin(ctas, static_cast<int64_t>(sms) * (per_sm > 0 ? per_sm : 1));
-    SatLaunch L2 = L;
+    SatLaunch L2 = Lp;
     // batches that cannot fill the resident warps are latency-bound on the strip chain
     if (n_tiles < 2LL * sms * (per_sm > 0 ? per_sm : 1) * kWarpsPerCta) L2.flags |= 2u;
     // at most one strip per SM: each strip gets an SM to itself
