@@ -374,6 +374,29 @@ def run_cfg1(args):
 
 
 # ------------------------------------------------------------------ config 2 --
+# Algorithmic fp64 operations per config-2 record (M = 512 fast-time samples x
+# N = 1024 traces, L = 1024, window 5, K = 25 band bins), the reference's
+# stages (pipeline.cpp:58-223): remove_dc 2M per trace, detrend_linear 6M per
+# trace (two moment sums, then r*slope + intercept subtracted), mean filter
+# (2h+1 adds + 1 division) per sample, normalise (1 division per sample + the
+# max), radix-2 FFT 5 L log2 L per row (10 ops per butterfly), |X|^2 3 per kept bin.
+_M2, _N2, _L2, _W2, _K2 = 512, 1024, 1024, 5, 25
+FE_FP64_OPS_PER_RECORD = (8 * _M2 * _N2 + (_W2 + 1) * _M2 * _N2 + 2 * _M2 * _N2 + 5 * _L2 * 10 * _M2
+                          + 3 * _K2 * _M2)
+
+
+def _fp64_peak():
+    """fp64 add throughput measured on the box (scripts/micro/fp64peak.cu,
+    profiles/r02_fp64_peak.json), else 148 SMs x 64 lanes x 1.965 GHz."""
+    import os
+    try:
+        with open(os.path.join(B.ROOT, "profiles", "r02_fp64_peak.json")) as f:
+            d = json.load(f)
+        return float(d["dadd_gops"]), "measured (profiles/r02_fp64_peak.json, scripts/micro/fp64peak.cu)"
+    except Exception:
+        return 148 * 64 * 1.965, "derived (148 SMs x 64 fp64 lanes x 1.965 GHz)"
+
+
 def run_cfg2(args):
     """Config 2 as a throughput config: a batch of raw fp32
     records through the batched device detect() (front end writing each band
@@ -393,10 +416,26 @@ def run_cfg2(args):
     sampler = B.ClockSampler(torch.cuda.current_device())
     sampler.start()
     l0 = kernel_launches()
-    ms = _events_time(lambda: db(recs), args.steps, args.warmup, world, dist)
+    from paper_2012_11077_b200.batch import phase_ms4
+    phase_ms4(1024)
+    ms = _events_time(lambda: db(recs, phase_events=True), args.steps, args.warmup, world, dist)
     launches = (kernel_launches() - l0) * args.steps // (args.steps + args.warmup)
     clocks = sampler.stop()
     db.check_inputs()
+    # the front end's share of the step: step time minus the CFAR call's phases
+    ph = _phases(args.steps)
+    cfar_ms = sum(ph.values()) if ph else 0.0
+    fe_ms = ms - cfar_ms
+    n_loc = m1 - m0
+    ops = FE_FP64_OPS_PER_RECORD * n_loc
+    peak_fp64, peak_src = _fp64_peak()
+    fe_roof = {"bound": "fp64", "kernel": "frontend_stats_kernel + frontend_fft1024_kernel",
+               "achieved": ops / (fe_ms / 1e3) / 1e9, "peak": peak_fp64, "unit": "Gop/s (fp64 add/mul)",
+               "frac": ops / (fe_ms / 1e3) / 1e9 / peak_fp64, "traffic": None,
+               "ops_per_record": FE_FP64_OPS_PER_RECORD, "launch_ms": fe_ms, "peak_source": peak_src,
+               "timing": "front end = step (CUDA events) minus the CFAR call's phase events",
+               "hbm_frac": (n_loc * (M * Nn * 4 + M * db.kept * 8)) / (fe_ms / 1e3) / 1e9 / B._peaks()[0],
+               "cfar_phases_ms": ph}
     # end to end: pinned host batch -> H2D -> detect -> D2H of masks and counts
     host = torch.empty(recs.shape, dtype=torch.float32, pin_memory=True)
     host.copy_(recs)
@@ -450,7 +489,7 @@ def run_cfg2(args):
                                   "Pfa 1e-3 (uwb_dev_detect_batch)",
                       "band_bins": db.kept, "parallelism": f"dp{world} (records sharded)",
                       "single_record_host_detect_ms": host_ms},
-              roofline=None, cpu_baseline=cpu,
+              roofline=fe_roof, cpu_baseline=cpu,
               e2e={"value": n_all / (e_ms / 1e3), "unit": "records/s",
                    "h2d_bytes_per_step": int(host.numel() * 4) * world,
                    "d2h_bytes_per_step": int(mask_host.numel() * 4 + cnt_host.numel() * 8) * world,

@@ -199,9 +199,11 @@ class DetectBatch:
             self.mask_bits.data_ptr(), self.words_per_row, self.m * self.words_per_row, None, None,
             self.dets.data_ptr(), self.det_capacity, self.counts.data_ptr(), self.first_bad.data_ptr())
 
-    def __call__(self, records: torch.Tensor, stream=None, general_kernels: bool = False) -> None:
+    def __call__(self, records: torch.Tensor, stream=None, general_kernels: bool = False,
+                 phase_events: bool = False) -> None:
         """``general_kernels`` (test hook): the per-stage front-end kernels instead
-        of the fused two-kernel front end (same results)."""
+        of the fused two-kernel front end (same results). ``phase_events``
+        records the CFAR call's phase events (read with :func:`phase_ms4`)."""
         if records.dtype != self.dtype or tuple(records.shape) != (self.n_records, self.m, self.n):
             raise ValueError(f"expected {(self.n_records, self.m, self.n)} {self.dtype}")
         if not records.is_cuda or not records.is_contiguous():
@@ -212,7 +214,7 @@ class DetectBatch:
                                              C.c_double(self.fast_rate), C.c_double(self.prf), C.byref(self._cfg),
                                              self.band.data_ptr(), C.byref(kept), C.byref(self._out),
                                              self.workspace.data_ptr(), C.c_uint64(self.workspace.numel()),
-                                             256 if general_kernels else 0,
+                                             (256 if general_kernels else 0) | (2 if phase_events else 0),
                                              C.c_void_p(s.cuda_stream)))
 
     def check_inputs(self) -> None:
