@@ -309,3 +309,27 @@ def test_ring_row_chunk_edges_bits_only(uwb, ref, cuda, rows, fixed):
         d = b.detections(i)
         assert np.array_equal(d["row"], exp.detections["row"]) and np.array_equal(d["col"], exp.detections["col"])
         assert_bitwise(d["threshold"], exp.detections["threshold"], f"rows {rows} map {i}: thresholds")
+
+
+@pytest.mark.parametrize("rows,cols", [(256, 256), (512, 512)])
+@pytest.mark.parametrize("certify", [False, True])
+def test_long_lists_merge_passes_vs_reference(uwb, ref, cuda, rows, cols, certify):
+    """Single maps (fewer lists than SMs: multi-CTA merge passes) with ~5k and
+    ~21k detections in a 65536-entry list: the runs need 2 and 4 merge passes
+    against the capacity's 5 (an odd / even pass count below the capacity's),
+    and the sorted lists must equal the reference's (cfar.cpp:170-173)."""
+    from paper_2012_11077_b200.batch import BatchCfar
+    gen = torch.Generator(device="cuda").manual_seed(rows)
+    maps = torch.empty((1, rows, cols), device=cuda, dtype=torch.float32).exponential_(1.0, generator=gen)
+    p = uwb.CfarParams(1, 4, 0.08)  # (g + b, g) = (5, 1): a certified-path window
+    b = BatchCfar(1, rows, cols, p, torch.float32, det_capacity=1 << 16)
+    b(maps, certify=certify)
+    torch.cuda.synchronize()
+    n = int(b.counts[0])
+    assert 4000 < n < 30000
+    exp = ref.cfar2d(maps[0].double().cpu().numpy(), 1, 4, 0.08, "integral")
+    d = b.detections(0)
+    assert len(d) == len(exp.detections)
+    assert np.array_equal(d["row"], exp.detections["row"]) and np.array_equal(d["col"], exp.detections["col"])
+    assert_bitwise(d["value"], exp.detections["value"], "values")
+    assert_bitwise(d["threshold"], exp.detections["threshold"], "thresholds")
