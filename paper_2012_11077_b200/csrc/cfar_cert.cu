@@ -249,6 +249,29 @@ __device__ __noinline__ void cert_service(const CertLaunch& L, int64_t map, uint
     if (lane == 0) stg[0] = 0;
 }
 
+// A passing tile's 4 cells (rows r0, r0+1, columns c0, c0+1; lb per cell in
+// the order (0,0), (0,1), (1,0), (1,1)) into the phase's staging buffer; when
+// the buffer is full, tested right here.
+template <typename T>
+__device__ __noinline__ void cert_stage_tile(const CertLaunch& L, int64_t map, uint32_t* stg, int r0, int c0, int r_s,
+                                             int r_e, int cols, uint32_t lb0, uint32_t lb1, uint32_t lb2, uint32_t lb3) {
+    const uint32_t lb[4] = {lb0, lb1, lb2, lb3};
+#pragma unroll
+    for (int cell = 0; cell < 4; ++cell) {
+        const int r = r0 + (cell >> 1), c = c0 + (cell & 1);
+        if (r >= r_s && r < r_e && c < cols) {
+            const unsigned i = atomicAdd(stg, 1u);
+            if (i < static_cast<unsigned>(kStage)) {
+                stg[1 + i] = static_cast<uint32_t>(r);
+                stg[1 + kStage + i] = static_cast<uint32_t>(c);
+                stg[1 + 2 * kStage + i] = lb[cell];
+            } else if (cert_cell_test<T>(L, map, r, c, lb[cell])) {
+                cert_append(L, map, r, c); // staging full (rare)
+            }
+        }
+    }
+}
+
 template <typename T, int HR, int GR, int HC, int GC>
 __global__ void __launch_bounds__(CertGeo<HR, GR, HC, GC, sizeof(T)>::NT, CertGeo<HR, GR, HC, GC, sizeof(T)>::OCC)
 cert_kernel(const __grid_constant__ CertLaunch L) {
@@ -408,27 +431,16 @@ cert_kernel(const __grid_constant__ CertLaunch L) {
                     if (__fmul_ru(cmax, kin.x) >= __fmaf_rd(__uint2float_rd(lbmin), L.inv_scale, -kin.z))
                         pass |= 1u << j;
                 }
-                // rare: exact per-cell tests of the tiles that passed (out of the unrolled code)
+                // rare: exact per-cell tests of the tiles that passed, staged by an
+                // out-of-line function (keeps the unrolled item code small for the
+                // instruction cache); static indices keep lbs in registers
                 if (pass) {
                     uint32_t* stg = stage + (p & 1) * (3 * kStage + 1);
-                    static_for<kItemTiles>([&](auto jc) { // static indices keep lbs in registers
+                    static_for<kItemTiles>([&](auto jc) {
                         constexpr int j = decltype(jc)::value;
-                        if (pass & (1u << j)) {
-#pragma unroll
-                            for (int cell = 0; cell < 4; ++cell) {
-                                const int r = 2 * I + (cell >> 1), c = 2 * (J0 + j) + (cell & 1);
-                                if (r >= r_s && r < r_e && c < cols) {
-                                    const unsigned i = atomicAdd(stg, 1u);
-                                    if (i < static_cast<unsigned>(kStage)) {
-                                        stg[1 + i] = static_cast<uint32_t>(r);
-                                        stg[1 + kStage + i] = static_cast<uint32_t>(c);
-                                        stg[1 + 2 * kStage + i] = lbs[j][cell];
-                                    } else if (cert_cell_test<T>(L, map, r, c, lbs[j][cell])) {
-                                        cert_append(L, map, r, c); // staging full (rare)
-                                    }
-                                }
-                            }
-                        }
+                        if (pass & (1u << j))
+                            cert_stage_tile<T>(L, map, stg, 2 * I, 2 * (J0 + j), r_s, r_e, cols, lbs[j][0], lbs[j][1],
+                                               lbs[j][2], lbs[j][3]);
                     });
                 }
             }
