@@ -471,7 +471,8 @@ sat_systolic_kernel(SatLaunch L) {
                 table[static_cast<int64_t>(s0 - 8 + lane + 1) * tld + kTabShift] = 0.0;
             const bool fast = s0 >= kWarp && s0 + kWarp + kAhead <= rows && warp_fast;
             if (fast) {
-#pragma unroll 16
+                // unrolled by 8, not 16: half the code, the instruction cache decides
+#pragma unroll 8
                 for (int u = 0; u < kWarp; ++u) step(s0, u, std::integral_constant<int, 0>{});
             } else if (first_fast && s0 == 0) {
                 // the first block at interior speed (it is on every later strip's
