@@ -97,14 +97,9 @@ struct CertGeo {
     static constexpr int NBO = rup(kTB * LAG + 2 * kTB + 1 - R.hl - SOMIN - R.lo, 8);
     static constexpr int NBG = rup(kTB * LAG + 2 * kTB + 1 - R.hl - SGMIN - R.lg, 8);
     static constexpr int NBC = rup(kTB * LAG + 2 * kTB - R.hl, 8);
-    // ring row stride (words) == 4 (mod 32): rows stay 16-byte aligned for the
-    // items' 128-bit loads, and the 8 lanes of a quarter warp (8 consecutive
-    // ring rows, same columns) hit 8 distinct 4-bank groups
-    static constexpr int SW = NT + 4;
-    // tile maxima are 16-bit upper bounds (the top half of the float, rounded up),
-    // stored at u16 index t + CPAD so an item's 8 tiles are one aligned 16-byte load
-    static constexpr int CPAD = (8 - C.hl % 8) % 8;
-    static constexpr int SWC = rup((NT + CPAD + 1) / 2 - 4, 32) + 4; // words per tile-max row, == 4 (mod 32)
+    static constexpr int SW = NT + 1; // ring row stride (words), == 1 (mod 32) with NT % 32 == 0
+    // tile maxima are 16-bit upper bounds (the top half of the float, rounded up)
+    static constexpr int SWC = rup(SW, 2) / 2 + 1; // words per tile-max row (odd)
     static constexpr size_t smem =
         sizeof(uint32_t) * (static_cast<size_t>(NBO + NBG) * SW + static_cast<size_t>(NBC) * SWC + 2 * (3 * kStage + 1));
     static constexpr int OCC = smem * 3 <= 220 * 1024 ? 3 : 2;
@@ -200,31 +195,17 @@ __device__ __forceinline__ void static_for(F&& f) {
     static_for_impl<0, N>(f);
 }
 
-__device__ __forceinline__ uint4 lds4(unsigned a) {
-    uint4 v;
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
-    return v;
-}
-
 // Sliding sums over L consecutive words of one ring row: out[m] = sum of words
-// [OFF + m, OFF + m + L), m = 0 .. N-1, from the 16-byte aligned address `row`
-// (the words are fetched with 128-bit loads, OFF < 4 compile-time).
-template <int L, int N, int OFF>
+// [m, m + L) (word address `row` + 4 * first column), m = 0 .. N-1.
+template <int L, int N>
 __device__ __forceinline__ void row_windows(unsigned row, uint32_t (&out)[N]) {
-    constexpr int NQ = (OFF + N + L - 1 + 3) / 4;
-    uint32_t w[4 * NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-        const uint4 v = lds4(row + 16u * q);
-        w[4 * q] = v.x, w[4 * q + 1] = v.y, w[4 * q + 2] = v.z, w[4 * q + 3] = v.w;
-    }
     uint32_t h = 0;
 #pragma unroll
-    for (int m = 0; m < L; ++m) h += w[OFF + m];
+    for (int m = 0; m < L; ++m) h += lds1(row + 4u * m);
     out[0] = h;
 #pragma unroll
     for (int m = 1; m < N; ++m) {
-        h += w[OFF + m + L - 1] - w[OFF + m - 1];
+        h += lds1(row + 4u * (m + L - 1)) - lds1(row + 4u * (m - 1));
         out[m] = h;
     }
 }
@@ -362,7 +343,7 @@ cert_kernel(const __grid_constant__ CertLaunch L) {
             pnext += static_cast<int64_t>(2 * kTB) * ld_t;
             const unsigned wO = sO + 4u * SW * static_cast<unsigned>(k0 % G::NBO) + a_me;
             const unsigned wG = sG + 4u * SW * static_cast<unsigned>(k0 % G::NBG) + a_me;
-            const unsigned wC = sC + 4u * G::SWC * static_cast<unsigned>(k0 % G::NBC) + 2u * (t + G::CPAD);
+            const unsigned wC = sC + 4u * G::SWC * static_cast<unsigned>(k0 % G::NBC) + 2u * t;
             const int r_pf = 2 * (K0 + k0 + kPT); // first row this phase prefetches
             const bool safe = r_pf >= rb_lo && r_pf + 2 * kTB <= rb_hi; // every prefetched row in the buffer
 #pragma unroll
@@ -411,27 +392,21 @@ cert_kernel(const __grid_constant__ CertLaunch L) {
                 constexpr int NO = kItemTiles + CO, NG = kItemTiles + CG;
                 constexpr int SOC = imn(G::C.so0, G::C.so1), SGC = imn(G::C.sg0, G::C.sg1);
                 // ring rows of the outer / guard tile boxes of both row parities
-                // first window word (J0 - J_s = 8 grp is a multiple of 8): the aligned
-                // part goes into the address, the rest (< 4) is a compile-time offset
-                constexpr int WO = SOC + G::C.hl, WG = SGC + G::C.hl;
                 auto rowO = [&](int so) {
                     const int k = kI + so + G::R.lo - 1;
-                    return sO + 4u * (SW * static_cast<unsigned>(k % G::NBO) + static_cast<unsigned>(J0 - J_s + (WO & ~3)));
+                    return sO + 4u * (SW * static_cast<unsigned>(k % G::NBO) + static_cast<unsigned>(J0 + SOC - J_s + G::C.hl));
                 };
                 auto rowG = [&](int sg) {
                     const int k = kI + sg + G::R.lg - 1;
-                    return sG + 4u * (SW * static_cast<unsigned>(k % G::NBG) + static_cast<unsigned>(J0 - J_s + (WG & ~3)));
+                    return sG + 4u * (SW * static_cast<unsigned>(k % G::NBG) + static_cast<unsigned>(J0 + SGC - J_s + G::C.hl));
                 };
                 uint32_t ho0[NO], ho1[NO], hg0[NG], hg1[NG];
-                row_windows<G::C.lo, NO, (WO & 3)>(rowO(G::R.so0), ho0);
-                if constexpr (G::R.so1 != G::R.so0) row_windows<G::C.lo, NO, (WO & 3)>(rowO(G::R.so1), ho1);
-                row_windows<G::C.lg, NG, (WG & 3)>(rowG(G::R.sg0), hg0);
-                if constexpr (G::R.sg1 != G::R.sg0) row_windows<G::C.lg, NG, (WG & 3)>(rowG(G::R.sg1), hg1);
-                // the item's 8 tile maxima: one aligned 16-byte load
+                row_windows<G::C.lo, NO>(rowO(G::R.so0), ho0);
+                if constexpr (G::R.so1 != G::R.so0) row_windows<G::C.lo, NO>(rowO(G::R.so1), ho1);
+                row_windows<G::C.lg, NG>(rowG(G::R.sg0), hg0);
+                if constexpr (G::R.sg1 != G::R.sg0) row_windows<G::C.lg, NG>(rowG(G::R.sg1), hg1);
                 const unsigned cC = sC + 4u * G::SWC * static_cast<unsigned>(kI % G::NBC) +
-                                    2u * static_cast<unsigned>(J0 - J_s + G::C.hl + G::CPAD);
-                const uint4 cm4 = lds4(cC);
-                const uint32_t cmw[4] = {cm4.x, cm4.y, cm4.z, cm4.w};
+                                    2u * static_cast<unsigned>(J0 - J_s + G::C.hl);
                 const uint32_t off = L.ring_off;
                 uint32_t lbs[kItemTiles][4]; // per tile, cells (a, b) = (0,0), (0,1), (1,0), (1,1)
                 unsigned pass = 0;
@@ -449,8 +424,9 @@ cert_kernel(const __grid_constant__ CertLaunch L) {
                         }
                     }
                     const uint32_t lbmin = min(min(lbs[j][0], lbs[j][1]), min(lbs[j][2], lbs[j][3]));
-                    const uint32_t cm16 = (j & 1) ? (cmw[j >> 1] >> 16) : (cmw[j >> 1] & 0xFFFFu);
-                    const float cmax = __uint_as_float(cm16 << 16); // >= the tile's max CUT
+                    unsigned short cm16;
+                    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(cm16) : "r"(cC + 2u * j));
+                    const float cmax = __uint_as_float(static_cast<uint32_t>(cm16) << 16); // >= the tile's max CUT
                     // tile test with the largest K_n, E_n (n_int): no cell of the tile can reach T
                     if (__fmul_ru(cmax, kin.x) >= __fmaf_rd(__uint2float_rd(lbmin), L.inv_scale, -kin.z))
                         pass |= 1u << j;
