@@ -35,6 +35,9 @@ NVCC_FLAGS = [
 # tuning build for the scripts/ probes only: environment knobs (common.cuh UWB_KNOB)
 if os.environ.get("UWB_TUNING_KNOBS") == "1":
     NVCC_FLAGS.append("-DUWB_TUNING_KNOBS")
+# device-side bounds checks (the compute-sanitizer stand-in)
+if os.environ.get("UWB_DEVICE_CHECKS") == "1":
+    NVCC_FLAGS.append("-DUWB_DEVICE_CHECKS")
 
 CAPI_SO = os.path.join(LIB, "libuwbvital_b200.so")
 DROPIN_SO = os.path.join(LIB, "libuwbvital.so")

@@ -414,9 +414,15 @@ cudaError_t launch_sort_detections(uwb_detection* dets, int64_t cap, const unsig
                                                                                             true);
         return cudaGetLastError();
     }
+    // one run per list: shared memory for the capacity's power of two only, so
+    // short lists (cfg 3: 512 entries) sort with many CTAs per SM
+    int64_t p2 = 1;
+    while (p2 < cap) p2 <<= 1;
+    const size_t smem1 = sizeof(uwb_detection) * static_cast<size_t>(p2);
+    const int threads = static_cast<int>(imin(kSortThreads, imax(64, p2 / 2)));
     ++g_kernel_launches;
-    sort_detections_kernel<<<static_cast<unsigned>(n_maps), kSortThreads, smem, stream>>>(dets, cap, counts, scratch,
-                                                                                        false);
+    sort_detections_kernel<<<static_cast<unsigned>(n_maps), threads, smem1, stream>>>(dets, cap, counts, scratch,
+                                                                                    false);
     return cudaGetLastError();
 }
 

@@ -484,6 +484,7 @@ struct TapView {
     int i0, j0; // global source row / column of the table's row / column 0
     __device__ __forceinline__ double operator()(int i, int j) const {
         const int il = i - i0, jl = j - j0;
+        UWB_DCHECK(il >= 0 && jl >= 0 && kTabShift + jl < ld);
         return (il == 0 || jl == 0) ? 0.0 : tab[static_cast<int64_t>(il) * ld + kTabShift + jl];
     }
 };
@@ -530,6 +531,8 @@ __global__ void cert_mark_kernel(const __grid_constant__ CertLaunch L) {
             if (il <= 0 || jl <= 0) continue; // padded row / column 0 is zero
             const int dr = il - 1, dc = jl - 1;
             const int strip = dc / span, bit = (dc % span) / L.cpl;
+            UWB_DCHECK(strip >= 0 && strip < L.strips && dr >= 0 && dr < L.need_rows && g.sat_job >= 0 &&
+                       g.sat_job < L.n_maps * L.geo.n_slabs * L.geo.n_bands);
             atomicOr(L.need + (g.sat_job * L.strips + strip) * L.need_rows + dr, 1u << bit);
         }
     }
@@ -566,6 +569,7 @@ __global__ void cert_resolve_kernel(const __grid_constant__ CertLaunch L) {
         const double mean = ddiv(sum, static_cast<double>(n));
         const double thr = dmul(__ldg(L.alpha + n), mean);
         const double v = widen(__ldg(src + (r - L.geo.buf_row0) * L.ld + c));
+        UWB_DCHECK(r >= L.geo.row_lo && r < L.geo.row_hi && c >= 0 && c < L.cols);
         if (v > thr) { // cfar.cpp:125, ties -> H0
             atomicOr(L.mask_bits + map * L.mask_map_stride + (r - L.geo.row_lo) * L.words_per_row + (c >> 5),
                      1u << (c & 31));

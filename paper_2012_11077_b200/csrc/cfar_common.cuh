@@ -22,6 +22,8 @@ __device__ __forceinline__ void emit_cells(const CfarLaunch& L, int64_t map, int
                                            double v, double thr) {
     const unsigned lane = threadIdx.x % kWarp;
     const unsigned bits = __ballot_sync(0xffffffffu, valid && hit);
+    UWB_DCHECK(!valid || (r >= L.geo.row_lo && r < L.geo.row_hi && c >= 0 && c < L.cols &&
+                          map >= 0 && map * L.geo.n_slabs < L.n_jobs));
     if (lane == 0 && L.mask_bits) {
         const int word = c >> 5;
         if (word < L.words_per_row)

@@ -12,6 +12,27 @@
 
 #include "uwbvital_b200.h"
 
+// Device-side bounds checks (-DUWB_DEVICE_CHECKS, UWB_DEVICE_CHECKS=1 python
+// paper_2012_11077_b200/build.py --force): every global / shared index the
+// kernels compute on their hot paths is asserted inside its buffer; a failure
+// prints the condition and traps. The stand-in for compute-sanitizer, which is
+// closed on this GPU pool. Compiled out of the release build.
+#ifdef UWB_DEVICE_CHECKS
+#include <cstdio>
+#define UWB_DCHECK(cond)                                                                   \
+    do {                                                                                   \
+        if (!(cond)) {                                                                     \
+            printf("UWB_DCHECK failed at %s:%d: %s (block %d, thread %d)\n", __FILE__, __LINE__, #cond, \
+                   static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));           \
+            __trap();                                                                      \
+        }                                                                                  \
+    } while (0)
+#else
+#define UWB_DCHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
+
 // Tuning knobs (ring depth, occupancy, chunking ...) read from the environment
 // exist only in a tuning build (-DUWB_TUNING_KNOBS, scripts/ probes); the
 // release library reads no environment variable, so nothing outside the call

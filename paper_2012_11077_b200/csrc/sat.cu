@@ -345,6 +345,7 @@ sat_systolic_kernel(SatLaunch L) {
             // (1) group g writes back row s - 8g - 8 (slot u mod 8, stored >= 1 step ago)
             const int rf = s - 8 * grp - 8;
             if (!kSparse && (kFirst ? rf >= 0 : (!kChecked || (rf >= 0 && rf < rows)))) {
+                UWB_DCHECK(rf >= 0 && rf < rows && tflush == table + static_cast<int64_t>(rf + 1) * tld + kTabShift + 1 + c);
                 double o[kCpl];
                 lds_out<kCpl>(o_lane + static_cast<unsigned>(u & (kOSlots - 1)) * kOSlotBytes, o);
                 if (!kChecked || nvalid == kCpl) {
@@ -407,9 +408,11 @@ sat_systolic_kernel(SatLaunch L) {
                     // a non-finite input, which the call reports as an error
                     const double e_new = canon_edge(sv[kCpl - 1]), e_prev = canon_edge(prev[kCpl - 1]);
                     if (kChecked) {
+                        UWB_DCHECK(r >= 0 && r < L.edge_stride);
                         st_edge(ge_out + r, e_new);
                         if (u == 0 && r >= 1) st_edge(ge_out + r - 1, e_prev); // row a fast block left unstored
                     } else if ((u & 1) == 0 && (!kFirst || r >= 1)) { // r = s - 31 is odd
+                        UWB_DCHECK(r >= 1 && r < L.edge_stride);
                         st_edge2(ge_out + r - 1, e_prev, e_new);
                     }
                 }
@@ -422,6 +425,7 @@ sat_systolic_kernel(SatLaunch L) {
                     // marked taps of row r: S(r, c..c+kCpl-1) = padded (r+1, c+1..)
                     const unsigned w = store_all ? ~0u : w_need;
                     if ((w >> lane) & 1u) {
+                        UWB_DCHECK(r >= 0 && r < rows && c >= 0 && c + nvalid <= cols && kTabShift + 1 + c + nvalid <= tld);
                         double* dst = table + static_cast<int64_t>(r + 1) * tld + kTabShift + 1 + c;
                         if (kCpl >= 2 && nvalid == kCpl) {
 #pragma unroll
@@ -641,6 +645,7 @@ __global__ void __launch_bounds__(kCtaMaxWarps * kWarp, 1) sat_cta_kernel(SatLau
             const int r = s - lane;
             const bool act = !kChecked || (r >= 0 && r < rows);
             const int xslot = xbase + u < kCtaXSlots ? xbase + u : xbase + u - kCtaXSlots;
+            UWB_DCHECK(xslot >= 0 && xslot < kCtaXSlots);
             const T* xs = xr + xslot * kXStride;
             double a[kC]; // x + S(r-1, .): independent of the left neighbour
 #pragma unroll
@@ -674,6 +679,7 @@ __global__ void __launch_bounds__(kCtaMaxWarps * kWarp, 1) sat_cta_kernel(SatLau
         for (int u = 0; u < kCtaSync; ++u) {
             const int rf = rf0 + u;
             if (!kChecked || (rf >= 0 && rf < rows)) {
+                UWB_DCHECK(rf >= 0 && rf < rows && dst == table + static_cast<int64_t>(rf + 1) * tld + kTabShift + 1 + c);
                 const double* o = orr + ((rf + lane) & (kCtaOSlots - 1)) * kOStride;
                 if (nvalid == kC) {
 #pragma unroll
