@@ -239,7 +239,9 @@ uint64_t uwb_dev_cfar2d_workspace(const uwb_map_batch* batch, const uwb_cfar_par
  *   batches. Bits 7 and 8 change the schedule only, never the results.
  * flags bit 9: take the certified path also for a small batch (at most one
  *   table per SM, each table's strips within one CTA), which by default runs
- *   the exact path with one CTA per table (latency-bound batches). */
+ *   the exact path with one CTA per table (latency-bound batches).
+ * flags bit 10 (test hook): small batches build their tables with one CTA per
+ *   table instead of one thread-block cluster per table (same results). */
 uwb_status uwb_dev_cfar2d(const uwb_map_batch* batch, const uwb_cfar_params* params,
                           const double* alpha_dev, int32_t sat_mode, uint64_t slab_rows,
                           const uwb_cfar_outputs* out, void* workspace, uint64_t workspace_bytes,

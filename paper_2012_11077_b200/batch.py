@@ -88,7 +88,7 @@ class BatchCfar:
     def __call__(self, maps: torch.Tensor, sort: bool = True, stream=None, phase_events: bool = False,
                  reuse_tables: bool = False, naive: bool = False, fused: bool = False,
                  exact: bool = False, dense_tables: bool = False, fixed_ring_rows: bool = False,
-                 certify: bool = False) -> None:
+                 certify: bool = False, cta_tables: bool = False) -> None:
         """Launch SAT + CFAR (+ sort) for ``maps`` of shape (n_maps, rows, cols).
         ``phase_events`` records per-phase CUDA events (read with :func:`phase_ms`).
         ``reuse_tables`` skips the SAT: the (shared) workspace already holds the
@@ -102,7 +102,9 @@ class BatchCfar:
         ``fixed_ring_rows`` are test hooks that change the schedule, not the
         results (full tables on the certified path; 256-row ring chunks).
         ``certify`` takes the certified path also for a small batch (which by
-        default runs the exact path with one CTA per table)."""
+        default runs the exact path with one thread-block cluster per table);
+        ``cta_tables`` (test hook) builds a small batch's tables with one CTA per
+        table instead."""
         if maps.dtype != self.dtype or tuple(maps.shape) != (self.n_maps, self.rows, self.cols):
             raise ValueError(f"expected {(self.n_maps, self.rows, self.cols)} {self.dtype}, got "
                              f"{tuple(maps.shape)} {maps.dtype}")
@@ -110,7 +112,7 @@ class BatchCfar:
             raise ValueError("maps must be a contiguous CUDA tensor")
         self._batch.maps = maps.data_ptr()
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
-        flags = (0 if sort else 1) | (2 if phase_events else 0) | (4 if reuse_tables else 0) | (8 if naive else 0) | (16 if fused else 0) | (64 if exact else 0) | (128 if dense_tables else 0) | (256 if fixed_ring_rows else 0) | (512 if certify else 0)
+        flags = (0 if sort else 1) | (2 if phase_events else 0) | (4 if reuse_tables else 0) | (8 if naive else 0) | (16 if fused else 0) | (64 if exact else 0) | (128 if dense_tables else 0) | (256 if fixed_ring_rows else 0) | (512 if certify else 0) | (1024 if cta_tables else 0)
         if self.window is None:
             st = N.lib.uwb_dev_cfar2d(C.byref(self._batch), C.byref(self._cparams), self.alpha.data_ptr(),
                                       self.sat_mode, C.c_uint64(self.slab_rows), C.byref(self._out),

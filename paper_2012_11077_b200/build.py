@@ -18,7 +18,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "lib")
 INCLUDE = os.path.join(ROOT, "include")
 
-CUDA_SOURCES = ["sat.cu", "cfar.cu", "cfar_ring.cu", "cfar_fused.cu", "cfar_cert.cu", "frontend.cu", "ingest.cu", "capi.cu"]
+CUDA_SOURCES = ["sat.cu", "sat_cluster.cu", "cfar.cu", "cfar_ring.cu", "cfar_fused.cu", "cfar_cert.cu", "frontend.cu", "ingest.cu", "capi.cu"]
 HEADERS = ["common.cuh", "kernels.cuh", "cfar_common.cuh"]
 NVCC = os.environ.get("NVCC", "nvcc")
 CXX = os.environ.get("CXX", "g++")

@@ -270,6 +270,8 @@ SatLaunch sat_launch(const Plan& P, const uwb_map_batch& b, char* ws, unsigned l
 }
 
 cudaError_t run_sat(const Plan& P, const SatLaunch& L, int dtype, cudaStream_t s) {
+    // the cluster kernel (small batches) needs no counters
+    if (!(L.flags & 256u) && sat_cluster_eligible(L, dtype)) return launch_sat(L, dtype, s);
     cudaError_t e = cudaMemsetAsync(L.gprog, 0, sizeof(unsigned) * P.sat_jobs * P.strips, s);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(L.tile_counter, 0, sizeof(unsigned), s);
@@ -397,7 +399,9 @@ bool cert_applies(const Plan& P, const uwb_map_batch& b, const uwb_cfar_params& 
     if (P.cand_cap == 0 || P.geo.rows >= (int64_t(1) << 30) || P.cols >= (int64_t(1) << 30)) return false;
     // small batches are latency-bound: the one-CTA-per-table exact SAT and the
     // ring CFAR take fewer dependent steps than certify + sparse SAT + resolve
-    if (!(flags & 512u) && sat_cta_eligible(P.sat_jobs, P.sat_cols, b.dtype)) return false;
+    if (!(flags & 512u) && (sat_cta_eligible(P.sat_jobs, P.sat_cols, b.dtype) ||
+                            sat_cluster_fits(P.sat_jobs, P.sat_cols, P.geo.max_table_rows(), b.dtype)))
+        return false;
     return cert_supported(p.guard_rows + p.background_rows, p.guard_rows, p.guard_cols + p.background_cols,
                           p.guard_cols);
 }
@@ -491,7 +495,8 @@ uwb_status dev_cfar(const uwb_map_batch& b, const uwb_cfar_params& p, const doub
         if (!fused) {
             if (!(flags & 4u)) { // bit 2: the workspace already holds this batch's tables
                 NvtxRange r("uwb.sat");
-                const SatLaunch SL = sat_launch(P, b, ws, reinterpret_cast<unsigned long long*>(o.first_bad));
+                SatLaunch SL = sat_launch(P, b, ws, reinterpret_cast<unsigned long long*>(o.first_bad));
+                if (flags & 1024u) SL.flags |= 256u; // bit 10 (test hook): no cluster kernel, same results
                 UWB_CUDA_TRY(run_sat(P, SL, b.dtype, s));
             }
             NvtxRange r("uwb.cfar");

@@ -222,6 +222,11 @@ int64_t sat_strips(int64_t cols, int cpl);       // strips of 32 * cpl columns
 int sat_cpl_for(int64_t n_jobs, int64_t cols);   // columns per lane for a batch
 // small batches whose tables each fit one CTA (sat_cta_kernel: strips hand over in shared memory)
 bool sat_cta_eligible(int64_t n_jobs, int64_t cols, int dtype);
+// small batches whose tables each run as one thread-block cluster (sat_cluster.cu: strips hand
+// over through distributed shared memory); _fits: by shape, _eligible: shape and alignment
+bool sat_cluster_fits(int64_t n_jobs, int64_t cols, int64_t max_rows, int dtype);
+bool sat_cluster_eligible(const SatLaunch& L, int dtype);
+cudaError_t launch_sat_cluster(const SatLaunch& L, int dtype, cudaStream_t stream);
 
 cudaError_t launch_cfar_integral(const CfarLaunch& L, int dtype, cudaStream_t stream);
 // the same over the flagged maps L.flagged_maps[0 .. *L.flagged_count) only (certified path's exact fallback)

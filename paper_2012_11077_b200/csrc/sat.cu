@@ -786,6 +786,8 @@ static cudaError_t launch_sat_t(const SatLaunch& L, cudaStream_t stream) {
 template <typename T>
 static cudaError_t launch_sat_cpl(const SatLaunch& L, cudaStream_t stream) {
     cudaError_t e = cudaSuccess;
+    constexpr int kDtype = sizeof(T) == 4 ? UWB_F32 : UWB_F64;
+    if (!(L.flags & 256u) && sat_cluster_eligible(L, kDtype)) return launch_sat_cluster(L, kDtype, stream);
     if (launch_sat_cta<T>(L, stream, &e)) return e;
     if (L.need) {
         switch (L.cpl) {

@@ -1,0 +1,350 @@
+// Kernel (c), latency path: exact summed-area table of a few small maps, one
+// thread-block cluster per table (replacing build_sat,
+// /root/reference/proj/src/sat.cpp:10-37, for single-map calls: the paper's
+// Table I shape and BASELINE config 1).
+//
+// A single table is bound by the dependent chain of the recurrence
+//     S(r,c) = ((x(r,c) + S(r-1,c)) + S(r,c-1)) - S(r-1,c-1)        (sat.cpp:33)
+// not by bandwidth: the wavefront needs rows + columns dependent steps whatever
+// the machine. This kernel keeps each step as close to that chain as it can:
+//   * a strip of 32 lanes x 16 source bytes (64 fp64 / 128 fp32 columns) is
+//     swept by ONE compute warp that has a scheduler of its own: lane l owns
+//     its 2 / 4 columns and handles row s - l at step s (the systolic schedule
+//     of sat.cu); per step a lane issues one 16-byte shared load of x, the
+//     x + S(r-1, .) additions (off the chain), one 64-bit shuffle and the
+//     2 x columns dependent additions of sat.cpp:33 in the reference's
+//     association, and stores its S values straight from registers (the table
+//     of a small map lives in L2, so 16-byte scattered stores cost nothing
+//     and no write-back ring, barrier or second pass sits on the chain);
+//   * the strips of a table are the CTAs of one thread-block cluster (up to 8
+//     CTAs x up to 3 strips). Lane 31 of strip w stores S(r, last column)
+//     into the shared memory of the CTA that runs strip w + 1 (a relaxed
+//     cluster-scope remote store through DSMEM); that strip's lanes 0..7 poll
+//     their own shared memory for the 8 rows of the next block. Every 8-byte
+//     value is its own flag: the edge column starts as a signalling-NaN
+//     sentinel (no IEEE addition returns one, so no S - not even one poisoned
+//     by a NaN input - can look like "not yet written"), and a whole column of
+//     `rows` values is kept, so there is no ring to recycle, no counter, no
+//     fence and no back-pressure: the chain is self-timed, strip w + 1 runs
+//     32 + ~8 steps behind strip w;
+//   * a helper warp per strip feeds the source ring with the TMA engine's 1-D
+//     bulk copies (one 512-byte row segment per lane, 8 rows per mbarrier
+//     phase, 11 chunks of look-ahead), so the compute warp never computes a
+//     global address for its inputs.
+// The same three additions per cell in the same order: bit-identical tables.
+#include <climits>
+#include <type_traits>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace uwb {
+
+namespace {
+
+constexpr int kClBlock = 8;                        // steps per block = rows per staged chunk
+constexpr int kClRingRows = 128;                   // source ring rows per strip
+constexpr int kClChunks = kClRingRows / kClBlock;  // 16 chunks, 5 live
+constexpr int kClRowBytes = kWarp * 16;            // 512 bytes of source per strip row
+constexpr unsigned kClRingBytes = kClRingRows * kClRowBytes; // 64 KB per strip
+constexpr int kClMaxSpc = 3;                       // strips per CTA
+constexpr int kClMaxCtas = 8;                      // portable cluster size
+constexpr size_t kClSmemCap = 227 * 1024;
+constexpr unsigned kClBarBytes = 2 * kClChunks * sizeof(uint64_t);
+
+__device__ __forceinline__ unsigned cluster_ctarank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// generic address of `local` (a pointer into my shared memory) in CTA `rank` of the cluster
+__device__ __forceinline__ unsigned long long map_to_cta(const void* local, unsigned rank) {
+    unsigned long long r;
+    asm volatile("mapa.u64 %0, %1, %2;" : "=l"(r) : "l"(reinterpret_cast<unsigned long long>(local)), "r"(rank));
+    return r;
+}
+// Hand-over pair: a relaxed cluster-scope store into the neighbour's shared
+// memory against relaxed cluster-scope polls (morally strong, single-copy
+// atomic per 8-byte value). The store is predicated, not branched: only lane
+// 31 of a strip with a right neighbour stores.
+__device__ __forceinline__ void st_edge_remote(unsigned long long addr, double v, unsigned on) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.u32 p, %2, 0;\n"
+        "@p st.relaxed.cluster.f64 [%0], %1;\n"
+        "}\n" ::"l"(addr),
+        "d"(v), "r"(on)); // no memory clobber: ordered against the other volatile asm only
+}
+__device__ __forceinline__ double ld_edge_poll(unsigned addr) {
+    double v;
+    asm volatile("ld.relaxed.cluster.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+    return v;
+}
+// "Not yet written": a signalling NaN. Every S is the result of an IEEE
+// addition, and an addition never returns a signalling NaN (a NaN result is
+// quiet whatever the inputs), so no table value can equal the sentinel.
+constexpr long long kClSentinel = 0x7ff0000000000001LL;
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <typename T>
+struct XVec;
+template <>
+struct XVec<double> {
+    using type = double2;
+    static __device__ __forceinline__ void get(const double2& v, double (&x)[2]) {
+        x[0] = v.x;
+        x[1] = v.y;
+    }
+};
+template <>
+struct XVec<float> {
+    using type = float4;
+    static __device__ __forceinline__ void get(const float4& v, float (&x)[4]) {
+        x[0] = v.x;
+        x[1] = v.y;
+        x[2] = v.z;
+        x[3] = v.w;
+    }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kClMaxSpc * 2 * kWarp, 1)
+sat_cluster_kernel(SatLaunch L, int spc, int csize, unsigned edge_bytes) {
+    constexpr int kC = 16 / static_cast<int>(sizeof(T));
+    constexpr int kStripCols = kWarp * kC;
+    extern __shared__ __align__(128) unsigned char cl_smem[];
+    const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+    const unsigned rank = cluster_ctarank();
+    const int64_t job = blockIdx.x / csize;
+    const bool helper = warp >= spc;
+    const int j = helper ? warp - spc : warp;           // my strip inside the CTA
+    const int g = static_cast<int>(rank) * spc + j;     // my strip of the table
+    const int cols = static_cast<int>(L.cols);
+    const int strips = (cols + kStripCols - 1) / kStripCols;
+    const bool live = g < strips;
+    const SatJobView J = sat_job(L, job);
+    const int rows = static_cast<int>(J.rows);
+    const int64_t ld = L.ld, tld = L.table_ld;
+    double* table = J.table;
+
+    unsigned char* ring = cl_smem + static_cast<size_t>(j) * kClRingBytes;
+    unsigned char* edges = cl_smem + static_cast<size_t>(spc) * kClRingBytes;
+    double* edge_in = reinterpret_cast<double*>(edges + static_cast<size_t>(j) * edge_bytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(edges + static_cast<size_t>(spc) * edge_bytes +
+                                                 static_cast<size_t>(j) * kClBarBytes);
+    uint64_t* empty = full + kClChunks;
+
+    // every edge value starts as the sentinel; barriers: one arrival per phase
+    for (unsigned i = threadIdx.x; i < static_cast<unsigned>(spc) * edge_bytes / 8; i += blockDim.x)
+        reinterpret_cast<long long*>(edges)[i] = kClSentinel;
+    if (!helper && lane == 0) {
+        for (int i = 0; i < kClChunks; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    cluster_sync_all(); // nobody stores into a neighbour before its sentinels are in place
+
+    const int n_chunks = (rows + kClBlock - 1) / kClBlock;
+    if (helper) {
+        if (live) {
+            const int c0 = g * kStripCols;
+            const unsigned row_bytes =
+                static_cast<unsigned>(min(kStripCols, cols - c0)) * static_cast<unsigned>(sizeof(T));
+            const T* src = static_cast<const T*>(J.src) + c0;
+            for (int q = 0; q < n_chunks; ++q) {
+                const int slot = q & (kClChunks - 1);
+                if (q >= kClChunks) mbar_wait(&empty[slot], static_cast<unsigned>(((q / kClChunks) - 1) & 1));
+                const int nr = min(kClBlock, rows - kClBlock * q);
+                if (lane == 0) mbar_expect_tx(&full[slot], static_cast<unsigned>(nr) * row_bytes);
+                __syncwarp();
+                const int r = kClBlock * q + lane;
+                if (lane < nr)
+                    bulk_g2s(ring + static_cast<size_t>(r & (kClRingRows - 1)) * kClRowBytes,
+                             src + static_cast<int64_t>(r) * ld, row_bytes, &full[slot]);
+            }
+            // padded column 0 (the compute lanes write padded row 0)
+            if (g == 0)
+                for (int r = lane; r <= rows; r += kWarp) table[static_cast<int64_t>(r) * tld + kTabShift] = 0.0;
+        }
+    } else if (live) {
+        const int c = g * kStripCols + lane * kC;
+        const bool valid = c < cols; // cols is a multiple of kC: all of my columns or none
+        if (valid) {
+#pragma unroll
+            for (int k = 0; k < kC; ++k) table[kTabShift + 1 + c + k] = 0.0; // padded row 0
+        }
+        const bool has_in = g > 0, has_out = g + 1 < strips;
+        unsigned long long edge_out = 0; // S(r, my last column) of lane 31 goes to edge_out + 8 r
+        if (has_out) {
+            const int gn = g + 1;
+            edge_out = map_to_cta(edges + static_cast<size_t>(gn % spc) * edge_bytes, static_cast<unsigned>(gn / spc));
+        }
+        const unsigned edge_lane = has_out && lane == kWarp - 1 ? 1u : 0u;
+        edge_out -= 8ull * static_cast<unsigned>(lane); // + 8 s = row s - lane
+        const unsigned edge_in_s = smem_u32(edge_in);
+        const unsigned char* xlane = ring + 16 * lane;
+        double prev[kC]; // S(r-1, c + k)
+#pragma unroll
+        for (int k = 0; k < kC; ++k) prev[k] = 0.0;
+        double left_prev = 0.0; // S(r-1, c-1)
+        // table row of my current row r = s - lane (padded row r + 1)
+        double* trow = table + kTabShift + 1 + c + static_cast<int64_t>(1 - lane) * tld;
+        const int steps = rows + kWarp - 1;
+        const int n_blocks = (steps + kClBlock - 1) / kClBlock;
+
+        auto steps8 = [&](const int s0, const double e, auto checked_tag) {
+            constexpr bool kChecked = decltype(checked_tag)::value;
+            using XV = typename XVec<T>::type;
+            // the next step's source values are loaded one step ahead
+            XV xn = *reinterpret_cast<const XV*>(xlane + static_cast<unsigned>((s0 - lane) & (kClRingRows - 1)) * kClRowBytes);
+#pragma unroll
+            for (int u = 0; u < kClBlock; ++u) {
+                const int r = s0 + u - lane;
+                const bool act = !kChecked || (r >= 0 && r < rows);
+                T x[kC];
+                XVec<T>::get(xn, x);
+                if (u + 1 < kClBlock)
+                    xn = *reinterpret_cast<const XV*>(xlane + static_cast<unsigned>((r + 1) & (kClRingRows - 1)) * kClRowBytes);
+                double a[kC]; // x + S(r-1, .): independent of the left neighbour
+#pragma unroll
+                for (int k = 0; k < kC; ++k) a[k] = dadd(widen(x[k]), prev[k]);
+                double left = __shfl_up_sync(0xffffffffu, prev[kC - 1], 1);
+                const double from_strip = __shfl_sync(0xffffffffu, e, u); // lane u polled row s0 + u
+                if (lane == 0) left = from_strip;
+                double sv[kC];
+                sv[0] = dsub(dadd(a[0], left), left_prev);
+#pragma unroll
+                for (int k = 1; k < kC; ++k) sv[k] = dsub(dadd(a[k], sv[k - 1]), prev[k - 1]);
+                if (act) {
+                    if (valid) {
+                        UWB_DCHECK(r >= 0 && r < rows && c + kC <= cols &&
+                                   trow == table + static_cast<int64_t>(r + 1) * tld + kTabShift + 1 + c);
+#pragma unroll
+                        for (int q = 0; q < kC / 2; ++q)
+                            reinterpret_cast<double2*>(trow)[q] = make_double2(sv[2 * q], sv[2 * q + 1]);
+                    }
+                    UWB_DCHECK(!edge_lane || static_cast<unsigned>(r) * 8u < edge_bytes);
+                    st_edge_remote(edge_out + 8ull * static_cast<unsigned>(s0 + u), sv[kC - 1], edge_lane);
+                    left_prev = left;
+#pragma unroll
+                    for (int k = 0; k < kC; ++k) prev[k] = sv[k];
+                }
+                trow += tld;
+            }
+        };
+
+        double e_ahead = has_in ? __longlong_as_double(kClSentinel) : 0.0; // strip 0: S(r, -1) = 0
+#pragma unroll 1
+        for (int b = 0; b < n_blocks; ++b) {
+            const int s0 = b * kClBlock;
+            if (s0 < rows) mbar_wait(&full[b & (kClChunks - 1)], static_cast<unsigned>((b / kClChunks) & 1));
+            // lane i < 8: the left strip's S(s0 + i, last column), read one block
+            // ahead; polled only when it had not arrived by then
+            double e = e_ahead;
+            if (has_in) {
+                const unsigned p = edge_in_s + 8u * static_cast<unsigned>(s0 + lane);
+                if (lane < kClBlock && s0 + lane < rows)
+                    while (__double_as_longlong(e) == kClSentinel) e = ld_edge_poll(p);
+                __syncwarp();
+                if (lane < kClBlock && s0 + kClBlock + lane < rows) e_ahead = ld_edge_poll(p + 8u * kClBlock);
+            }
+            if (s0 >= kWarp - 1 && s0 + kClBlock <= rows) steps8(s0, e, std::false_type{});
+            else steps8(s0, e, std::true_type{});
+            // rows below 8b - 23 are not read again: chunk b - 4 may be refilled
+            if (b >= 4 && b - 4 + kClChunks < n_chunks) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[(b - 4) & (kClChunks - 1)]);
+            }
+        }
+        // non-finite inputs poison every later S of their column (sat.cu header)
+        bool finite = true;
+#pragma unroll
+        for (int k = 0; k < kC; ++k) finite &= isfinite(prev[k]);
+        if (valid && !finite && J.nonfinite) {
+            int col = c;
+            const int bad = first_nonfinite<T>(static_cast<const T*>(J.src), ld, c, kC, rows, &col);
+            if (bad != INT_MAX)
+                report_min(J.nonfinite,
+                           static_cast<unsigned long long>((J.row0 + bad) * L.geo.map_cols + J.col0 + col));
+        }
+    }
+    __syncthreads();
+    cluster_sync_all(); // a CTA's shared memory must outlive its neighbour's stores
+}
+
+struct ClShape {
+    int spc, csize;
+    unsigned edge_bytes;
+    size_t smem;
+};
+
+static bool cluster_shape(int64_t cols, int64_t rows, int elem, ClShape* S) {
+    const int64_t strip_cols = kWarp * (16 / elem);
+    const int64_t strips = (cols + strip_cols - 1) / strip_cols;
+    const int64_t spc = (strips + kClMaxCtas - 1) / kClMaxCtas;
+    if (strips < 1 || spc > kClMaxSpc) return false;
+    if (rows < 1 || rows > 16384) return false;
+    S->spc = static_cast<int>(spc);
+    S->csize = static_cast<int>((strips + spc - 1) / spc);
+    S->edge_bytes = static_cast<unsigned>((rows * 8 + 127) / 128 * 128);
+    S->smem = static_cast<size_t>(spc) * (kClRingBytes + S->edge_bytes + kClBarBytes);
+    return S->smem <= kClSmemCap;
+}
+
+} // namespace
+
+// One cluster per table when every cluster of the batch is resident at once
+// (dense tables, 16-byte aligned rows whose length is a multiple of 16 bytes).
+bool sat_cluster_fits(int64_t n_jobs, int64_t cols, int64_t max_rows, int dtype) {
+    const int elem = dtype == UWB_F32 ? 4 : 8;
+    ClShape S;
+    if (n_jobs < 1 || (cols * elem) % 16 != 0 || !cluster_shape(cols, max_rows, elem, &S)) return false;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return n_jobs * S.csize <= sms;
+}
+
+bool sat_cluster_eligible(const SatLaunch& L, int dtype) {
+    if (L.need || !L.vec_ok) return false;
+    // column bands start at multiples of 32 columns: every band row stays 16-byte aligned
+    return sat_cluster_fits(L.n_jobs, L.cols, L.geo.max_table_rows(), dtype);
+}
+
+template <typename T>
+static cudaError_t launch_sat_cluster_t(const SatLaunch& L, const ClShape& S, cudaStream_t stream) {
+    auto kern = sat_cluster_kernel<T>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S.smem));
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(L.n_jobs * S.csize), 1, 1);
+    cfg.blockDim = dim3(static_cast<unsigned>(2 * S.spc * kWarp), 1, 1);
+    cfg.dynamicSmemBytes = S.smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = static_cast<unsigned>(S.csize);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ++g_kernel_launches;
+    return cudaLaunchKernelEx(&cfg, kern, L, S.spc, S.csize, S.edge_bytes);
+}
+
+cudaError_t launch_sat_cluster(const SatLaunch& L, int dtype, cudaStream_t stream) {
+    ClShape S;
+    if (!cluster_shape(L.cols, L.geo.max_table_rows(), dtype == UWB_F32 ? 4 : 8, &S)) return cudaErrorInvalidValue;
+    return dtype == UWB_F32 ? launch_sat_cluster_t<float>(L, S, stream) : launch_sat_cluster_t<double>(L, S, stream);
+}
+
+} // namespace uwb
