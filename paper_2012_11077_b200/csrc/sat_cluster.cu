@@ -42,15 +42,24 @@ namespace uwb {
 
 namespace {
 
-constexpr int kClBlock = 8;                        // steps per block = rows per staged chunk
+#ifndef UWB_CL_PROBE
+#define UWB_CL_PROBE 0 // timing probes (scripts/cl_probe.sh): 1 no table stores, 2 no hand-over shuffle, 4 no source waits
+#endif
+#ifndef UWB_CL_BLOCK
+#define UWB_CL_BLOCK 32
+#endif
+constexpr int kClBlock = UWB_CL_BLOCK;             // steps per block = rows per staged chunk
 constexpr int kClRingRows = 128;                   // source ring rows per strip
-constexpr int kClChunks = kClRingRows / kClBlock;  // 16 chunks, 5 live
+constexpr int kClChunks = kClRingRows / kClBlock;  // chunks of the ring
+constexpr int kClGroup = 8;                        // hand-over values polled per group of steps
+constexpr int kClBack = (kWarp - 1 + kClBlock - 1) / kClBlock; // chunks behind the newest that are still read
 constexpr int kClRowBytes = kWarp * 16;            // 512 bytes of source per strip row
 constexpr unsigned kClRingBytes = kClRingRows * kClRowBytes; // 64 KB per strip
 constexpr int kClMaxSpc = 3;                       // strips per CTA
 constexpr int kClMaxCtas = 8;                      // portable cluster size
 constexpr size_t kClSmemCap = 227 * 1024;
 constexpr unsigned kClBarBytes = 2 * kClChunks * sizeof(uint64_t);
+constexpr unsigned kClZeroBytes = 128;             // strip 0's "hand-over values"
 
 __device__ __forceinline__ unsigned cluster_ctarank() {
     unsigned r;
@@ -79,15 +88,27 @@ __device__ __forceinline__ void st_edge_remote(unsigned long long addr, double v
         "}\n" ::"l"(addr),
         "d"(v), "r"(on)); // no memory clobber: ordered against the other volatile asm only
 }
-__device__ __forceinline__ double ld_edge_poll(unsigned addr) {
-    double v;
-    asm volatile("ld.relaxed.cluster.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
-    return v;
+// two consecutive rows per load; every 8-byte element is its own single-copy atomic access
+__device__ __forceinline__ void ld_edge_poll2(unsigned addr, double& a, double& b) {
+    asm volatile("ld.relaxed.cluster.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "r"(addr) : "memory");
 }
 // "Not yet written": a signalling NaN. Every S is the result of an IEEE
 // addition, and an addition never returns a signalling NaN (a NaN result is
 // quiet whatever the inputs), so no table value can equal the sentinel.
 constexpr long long kClSentinel = 0x7ff0000000000001LL;
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -101,6 +122,11 @@ struct XVec<double> {
         x[0] = v.x;
         x[1] = v.y;
     }
+    static __device__ __forceinline__ double2 lds(unsigned addr) {
+        double2 v;
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+        return v;
+    }
 };
 template <>
 struct XVec<float> {
@@ -110,6 +136,11 @@ struct XVec<float> {
         x[1] = v.y;
         x[2] = v.z;
         x[3] = v.w;
+    }
+    static __device__ __forceinline__ float4 lds(unsigned addr) {
+        float4 v;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+        return v;
     }
 };
 
@@ -139,10 +170,13 @@ sat_cluster_kernel(SatLaunch L, int spc, int csize, unsigned edge_bytes) {
     uint64_t* full = reinterpret_cast<uint64_t*>(edges + static_cast<size_t>(spc) * edge_bytes +
                                                  static_cast<size_t>(j) * kClBarBytes);
     uint64_t* empty = full + kClChunks;
+    unsigned char* zeros = edges + static_cast<size_t>(spc) * (edge_bytes + kClBarBytes); // kClZeroBytes
+    const unsigned zero_s = smem_u32(zeros);
 
     // every edge value starts as the sentinel; barriers: one arrival per phase
     for (unsigned i = threadIdx.x; i < static_cast<unsigned>(spc) * edge_bytes / 8; i += blockDim.x)
         reinterpret_cast<long long*>(edges)[i] = kClSentinel;
+    if (threadIdx.x < kClZeroBytes / 8) reinterpret_cast<long long*>(zeros)[threadIdx.x] = 0;
     if (!helper && lane == 0) {
         for (int i = 0; i < kClChunks; ++i) {
             mbar_init(&full[i], 1);
@@ -162,7 +196,12 @@ sat_cluster_kernel(SatLaunch L, int spc, int csize, unsigned edge_bytes) {
             const T* src = static_cast<const T*>(J.src) + c0;
             for (int q = 0; q < n_chunks; ++q) {
                 const int slot = q & (kClChunks - 1);
-                if (q >= kClChunks) mbar_wait(&empty[slot], static_cast<unsigned>(((q / kClChunks) - 1) & 1));
+                // sleeping between tries: a spinning try_wait loop shares the SM's shared-memory
+                // pipeline with the compute warp's shuffles and loads and stretches every step
+                if (q >= kClChunks) {
+                    const unsigned par = static_cast<unsigned>(((q / kClChunks) - 1) & 1);
+                    while (!mbar_test(&empty[slot], par)) __nanosleep(256);
+                }
                 const int nr = min(kClBlock, rows - kClBlock * q);
                 if (lane == 0) mbar_expect_tx(&full[slot], static_cast<unsigned>(nr) * row_bytes);
                 __syncwarp();
@@ -191,7 +230,10 @@ sat_cluster_kernel(SatLaunch L, int spc, int csize, unsigned edge_bytes) {
         const unsigned edge_lane = has_out && lane == kWarp - 1 ? 1u : 0u;
         edge_out -= 8ull * static_cast<unsigned>(lane); // + 8 s = row s - lane
         const unsigned edge_in_s = smem_u32(edge_in);
-        const unsigned char* xlane = ring + 16 * lane;
+        // every shared address of the loop is a 32-bit shared-window address held in a
+        // register (a generic pointer would be converted again in every block)
+        const unsigned xbase = smem_u32(ring) + 16u * static_cast<unsigned>(lane);
+        unsigned xoff = (static_cast<unsigned>(-lane) & (kClRingRows - 1)) * kClRowBytes; // ring row of my step-0 row
         double prev[kC]; // S(r-1, c + k)
 #pragma unroll
         for (int k = 0; k < kC; ++k) prev[k] = 0.0;
@@ -200,32 +242,64 @@ sat_cluster_kernel(SatLaunch L, int spc, int csize, unsigned edge_bytes) {
         double* trow = table + kTabShift + 1 + c + static_cast<int64_t>(1 - lane) * tld;
         const int steps = rows + kWarp - 1;
         const int n_blocks = (steps + kClBlock - 1) / kClBlock;
+        using XV = typename XVec<T>::type;
+        XV xn; // source values of the next step (loaded one step ahead inside a block)
 
-        auto steps8 = [&](const int s0, const double e, auto checked_tag) {
+        // Hand-over values: f[i] = the left strip's S(row, last column) for the 8 rows
+        // of a group of steps, fn[] the next group's, read one group ahead. Every lane
+        // reads the same 64 bytes (a broadcast: no shuffle, no divergence, no staging
+        // between the hand-over and lane 0's additions); a value still equal to the
+        // sentinel is polled when its group starts. Strip 0 reads a block of zeros
+        // (S(r, -1) = 0) with a stride of 0, so the loop has no "first strip" branch.
+        double f[kClGroup], fn[kClGroup];
+        unsigned ep = has_in ? edge_in_s : zero_s;          // address of the next group to load
+        const unsigned ep_step = has_in ? 8u * kClGroup : 0u;
+        auto load_group = [&](const unsigned p, double (&v)[kClGroup]) {
+#pragma unroll
+            for (int i = 0; i < kClGroup; i += 2) ld_edge_poll2(p + 8u * i, v[i], v[i + 1]);
+        };
+        load_group(ep, fn);
+
+        auto block = [&](const int s0, auto checked_tag) {
             constexpr bool kChecked = decltype(checked_tag)::value;
-            using XV = typename XVec<T>::type;
-            // the next step's source values are loaded one step ahead
-            XV xn = *reinterpret_cast<const XV*>(xlane + static_cast<unsigned>((s0 - lane) & (kClRingRows - 1)) * kClRowBytes);
 #pragma unroll
             for (int u = 0; u < kClBlock; ++u) {
+                if (u % kClGroup == 0) {
+                    bool miss = false;
+#pragma unroll
+                    for (int i = 0; i < kClGroup; ++i) {
+                        f[i] = fn[i];
+                        miss |= (!kChecked || s0 + u + i < rows) && __double_as_longlong(f[i]) == kClSentinel;
+                    }
+                    while (miss) { // warp-uniform: every lane reads the same values
+                        load_group(ep, f);
+                        miss = false;
+#pragma unroll
+                        for (int i = 0; i < kClGroup; ++i)
+                            miss |= (!kChecked || s0 + u + i < rows) && __double_as_longlong(f[i]) == kClSentinel;
+                    }
+                    ep += ep_step;
+                    if (!kChecked || s0 + u + kClGroup < rows) load_group(ep, fn); // (never past the edge column)
+                }
                 const int r = s0 + u - lane;
                 const bool act = !kChecked || (r >= 0 && r < rows);
                 T x[kC];
                 XVec<T>::get(xn, x);
-                if (u + 1 < kClBlock)
-                    xn = *reinterpret_cast<const XV*>(xlane + static_cast<unsigned>((r + 1) & (kClRingRows - 1)) * kClRowBytes);
+                xoff = (xoff + kClRowBytes) & (kClRingBytes - 1u);
+                if (u + 1 < kClBlock) xn = XVec<T>::lds(xbase + xoff);
                 double a[kC]; // x + S(r-1, .): independent of the left neighbour
 #pragma unroll
                 for (int k = 0; k < kC; ++k) a[k] = dadd(widen(x[k]), prev[k]);
                 double left = __shfl_up_sync(0xffffffffu, prev[kC - 1], 1);
-                const double from_strip = __shfl_sync(0xffffffffu, e, u); // lane u polled row s0 + u
-                if (lane == 0) left = from_strip;
+#if !(UWB_CL_PROBE & 2)
+                if (lane == 0) left = f[u % kClGroup];
+#endif
                 double sv[kC];
                 sv[0] = dsub(dadd(a[0], left), left_prev);
 #pragma unroll
                 for (int k = 1; k < kC; ++k) sv[k] = dsub(dadd(a[k], sv[k - 1]), prev[k - 1]);
                 if (act) {
-                    if (valid) {
+                    if (valid && !(UWB_CL_PROBE & 1)) {
                         UWB_DCHECK(r >= 0 && r < rows && c + kC <= cols &&
                                    trow == table + static_cast<int64_t>(r + 1) * tld + kTabShift + 1 + c);
 #pragma unroll
@@ -242,27 +316,19 @@ sat_cluster_kernel(SatLaunch L, int spc, int csize, unsigned edge_bytes) {
             }
         };
 
-        double e_ahead = has_in ? __longlong_as_double(kClSentinel) : 0.0; // strip 0: S(r, -1) = 0
 #pragma unroll 1
         for (int b = 0; b < n_blocks; ++b) {
             const int s0 = b * kClBlock;
-            if (s0 < rows) mbar_wait(&full[b & (kClChunks - 1)], static_cast<unsigned>((b / kClChunks) & 1));
-            // lane i < 8: the left strip's S(s0 + i, last column), read one block
-            // ahead; polled only when it had not arrived by then
-            double e = e_ahead;
-            if (has_in) {
-                const unsigned p = edge_in_s + 8u * static_cast<unsigned>(s0 + lane);
-                if (lane < kClBlock && s0 + lane < rows)
-                    while (__double_as_longlong(e) == kClSentinel) e = ld_edge_poll(p);
+            // this block reads rows s0 - 31 .. s0 + 31: chunks b - 1 (waited for) and b
+            if (!(UWB_CL_PROBE & 4) && s0 < rows)
+                mbar_wait(&full[b & (kClChunks - 1)], static_cast<unsigned>((b / kClChunks) & 1));
+            xn = XVec<T>::lds(xbase + xoff);
+            if (s0 >= kWarp - 1 && s0 + kClBlock <= rows) block(s0, std::false_type{});
+            else block(s0, std::true_type{});
+            // the next block reads rows >= s0 + 1: chunk b - 1 may be refilled
+            if (b >= kClBack && b - kClBack + kClChunks < n_chunks) {
                 __syncwarp();
-                if (lane < kClBlock && s0 + kClBlock + lane < rows) e_ahead = ld_edge_poll(p + 8u * kClBlock);
-            }
-            if (s0 >= kWarp - 1 && s0 + kClBlock <= rows) steps8(s0, e, std::false_type{});
-            else steps8(s0, e, std::true_type{});
-            // rows below 8b - 23 are not read again: chunk b - 4 may be refilled
-            if (b >= 4 && b - 4 + kClChunks < n_chunks) {
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[(b - 4) & (kClChunks - 1)]);
+                if (lane == 0) mbar_arrive(&empty[(b - kClBack) & (kClChunks - 1)]);
             }
         }
         // non-finite inputs poison every later S of their column (sat.cu header)
@@ -295,8 +361,9 @@ static bool cluster_shape(int64_t cols, int64_t rows, int elem, ClShape* S) {
     if (rows < 1 || rows > 16384) return false;
     S->spc = static_cast<int>(spc);
     S->csize = static_cast<int>((strips + spc - 1) / spc);
-    S->edge_bytes = static_cast<unsigned>((rows * 8 + 127) / 128 * 128);
-    S->smem = static_cast<size_t>(spc) * (kClRingBytes + S->edge_bytes + kClBarBytes);
+    // one group past the last row is read ahead (and stays a sentinel)
+    S->edge_bytes = static_cast<unsigned>((rows * 8 + 8 * kClGroup + 127) / 128 * 128);
+    S->smem = static_cast<size_t>(spc) * (kClRingBytes + S->edge_bytes + kClBarBytes) + kClZeroBytes;
     return S->smem <= kClSmemCap;
 }
 

@@ -7,7 +7,7 @@ from paper_2012_11077_b200 import synth
 from paper_2012_11077_b200.batch import BatchCfar, phase_ms
 
 for (rows, cols, dt, g, b) in [(1024, 600, torch.float64, 4, 8), (256, 512, torch.float64, 2, 8),
-                               (1024, 1024, torch.float32, 2, 8)]:
+                               (1024, 1024, torch.float32, 2, 8), (1024, 8, torch.float64, 4, 8)]:
     m = synth.exponential_maps(1, rows, cols, seed=77, dtype=dt, device="cuda")
     r = BatchCfar(1, rows, cols, uwb.CfarParams(g, b, 1e-4), dt, det_capacity=1 << 14)
     for cta in (False, True):
