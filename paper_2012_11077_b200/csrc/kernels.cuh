@@ -224,7 +224,7 @@ int sat_cpl_for(int64_t n_jobs, int64_t cols);   // columns per lane for a batch
 bool sat_cta_eligible(int64_t n_jobs, int64_t cols, int dtype);
 // small batches whose tables each run as one thread-block cluster (sat_cluster.cu: strips hand
 // over through distributed shared memory); _fits: by shape, _eligible: shape and alignment
-bool sat_cluster_fits(int64_t n_jobs, int64_t cols, int64_t max_rows, int dtype);
+bool sat_cluster_fits(int64_t n_jobs, int64_t cols, int64_t max_rows, int dtype, bool allow_chain = false);
 bool sat_cluster_eligible(const SatLaunch& L, int dtype);
 cudaError_t launch_sat_cluster(const SatLaunch& L, int dtype, cudaStream_t stream);
 

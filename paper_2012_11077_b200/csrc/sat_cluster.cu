@@ -33,6 +33,9 @@
 //     global address for its inputs.
 // The same three additions per cell in the same order: bit-identical tables.
 #include <climits>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <type_traits>
 
 #include "common.cuh"
@@ -84,7 +87,7 @@ __device__ __forceinline__ void st_edge_remote(unsigned long long addr, double v
         "{\n"
         ".reg .pred p;\n"
         "setp.ne.u32 p, %2, 0;\n"
-        "@p st.relaxed.cluster.f64 [%0], %1;\n"
+        "@p st.relaxed.gpu.f64 [%0], %1;\n"
         "}\n" ::"l"(addr),
         "d"(v), "r"(on)); // no memory clobber: ordered against the other volatile asm only
 }
@@ -145,17 +148,23 @@ struct XVec<float> {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(kClMaxSpc * 2 * kWarp, 1)
-sat_cluster_kernel(SatLaunch L, int spc, int csize, unsigned edge_bytes) {
+__global__ void __launch_bounds__((kClMaxSpc * 2 + 1) * kWarp, 1)
+sat_cluster_kernel(SatLaunch L, int spc, int csize, int chain, unsigned edge_bytes) {
     constexpr int kC = 16 / static_cast<int>(sizeof(T));
     constexpr int kStripCols = kWarp * kC;
     extern __shared__ __align__(128) unsigned char cl_smem[];
     const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
     const unsigned rank = cluster_ctarank();
-    const int64_t job = blockIdx.x / csize;
-    const bool helper = warp >= spc;
-    const int j = helper ? warp - spc : warp;           // my strip inside the CTA
-    const int g = static_cast<int>(rank) * spc + j;     // my strip of the table
+    // a table wider than one cluster's strips is a chain of `chain` clusters (cluster q
+    // of a job owns strips [q, q + 1) * csize * spc); clusters are dispatched in
+    // block-index order, so the cluster a strip waits on started earlier
+    const int cl = static_cast<int>(blockIdx.x) / csize;
+    const int q_cl = cl % chain;
+    const int64_t job = cl / chain;
+    const bool relay = warp == 2 * spc;                 // one extra warp: the global hand-over's relay
+    const bool helper = warp >= spc && !relay;
+    const int j = relay ? 0 : (helper ? warp - spc : warp); // my strip inside the CTA
+    const int g = (q_cl * csize + static_cast<int>(rank)) * spc + j; // my strip of the table
     const int cols = static_cast<int>(L.cols);
     const int strips = (cols + kStripCols - 1) / kStripCols;
     const bool live = g < strips;
@@ -188,7 +197,27 @@ sat_cluster_kernel(SatLaunch L, int spc, int csize, unsigned edge_bytes) {
     cluster_sync_all(); // nobody stores into a neighbour before its sentinels are in place
 
     const int n_chunks = (rows + kClBlock - 1) / kClBlock;
-    if (helper) {
+    if (relay) {
+        // The first strip of a chained cluster takes its left edge from the previous
+        // cluster through global memory: this warp polls that column (lane l: rows
+        // l, l + 32, ...; the same sentinel, written by fill_sentinel_kernel) and stores
+        // every value that has arrived into the strip's shared edge column, so the
+        // compute warp polls shared memory like every other strip.
+        if (rank == 0 && q_cl > 0 && live) {
+            const double* ge = L.gedge + (job * L.strips + (q_cl - 1)) * L.edge_stride;
+            const unsigned dst = smem_u32(edge_in);
+            for (int r = lane; r < rows; r += kWarp) {
+                double v;
+                for (;;) {
+                    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(ge + r) : "memory");
+                    if (__double_as_longlong(v) != kClSentinel) break;
+                    __nanosleep(64);
+                }
+                asm volatile("st.relaxed.cluster.shared::cta.f64 [%0], %1;" ::"r"(dst + 8u * static_cast<unsigned>(r)), "d"(v)
+                             : "memory");
+            }
+        }
+    } else if (helper) {
         if (live) {
             const int c0 = g * kStripCols;
             const unsigned row_bytes =
@@ -224,8 +253,12 @@ sat_cluster_kernel(SatLaunch L, int spc, int csize, unsigned edge_bytes) {
         const bool has_in = g > 0, has_out = g + 1 < strips;
         unsigned long long edge_out = 0; // S(r, my last column) of lane 31 goes to edge_out + 8 r
         if (has_out) {
-            const int gn = g + 1;
-            edge_out = map_to_cta(edges + static_cast<size_t>(gn % spc) * edge_bytes, static_cast<unsigned>(gn / spc));
+            const int gn = g + 1, per_cluster = spc * csize;
+            if (gn / per_cluster == q_cl) // the right neighbour is in my cluster: its shared memory
+                edge_out = map_to_cta(edges + static_cast<size_t>(gn % spc) * edge_bytes,
+                                      static_cast<unsigned>((gn % per_cluster) / spc));
+            else // the next cluster of the chain: boundary column q_cl in global memory
+                edge_out = reinterpret_cast<unsigned long long>(L.gedge + (job * L.strips + q_cl) * L.edge_stride);
         }
         const unsigned edge_lane = has_out && lane == kWarp - 1 ? 1u : 0u;
         edge_out -= 8ull * static_cast<unsigned>(lane); // + 8 s = row s - lane
@@ -348,43 +381,124 @@ sat_cluster_kernel(SatLaunch L, int spc, int csize, unsigned edge_bytes) {
 }
 
 struct ClShape {
-    int spc, csize;
+    int spc, csize, chain;
     unsigned edge_bytes;
     size_t smem;
 };
 
-static bool cluster_shape(int64_t cols, int64_t rows, int elem, ClShape* S) {
+template <typename T>
+__global__ void sat_cluster_kernel(SatLaunch L, int spc, int csize, int chain, unsigned edge_bytes);
+
+// Clusters of `csize` CTAs with this much shared memory that the device keeps
+// resident at once (the GPCs limit how many 8-CTA clusters fit: a chain whose last
+// clusters only start when the first ones finish would double its time).
+static int max_active_clusters(int elem, int csize, int spc, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int, size_t>, int> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_tuple(elem, csize, spc, smem);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(csize), 1, 1);
+    cfg.blockDim = dim3(static_cast<unsigned>((2 * spc + 1) * kWarp), 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = static_cast<unsigned>(csize);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    cudaError_t e;
+    if (elem == 4) {
+        e = cudaFuncSetAttribute(sat_cluster_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveClusters(&n, sat_cluster_kernel<float>, &cfg);
+    } else {
+        e = cudaFuncSetAttribute(sat_cluster_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveClusters(&n, sat_cluster_kernel<double>, &cfg);
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+    }
+    cache[key] = n;
+    return n;
+}
+
+// Strips per CTA, CTAs per cluster and clusters per table. Up to 24 strips run as
+// one cluster; wider tables as a chain of clusters (8, 4, 2 or 1 CTAs: the largest
+// that keeps every cluster of the batch resident at once) with the fewest strips
+// per CTA.
+static bool cluster_shape(int64_t cols, int64_t rows, int elem, int64_t n_jobs, int sms, ClShape* S) {
     const int64_t strip_cols = kWarp * (16 / elem);
     const int64_t strips = (cols + strip_cols - 1) / strip_cols;
-    const int64_t spc = (strips + kClMaxCtas - 1) / kClMaxCtas;
-    if (strips < 1 || spc > kClMaxSpc) return false;
-    if (rows < 1 || rows > 16384) return false;
-    S->spc = static_cast<int>(spc);
-    S->csize = static_cast<int>((strips + spc - 1) / spc);
+    if (strips < 1 || rows < 1 || rows > 16384 || n_jobs < 1) return false;
     // one group past the last row is read ahead (and stays a sentinel)
     S->edge_bytes = static_cast<unsigned>((rows * 8 + 8 * kClGroup + 127) / 128 * 128);
-    S->smem = static_cast<size_t>(spc) * (kClRingBytes + S->edge_bytes + kClBarBytes) + kClZeroBytes;
-    return S->smem <= kClSmemCap;
+    const size_t per_strip = kClRingBytes + S->edge_bytes + kClBarBytes;
+    // pass 0: one cluster (hand-overs through shared memory only); pass 1: a chain
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int cmax = kClMaxCtas; cmax >= 1; cmax /= 2) {
+            for (int spc = 1; spc <= kClMaxSpc; ++spc) {
+                if (spc * per_strip + kClZeroBytes > kClSmemCap) break;
+                const int64_t ctas = (strips + spc - 1) / spc;
+                const int64_t chain = (ctas + cmax - 1) / cmax;
+                const int64_t csize = chain == 1 ? ctas : cmax;
+                if ((pass == 0) != (chain == 1) || n_jobs * chain * csize > sms) continue;
+                const size_t smem = spc * per_strip + kClZeroBytes;
+                if (pass == 1 && max_active_clusters(elem, static_cast<int>(csize), spc, smem) < n_jobs * chain) continue;
+                S->spc = spc;
+                S->csize = static_cast<int>(csize);
+                S->chain = static_cast<int>(chain);
+                S->smem = smem;
+                return true;
+            }
+            if (pass == 0) break; // one cluster: only the 8-CTA limit applies
+        }
+    }
+    return false;
+}
+
+static int sm_count() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
+
+__global__ void fill_sentinel_kernel(double* gedge, int64_t strips, int64_t edge_stride, int chain, int64_t rows) {
+    // boundary column q of job blockIdx.y: (job * strips + q) * edge_stride
+    const int64_t q = blockIdx.x % chain, part = blockIdx.x / chain, parts = gridDim.x / chain;
+    long long* col = reinterpret_cast<long long*>(gedge + (static_cast<int64_t>(blockIdx.y) * strips + q) * edge_stride);
+    for (int64_t r = part * blockDim.x + threadIdx.x; r < rows; r += parts * blockDim.x) col[r] = kClSentinel;
 }
 
 } // namespace
 
-// One cluster per table when every cluster of the batch is resident at once
-// (dense tables, 16-byte aligned rows whose length is a multiple of 16 bytes).
-bool sat_cluster_fits(int64_t n_jobs, int64_t cols, int64_t max_rows, int dtype) {
+// One cluster (or, with `allow_chain`, a chain of clusters) per table when every
+// CTA of the batch is resident at once (dense tables, 16-byte aligned rows whose
+// length is a multiple of 16 bytes).
+bool sat_cluster_fits(int64_t n_jobs, int64_t cols, int64_t max_rows, int dtype, bool allow_chain) {
     const int elem = dtype == UWB_F32 ? 4 : 8;
     ClShape S;
-    if (n_jobs < 1 || (cols * elem) % 16 != 0 || !cluster_shape(cols, max_rows, elem, &S)) return false;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    return n_jobs * S.csize <= sms;
+    if (n_jobs < 1 || (cols * elem) % 16 != 0 || !cluster_shape(cols, max_rows, elem, n_jobs, sm_count(), &S)) return false;
+    return allow_chain || S.chain == 1;
 }
 
 bool sat_cluster_eligible(const SatLaunch& L, int dtype) {
-    if (L.need || !L.vec_ok) return false;
+    if (!L.vec_ok) return false;
     // column bands start at multiples of 32 columns: every band row stays 16-byte aligned
-    return sat_cluster_fits(L.n_jobs, L.cols, L.geo.max_table_rows(), dtype);
+    const int elem = dtype == UWB_F32 ? 4 : 8;
+    ClShape S;
+    if ((L.cols * elem) % 16 != 0 || !cluster_shape(L.cols, L.geo.max_table_rows(), elem, L.n_jobs, sm_count(), &S))
+        return false;
+    // a sparse-mode call (certified path) only reaches here with a table too wide for
+    // the small-batch exact path: the chain writes the whole table, a superset of the
+    // marked taps, far faster than the one-warp-per-strip chain of sat.cu
+    if (L.need) return S.chain > 1 && L.gedge != nullptr;
+    return S.chain == 1 || L.gedge != nullptr;
 }
 
 template <typename T>
@@ -392,9 +506,16 @@ static cudaError_t launch_sat_cluster_t(const SatLaunch& L, const ClShape& S, cu
     auto kern = sat_cluster_kernel<T>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S.smem));
     if (e != cudaSuccess) return e;
+    if (S.chain > 1) {
+        // the boundary columns between the clusters of a chain start as sentinels
+        ++g_kernel_launches;
+        fill_sentinel_kernel<<<dim3(static_cast<unsigned>(S.chain * 4), static_cast<unsigned>(L.n_jobs)), 256, 0, stream>>>(
+            L.gedge, L.strips, L.edge_stride, S.chain, L.geo.max_table_rows());
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(static_cast<unsigned>(L.n_jobs * S.csize), 1, 1);
-    cfg.blockDim = dim3(static_cast<unsigned>(2 * S.spc * kWarp), 1, 1);
+    cfg.gridDim = dim3(static_cast<unsigned>(L.n_jobs * S.chain * S.csize), 1, 1);
+    cfg.blockDim = dim3(static_cast<unsigned>((2 * S.spc + 1) * kWarp), 1, 1);
     cfg.dynamicSmemBytes = S.smem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
@@ -405,12 +526,14 @@ static cudaError_t launch_sat_cluster_t(const SatLaunch& L, const ClShape& S, cu
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     ++g_kernel_launches;
-    return cudaLaunchKernelEx(&cfg, kern, L, S.spc, S.csize, S.edge_bytes);
+    return cudaLaunchKernelEx(&cfg, kern, L, S.spc, S.csize, S.chain, S.edge_bytes);
 }
 
 cudaError_t launch_sat_cluster(const SatLaunch& L, int dtype, cudaStream_t stream) {
     ClShape S;
-    if (!cluster_shape(L.cols, L.geo.max_table_rows(), dtype == UWB_F32 ? 4 : 8, &S)) return cudaErrorInvalidValue;
+    if (!cluster_shape(L.cols, L.geo.max_table_rows(), dtype == UWB_F32 ? 4 : 8, L.n_jobs, sm_count(), &S))
+        return cudaErrorInvalidValue;
+    if (S.chain > 1 && (!L.gedge || S.chain > L.strips || L.geo.max_table_rows() > L.edge_stride)) return cudaErrorInvalidValue;
     return dtype == UWB_F32 ? launch_sat_cluster_t<float>(L, S, stream) : launch_sat_cluster_t<double>(L, S, stream);
 }
 

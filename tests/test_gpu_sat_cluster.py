@@ -52,6 +52,25 @@ def test_cluster_sat_f32_bit_identical(ref, cuda, rows, cols):
     assert_bitwise(got[0], ref.build_sat(m.astype(np.float64)), f"cluster SAT f32 {rows}x{cols}")
 
 
+@pytest.mark.parametrize("rows,cols,dt", [(300, 4000, np.float32), (33, 3200, np.float32), (1000, 8192, np.float32),
+                                          (200, 2048, np.float64), (70, 1600, np.float64)])
+def test_cluster_chain_bit_identical(ref, cuda, rows, cols, dt):
+    """Tables wider than one cluster's 24 strips: a chain of 8-CTA clusters, the
+    boundary columns handed over through global memory (relay warp)."""
+    m = np.random.default_rng(rows + 13 * cols).exponential(1.0, (rows, cols)).astype(dt)
+    got, bad = dev_tables(torch.from_numpy(m).to(cuda).unsqueeze(0).contiguous())
+    assert_bitwise(got[0], ref.build_sat(m.astype(np.float64)), f"cluster chain {rows}x{cols}")
+    assert bad[0] == np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def test_cluster_chain_two_maps(ref, cuda):
+    """Two chained tables in one launch (2 x 4 clusters x 8 CTAs)."""
+    m = np.random.default_rng(17).exponential(1.0, (2, 150, 4096)).astype(np.float32)
+    got, _ = dev_tables(torch.from_numpy(m).to(cuda))
+    for i in range(2):
+        assert_bitwise(got[i], ref.build_sat(m[i].astype(np.float64)), f"cluster chain map {i}")
+
+
 def test_cluster_sat_batch_of_clusters(ref, cuda):
     """18 tables x 8-CTA clusters = 144 CTAs resident at once; every table checked."""
     m = np.random.default_rng(5).exponential(1.0, (18, 300, 500))
