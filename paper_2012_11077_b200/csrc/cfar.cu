@@ -376,6 +376,15 @@ cudaError_t launch_sort_detections(uwb_detection* dets, int64_t cap, const unsig
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     const int64_t runs = (cap + kSortRun - 1) / kSortRun;
+    if (runs > 1 && runs <= 8 && n_maps <= 16 && scratch) {
+        // a few lists of modest capacity (single-map calls): one launch, one CTA per
+        // list sorting its runs and merging them; a short list (the usual case) is one
+        // bitonic sort, and the call saves the 2-4 launches of the multi-CTA passes
+        ++g_kernel_launches;
+        sort_detections_kernel<<<static_cast<unsigned>(n_maps), kSortThreads, smem, stream>>>(dets, cap, counts, scratch,
+                                                                                            false);
+        return cudaGetLastError();
+    }
     if (runs > 1 && runs <= 65535) {
         // long lists: the runs of every list sort in parallel CTAs
         e = cudaFuncSetAttribute(sort_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));

@@ -15,22 +15,38 @@
 //     2 x columns dependent additions of sat.cpp:33 in the reference's
 //     association, and stores its S values straight from registers (the table
 //     of a small map lives in L2, so 16-byte scattered stores cost nothing
-//     and no write-back ring, barrier or second pass sits on the chain);
+//     and no write-back ring, barrier or second pass sits on the chain).
+//     Steps run in straight-line blocks of 32 (a block end costs ~190 cycles
+//     of branches and barrier tests: measured 62 -> 43 ns per step against
+//     8-step blocks; scripts/micro/chain.cu has the bare chain at 22 ns);
 //   * the strips of a table are the CTAs of one thread-block cluster (up to 8
 //     CTAs x up to 3 strips). Lane 31 of strip w stores S(r, last column)
 //     into the shared memory of the CTA that runs strip w + 1 (a relaxed
-//     cluster-scope remote store through DSMEM); that strip's lanes 0..7 poll
-//     their own shared memory for the 8 rows of the next block. Every 8-byte
-//     value is its own flag: the edge column starts as a signalling-NaN
-//     sentinel (no IEEE addition returns one, so no S - not even one poisoned
-//     by a NaN input - can look like "not yet written"), and a whole column of
-//     `rows` values is kept, so there is no ring to recycle, no counter, no
-//     fence and no back-pressure: the chain is self-timed, strip w + 1 runs
-//     32 + ~8 steps behind strip w;
+//     remote store through DSMEM); that strip reads the 8 values of its next
+//     group of steps one group ahead with broadcast shared loads (every lane
+//     the same 64 bytes: no shuffle, no divergence) and polls them when the
+//     group starts if they had not arrived. Every 8-byte value is its own
+//     flag: the edge column starts as a signalling-NaN sentinel (no IEEE
+//     addition returns one, so no S - not even one poisoned by a NaN input -
+//     can look like "not yet written"), and a whole column of `rows` values
+//     is kept, so there is no ring to recycle, no counter, no fence and no
+//     back-pressure: the chain is self-timed, strip w + 1 runs 32 + 8 steps
+//     plus the hand-over latency behind strip w (measured ~75 steps);
+//   * a table wider than 24 strips is a CHAIN of clusters (config 4's global
+//     table: 128 strips, one per SM): the last strip
+//     of a cluster stores its edge column into a global boundary column, and
+//     a relay warp of the next cluster's first CTA polls that column and
+//     copies arrived values into the strip's shared edge column, so the
+//     compute warps are the same in both cases. Clusters are dispatched in
+//     block-index order, so a cluster never waits on one that has not started;
+//     the cluster size (8, 4, 2, 1) is the largest for which
+//     cudaOccupancyMaxActiveClusters keeps the whole chain resident (config 4
+//     with 8-CTA clusters whatever the occupancy: 2.55 ms, the last clusters
+//     waiting for SMs; with the resident size: 1.93 ms);
 //   * a helper warp per strip feeds the source ring with the TMA engine's 1-D
-//     bulk copies (one 512-byte row segment per lane, 8 rows per mbarrier
-//     phase, 11 chunks of look-ahead), so the compute warp never computes a
-//     global address for its inputs.
+//     bulk copies (one 512-byte row segment per lane, 32 rows per mbarrier
+//     phase, a 128-row ring), so the compute warp never computes a global
+//     address for its inputs.
 // The same three additions per cell in the same order: bit-identical tables.
 #include <climits>
 #include <map>
@@ -72,28 +88,41 @@ __device__ __forceinline__ unsigned cluster_ctarank() {
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-// generic address of `local` (a pointer into my shared memory) in CTA `rank` of the cluster
-__device__ __forceinline__ unsigned long long map_to_cta(const void* local, unsigned rank) {
-    unsigned long long r;
-    asm volatile("mapa.u64 %0, %1, %2;" : "=l"(r) : "l"(reinterpret_cast<unsigned long long>(local)), "r"(rank));
-    return r;
-}
 // Hand-over pair: a relaxed cluster-scope store into the neighbour's shared
 // memory against relaxed cluster-scope polls (morally strong, single-copy
 // atomic per 8-byte value). The store is predicated, not branched: only lane
 // 31 of a strip with a right neighbour stores.
-__device__ __forceinline__ void st_edge_remote(unsigned long long addr, double v, unsigned on) {
+__device__ __forceinline__ void st_edge_dsmem(unsigned addr, double v, unsigned on) {
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
         "setp.ne.u32 p, %2, 0;\n"
-        "@p st.relaxed.gpu.f64 [%0], %1;\n"
-        "}\n" ::"l"(addr),
+        "@p st.relaxed.cluster.shared::cluster.f64 [%0], %1;\n"
+        "}\n" ::"r"(addr),
         "d"(v), "r"(on)); // no memory clobber: ordered against the other volatile asm only
+}
+// ... and into the boundary column of a chain (global memory, polled by the next cluster's relay warp)
+__device__ __forceinline__ void st_edge_global(unsigned long long addr, double v, unsigned on) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.u32 p, %2, 0;\n"
+        "@p st.relaxed.gpu.global.f64 [%0], %1;\n"
+        "}\n" ::"l"(addr),
+        "d"(v), "r"(on));
+}
+// shared-window address of `local_s` (an address in my shared memory) in CTA `rank` of the cluster
+__device__ __forceinline__ unsigned map_to_cta_s(unsigned local_s, unsigned rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_s), "r"(rank));
+    return r;
 }
 // two consecutive rows per load; every 8-byte element is its own single-copy atomic access
 __device__ __forceinline__ void ld_edge_poll2(unsigned addr, double& a, double& b) {
-    asm volatile("ld.relaxed.cluster.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "r"(addr) : "memory");
+    // volatile = relaxed at system scope (PTX memory model), and on my own shared memory it is a
+    // plain LDS (~30 cycles); ld.relaxed.cluster.shared::cluster compiles to a generic strong load
+    // whose round trip (~1 us) was added to every strip's lag
+    asm volatile("ld.volatile.shared::cta.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "r"(addr) : "memory");
 }
 // "Not yet written": a signalling NaN. Every S is the result of an IEEE
 // addition, and an addition never returns a signalling NaN (a NaN result is
@@ -251,17 +280,24 @@ sat_cluster_kernel(SatLaunch L, int spc, int csize, int chain, unsigned edge_byt
             for (int k = 0; k < kC; ++k) table[kTabShift + 1 + c + k] = 0.0; // padded row 0
         }
         const bool has_in = g > 0, has_out = g + 1 < strips;
-        unsigned long long edge_out = 0; // S(r, my last column) of lane 31 goes to edge_out + 8 r
+        // S(r, my last column) of lane 31 goes to edge_out + 8 r: the right neighbour's shared
+        // edge column (same cluster) or boundary column q_cl of the chain (global memory)
+        unsigned edge_out_s = 0;
+        unsigned long long edge_out_g = 0;
+        bool out_dsmem = false;
         if (has_out) {
             const int gn = g + 1, per_cluster = spc * csize;
-            if (gn / per_cluster == q_cl) // the right neighbour is in my cluster: its shared memory
-                edge_out = map_to_cta(edges + static_cast<size_t>(gn % spc) * edge_bytes,
-                                      static_cast<unsigned>((gn % per_cluster) / spc));
-            else // the next cluster of the chain: boundary column q_cl in global memory
-                edge_out = reinterpret_cast<unsigned long long>(L.gedge + (job * L.strips + q_cl) * L.edge_stride);
+            out_dsmem = gn / per_cluster == q_cl;
+            if (out_dsmem)
+                edge_out_s = map_to_cta_s(smem_u32(edges + static_cast<size_t>(gn % spc) * edge_bytes),
+                                          static_cast<unsigned>((gn % per_cluster) / spc));
+            else
+                edge_out_g = reinterpret_cast<unsigned long long>(L.gedge + (job * L.strips + q_cl) * L.edge_stride);
         }
-        const unsigned edge_lane = has_out && lane == kWarp - 1 ? 1u : 0u;
-        edge_out -= 8ull * static_cast<unsigned>(lane); // + 8 s = row s - lane
+        const unsigned edge_lane_s = has_out && out_dsmem && lane == kWarp - 1 ? 1u : 0u;
+        const unsigned edge_lane_g = has_out && !out_dsmem && lane == kWarp - 1 ? 1u : 0u;
+        edge_out_s -= 8u * static_cast<unsigned>(lane); // + 8 s = row s - lane
+        edge_out_g -= 8ull * static_cast<unsigned>(lane);
         const unsigned edge_in_s = smem_u32(edge_in);
         // every shared address of the loop is a 32-bit shared-window address held in a
         // register (a generic pointer would be converted again in every block)
@@ -339,8 +375,9 @@ sat_cluster_kernel(SatLaunch L, int spc, int csize, int chain, unsigned edge_byt
                         for (int q = 0; q < kC / 2; ++q)
                             reinterpret_cast<double2*>(trow)[q] = make_double2(sv[2 * q], sv[2 * q + 1]);
                     }
-                    UWB_DCHECK(!edge_lane || static_cast<unsigned>(r) * 8u < edge_bytes);
-                    st_edge_remote(edge_out + 8ull * static_cast<unsigned>(s0 + u), sv[kC - 1], edge_lane);
+                    UWB_DCHECK(!(edge_lane_s | edge_lane_g) || static_cast<unsigned>(r) * 8u < edge_bytes);
+                    st_edge_dsmem(edge_out_s + 8u * static_cast<unsigned>(s0 + u), sv[kC - 1], edge_lane_s);
+                    st_edge_global(edge_out_g + 8ull * static_cast<unsigned>(s0 + u), sv[kC - 1], edge_lane_g);
                     left_prev = left;
 #pragma unroll
                     for (int k = 0; k < kC; ++k) prev[k] = sv[k];
