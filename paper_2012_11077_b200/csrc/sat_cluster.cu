@@ -92,7 +92,27 @@ __device__ __forceinline__ void cluster_sync_all() {
 // memory against relaxed cluster-scope polls (morally strong, single-copy
 // atomic per 8-byte value). The store is predicated, not branched: only lane
 // 31 of a strip with a right neighbour stores.
+#ifndef UWB_CL_SLACK
+#define UWB_CL_SLACK 0 // rows of slack a strip starts with behind its left neighbour (beyond the first group)
+#endif
+#ifndef UWB_CL_HANDOVER
+#define UWB_CL_HANDOVER 0 // 0: st.relaxed.cluster, 1: atom.exch (result unused)
+#endif
 __device__ __forceinline__ void st_edge_dsmem(unsigned addr, double v, unsigned on) {
+#if UWB_CL_HANDOVER == 1
+    // An exchange, not a store: a plain remote store may sit in the sender's write path
+    // for ~2 us before the neighbour sees it (measured: a strip that had caught up with
+    // its left neighbour advanced 8 rows per ~2.3 us); an atomic is performed at the
+    // destination at once (~180 ns one way, scripts/micro/dsmem_pingpong.cu).
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        ".reg .b64 old;\n"
+        "setp.ne.u32 p, %2, 0;\n"
+        "@p atom.relaxed.cluster.shared::cluster.exch.b64 old, [%0], %1;\n"
+        "}\n" ::"r"(addr),
+        "l"(__double_as_longlong(v)), "r"(on));
+#else
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
@@ -100,6 +120,7 @@ __device__ __forceinline__ void st_edge_dsmem(unsigned addr, double v, unsigned 
         "@p st.relaxed.cluster.shared::cluster.f64 [%0], %1;\n"
         "}\n" ::"r"(addr),
         "d"(v), "r"(on)); // no memory clobber: ordered against the other volatile asm only
+#endif
 }
 // ... and into the boundary column of a chain (global memory, polled by the next cluster's relay warp)
 __device__ __forceinline__ void st_edge_global(unsigned long long addr, double v, unsigned on) {
@@ -329,8 +350,20 @@ sat_cluster_kernel(SatLaunch L, int spc, int csize, int chain, unsigned edge_byt
         };
         load_group(ep, fn);
 
-        auto block = [&](const int s0, auto checked_tag) {
-            constexpr bool kChecked = decltype(checked_tag)::value;
+        // One block of 32 steps. Mode 0: interior (every lane's row is inside the map).
+        // Mode 2: the first block (rows >= 32): a lane whose row r = s - lane is still
+        // negative computes a virtual row of zeros (its x reads as zero and its state is
+        // zero, so every S stays +0) - only the stores are predicated, nothing
+        // conditional sits on the dependent chain. Every strip's first 39 steps are the
+        // lag of the strip to its right, so this block is on the critical path of the
+        // whole table. Mode 3: the last blocks (r >= 0 everywhere): lanes past the last
+        // row keep adding zeros, unstored; a non-finite S of the last row stays
+        // non-finite, a finite one stays finite, so the check after the loop holds (and
+        // does not start a column rescan on stale ring contents).
+        // Mode 1: maps shorter than a block (state updates conditional).
+        auto block = [&](const int s0, auto mode_tag) {
+            constexpr int kMode = decltype(mode_tag)::value;
+            constexpr bool kRowCheck = kMode == 1 || kMode == 3; // rows >= `rows` exist in this block
 #pragma unroll
             for (int u = 0; u < kClBlock; ++u) {
                 if (u % kClGroup == 0) {
@@ -338,22 +371,33 @@ sat_cluster_kernel(SatLaunch L, int spc, int csize, int chain, unsigned edge_byt
 #pragma unroll
                     for (int i = 0; i < kClGroup; ++i) {
                         f[i] = fn[i];
-                        miss |= (!kChecked || s0 + u + i < rows) && __double_as_longlong(f[i]) == kClSentinel;
+                        miss |= (!kRowCheck || s0 + u + i < rows) && __double_as_longlong(f[i]) == kClSentinel;
                     }
                     while (miss) { // warp-uniform: every lane reads the same values
+#ifdef UWB_CL_POLL_SLEEP
+                        __nanosleep(UWB_CL_POLL_SLEEP);
+#endif
                         load_group(ep, f);
                         miss = false;
 #pragma unroll
                         for (int i = 0; i < kClGroup; ++i)
-                            miss |= (!kChecked || s0 + u + i < rows) && __double_as_longlong(f[i]) == kClSentinel;
+                            miss |= (!kRowCheck || s0 + u + i < rows) && __double_as_longlong(f[i]) == kClSentinel;
+                    }
+                    if (kMode == 3) { // rows past the map: lane 0 adds zeros, not the sentinel (a NaN)
+#pragma unroll
+                        for (int i = 0; i < kClGroup; ++i) f[i] = s0 + u + i < rows ? f[i] : 0.0;
                     }
                     ep += ep_step;
-                    if (!kChecked || s0 + u + kClGroup < rows) load_group(ep, fn); // (never past the edge column)
+                    if (!kRowCheck || s0 + u + kClGroup < rows) load_group(ep, fn); // (never past the edge column)
                 }
                 const int r = s0 + u - lane;
-                const bool act = !kChecked || (r >= 0 && r < rows);
+                const bool in_map = kMode == 0 || (kMode == 2 ? r >= 0 : kMode == 3 ? r < rows : (r >= 0 && r < rows));
                 T x[kC];
                 XVec<T>::get(xn, x);
+                if (kMode == 2 || kMode == 3) { // rows outside the map read as zeros (stale ring rows may hold NaNs)
+#pragma unroll
+                    for (int k = 0; k < kC; ++k) x[k] = in_map ? x[k] : T(0);
+                }
                 xoff = (xoff + kClRowBytes) & (kClRingBytes - 1u);
                 if (u + 1 < kClBlock) xn = XVec<T>::lds(xbase + xoff);
                 double a[kC]; // x + S(r-1, .): independent of the left neighbour
@@ -367,7 +411,7 @@ sat_cluster_kernel(SatLaunch L, int spc, int csize, int chain, unsigned edge_byt
                 sv[0] = dsub(dadd(a[0], left), left_prev);
 #pragma unroll
                 for (int k = 1; k < kC; ++k) sv[k] = dsub(dadd(a[k], sv[k - 1]), prev[k - 1]);
-                if (act) {
+                if (in_map) {
                     if (valid && !(UWB_CL_PROBE & 1)) {
                         UWB_DCHECK(r >= 0 && r < rows && c + kC <= cols &&
                                    trow == table + static_cast<int64_t>(r + 1) * tld + kTabShift + 1 + c);
@@ -376,8 +420,10 @@ sat_cluster_kernel(SatLaunch L, int spc, int csize, int chain, unsigned edge_byt
                             reinterpret_cast<double2*>(trow)[q] = make_double2(sv[2 * q], sv[2 * q + 1]);
                     }
                     UWB_DCHECK(!(edge_lane_s | edge_lane_g) || static_cast<unsigned>(r) * 8u < edge_bytes);
-                    st_edge_dsmem(edge_out_s + 8u * static_cast<unsigned>(s0 + u), sv[kC - 1], edge_lane_s);
-                    st_edge_global(edge_out_g + 8ull * static_cast<unsigned>(s0 + u), sv[kC - 1], edge_lane_g);
+                }
+                st_edge_dsmem(edge_out_s + 8u * static_cast<unsigned>(s0 + u), sv[kC - 1], in_map ? edge_lane_s : 0u);
+                st_edge_global(edge_out_g + 8ull * static_cast<unsigned>(s0 + u), sv[kC - 1], in_map ? edge_lane_g : 0u);
+                if (kMode != 1 || in_map) {
                     left_prev = left;
 #pragma unroll
                     for (int k = 0; k < kC; ++k) prev[k] = sv[k];
@@ -386,6 +432,16 @@ sat_cluster_kernel(SatLaunch L, int spc, int csize, int chain, unsigned edge_byt
             }
         };
 
+#if UWB_CL_SLACK > 0
+        // start with some slack behind the left strip (see UWB_CL_SLACK)
+        if (has_in) {
+            const unsigned p = edge_in_s + 8u * static_cast<unsigned>(min(kClGroup - 1 + UWB_CL_SLACK, rows - 1) & ~1);
+            double v0, v1;
+            do {
+                ld_edge_poll2(p, v0, v1);
+            } while (__double_as_longlong(v0) == kClSentinel);
+        }
+#endif
 #pragma unroll 1
         for (int b = 0; b < n_blocks; ++b) {
             const int s0 = b * kClBlock;
@@ -393,8 +449,10 @@ sat_cluster_kernel(SatLaunch L, int spc, int csize, int chain, unsigned edge_byt
             if (!(UWB_CL_PROBE & 4) && s0 < rows)
                 mbar_wait(&full[b & (kClChunks - 1)], static_cast<unsigned>((b / kClChunks) & 1));
             xn = XVec<T>::lds(xbase + xoff);
-            if (s0 >= kWarp - 1 && s0 + kClBlock <= rows) block(s0, std::false_type{});
-            else block(s0, std::true_type{});
+            if (s0 >= kWarp - 1 && s0 + kClBlock <= rows) block(s0, std::integral_constant<int, 0>{});
+            else if (s0 == 0 && rows >= kClBlock) block(s0, std::integral_constant<int, 2>{});
+            else if (s0 >= kWarp - 1) block(s0, std::integral_constant<int, 3>{});
+            else block(s0, std::integral_constant<int, 1>{});
             // the next block reads rows >= s0 + 1: chunk b - 1 may be refilled
             if (b >= kClBack && b - kClBack + kClChunks < n_chunks) {
                 __syncwarp();
