@@ -522,38 +522,39 @@ static int max_active_clusters(int elem, int csize, int spc, size_t smem) {
     return n;
 }
 
-// Strips per CTA, CTAs per cluster and clusters per table. Up to 24 strips run as
-// one cluster; wider tables as a chain of clusters (8, 4, 2 or 1 CTAs: the largest
-// that keeps every cluster of the batch resident at once) with the fewest strips
-// per CTA.
-static bool cluster_shape(int64_t cols, int64_t rows, int elem, int64_t n_jobs, int sms, ClShape* S) {
+// Strips per CTA, CTAs per cluster and clusters per table, in the order measured
+// fastest (1024-row fp32 maps): one strip per CTA in one cluster (8 strips 121 us),
+// two per CTA (16 strips 160 us), a chain of one-strip clusters (32 strips 227 us,
+// 128 strips 642 us), and only then three strips per CTA (24 strips 240 us: three
+// compute warps, their helpers and the relay share four schedulers). A chain's
+// cluster size (8, 4, 2, 1) is the largest that keeps every cluster resident.
+static bool cluster_shape(int64_t cols, int64_t rows, int elem, int64_t n_jobs, int sms, ClShape* S,
+                          bool single_only = false) {
     const int64_t strip_cols = kWarp * (16 / elem);
     const int64_t strips = (cols + strip_cols - 1) / strip_cols;
     if (strips < 1 || rows < 1 || rows > 16384 || n_jobs < 1) return false;
     // one group past the last row is read ahead (and stays a sentinel)
     S->edge_bytes = static_cast<unsigned>((rows * 8 + 8 * kClGroup + 127) / 128 * 128);
     const size_t per_strip = kClRingBytes + S->edge_bytes + kClBarBytes;
-    // pass 0: one cluster (hand-overs through shared memory only); pass 1: a chain
-    for (int pass = 0; pass < 2; ++pass) {
-        for (int cmax = kClMaxCtas; cmax >= 1; cmax /= 2) {
-            for (int spc = 1; spc <= kClMaxSpc; ++spc) {
-                if (spc * per_strip + kClZeroBytes > kClSmemCap) break;
-                const int64_t ctas = (strips + spc - 1) / spc;
-                const int64_t chain = (ctas + cmax - 1) / cmax;
-                const int64_t csize = chain == 1 ? ctas : cmax;
-                if ((pass == 0) != (chain == 1) || n_jobs * chain * csize > sms) continue;
-                const size_t smem = spc * per_strip + kClZeroBytes;
-                if (pass == 1 && max_active_clusters(elem, static_cast<int>(csize), spc, smem) < n_jobs * chain) continue;
-                S->spc = spc;
-                S->csize = static_cast<int>(csize);
-                S->chain = static_cast<int>(chain);
-                S->smem = smem;
-                return true;
-            }
-            if (pass == 0) break; // one cluster: only the 8-CTA limit applies
+    auto take = [&](int spc, bool chained) {
+        const size_t smem = spc * per_strip + kClZeroBytes;
+        if (smem > kClSmemCap) return false;
+        const int64_t ctas = (strips + spc - 1) / spc;
+        if (!chained) {
+            if (ctas > kClMaxCtas || n_jobs * ctas > sms) return false;
+            *S = ClShape{spc, static_cast<int>(ctas), 1, S->edge_bytes, smem};
+            return true;
         }
-    }
-    return false;
+        if (single_only || ctas <= kClMaxCtas) return false;
+        for (int csize = kClMaxCtas; csize >= 1; csize /= 2) {
+            const int64_t chain = (ctas + csize - 1) / csize;
+            if (n_jobs * chain * csize > sms || max_active_clusters(elem, csize, spc, smem) < n_jobs * chain) continue;
+            *S = ClShape{spc, csize, static_cast<int>(chain), S->edge_bytes, smem};
+            return true;
+        }
+        return false;
+    };
+    return take(1, false) || take(2, false) || take(1, true) || take(2, true) || take(3, false) || take(3, true);
 }
 
 static int sm_count() {
@@ -578,22 +579,27 @@ __global__ void fill_sentinel_kernel(double* gedge, int64_t strips, int64_t edge
 bool sat_cluster_fits(int64_t n_jobs, int64_t cols, int64_t max_rows, int dtype, bool allow_chain) {
     const int elem = dtype == UWB_F32 ? 4 : 8;
     ClShape S;
-    if (n_jobs < 1 || (cols * elem) % 16 != 0 || !cluster_shape(cols, max_rows, elem, n_jobs, sm_count(), &S)) return false;
-    return allow_chain || S.chain == 1;
+    return n_jobs >= 1 && (cols * elem) % 16 == 0 &&
+           cluster_shape(cols, max_rows, elem, n_jobs, sm_count(), &S, !allow_chain);
 }
 
 bool sat_cluster_eligible(const SatLaunch& L, int dtype) {
     if (!L.vec_ok) return false;
     // column bands start at multiples of 32 columns: every band row stays 16-byte aligned
     const int elem = dtype == UWB_F32 ? 4 : 8;
+    if ((L.cols * elem) % 16 != 0) return false;
     ClShape S;
-    if ((L.cols * elem) % 16 != 0 || !cluster_shape(L.cols, L.geo.max_table_rows(), elem, L.n_jobs, sm_count(), &S))
-        return false;
+    // without an edge buffer (one-strip plans) only single clusters
+    const bool single_only = L.gedge == nullptr;
+    if (!cluster_shape(L.cols, L.geo.max_table_rows(), elem, L.n_jobs, sm_count(), &S, single_only)) return false;
     // a sparse-mode call (certified path) only reaches here with a table too wide for
-    // the small-batch exact path: the chain writes the whole table, a superset of the
-    // marked taps, far faster than the one-warp-per-strip chain of sat.cu
-    if (L.need) return S.chain > 1 && L.gedge != nullptr;
-    return S.chain == 1 || L.gedge != nullptr;
+    // the small-batch exact path (cert_applies): the chain writes the whole table, a
+    // superset of the marked taps, far faster than the one-warp-per-strip chain of sat.cu
+    if (L.need) {
+        ClShape S1;
+        return !cluster_shape(L.cols, L.geo.max_table_rows(), elem, L.n_jobs, sm_count(), &S1, true);
+    }
+    return true;
 }
 
 template <typename T>
@@ -626,7 +632,8 @@ static cudaError_t launch_sat_cluster_t(const SatLaunch& L, const ClShape& S, cu
 
 cudaError_t launch_sat_cluster(const SatLaunch& L, int dtype, cudaStream_t stream) {
     ClShape S;
-    if (!cluster_shape(L.cols, L.geo.max_table_rows(), dtype == UWB_F32 ? 4 : 8, L.n_jobs, sm_count(), &S))
+    if (!cluster_shape(L.cols, L.geo.max_table_rows(), dtype == UWB_F32 ? 4 : 8, L.n_jobs, sm_count(), &S,
+                       L.gedge == nullptr))
         return cudaErrorInvalidValue;
     if (S.chain > 1 && (!L.gedge || S.chain > L.strips || L.geo.max_table_rows() > L.edge_stride)) return cudaErrorInvalidValue;
     return dtype == UWB_F32 ? launch_sat_cluster_t<float>(L, S, stream) : launch_sat_cluster_t<double>(L, S, stream);
