@@ -643,7 +643,7 @@ cudaError_t go(const CfarLaunch& L0, cudaStream_t stream) {
     L.ring_rows = 2 * L.hr + 1 > 48 ? 2 * kRingRows : kRingRows;
     auto ctas = [&](int64_t rr) { return L.col_tiles * ((L.geo.slab_rows + rr - 1) / rr) * L.n_jobs; };
     if (const char* e = UWB_KNOB("UWB_RING_ROWS")) L.ring_rows = atoi(e) > 0 ? atoi(e) : kRingRows;
-    while (L.ring_rows > 32 && ctas(L.ring_rows) < 2 * sms && !L.fixed_rows && !UWB_KNOB("UWB_RING_FIXED_ROWS")) L.ring_rows /= 2;
+    while (L.ring_rows > 16 && ctas(L.ring_rows) < 2 * sms && !L.fixed_rows && !UWB_KNOB("UWB_RING_FIXED_ROWS")) L.ring_rows /= 2;
     L.row_chunks = (L.geo.slab_rows + L.ring_rows - 1) / L.ring_rows;
     const int64_t n_maps = L.n_jobs / L.geo.n_slabs;
     CUtensorMap tmap_tab, tmap_cut;
