@@ -119,3 +119,30 @@ def test_cluster_and_cta_tables_give_the_same_cfar(uwb, ref, cuda, dtype, shape,
     assert np.array_equal(outs[0][1], exp.mask)
     assert_bitwise(outs[1][0], outs[0][0], "CTA tables vs cluster tables")
     assert np.array_equal(outs[1][1], outs[0][1]) and outs[1][2] == outs[0][2]
+
+
+@pytest.mark.parametrize("rows,cols,certified", [(200, 2560, False), (300, 6016, True), (96, 4096, True)])
+def test_cluster_chain_through_cfar(uwb, ref, cuda, rows, cols, certified):
+    """Wide single maps end to end (BatchCfar -> uwb_dev_cfar2d): the exact path (a map
+    whose strips fit one cluster only three per CTA runs as a chain of one-strip
+    clusters) and the certified path (sparse-mode call answered by the dense chain),
+    masks and detection lists against the reference."""
+    from paper_2012_11077_b200 import synth
+    from paper_2012_11077_b200.batch import BatchCfar
+    m = synth.exponential_maps(1, rows, cols, seed=rows + cols, dtype=torch.float32, device=cuda)
+    m[0, rows // 2, cols // 3] += 400.0
+    m[0, 5, cols - 7] += 300.0
+    p = uwb.CfarParams(2, 8, 1e-4)
+    b = BatchCfar(1, rows, cols, p, torch.float32, det_capacity=1 << 13)
+    b(m)
+    torch.cuda.synchronize()
+    b.check_inputs()
+    status = b.cert_status.cpu().numpy()  # -1: the exact path decided the map
+    exp = ref.cfar2d(m[0].double().cpu().numpy(), 2, 8, 1e-4, "integral")
+    assert np.array_equal(b.mask(0), exp.mask), "mask"
+    d, r = b.detections(0), exp.detections
+    assert len(d) == len(r) and len(d) >= 2
+    assert np.array_equal(d["row"], r["row"]) and np.array_equal(d["col"], r["col"])
+    assert_bitwise(d["value"], r["value"], "values")
+    assert_bitwise(d["threshold"], r["threshold"], "thresholds")
+    assert (int(status[0]) != -1) == certified, "path taken"
