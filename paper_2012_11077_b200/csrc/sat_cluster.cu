@@ -273,6 +273,7 @@ sat_cluster_kernel(SatLaunch L, int spc, int csize, int chain, unsigned edge_byt
             const unsigned row_bytes =
                 static_cast<unsigned>(min(kStripCols, cols - c0)) * static_cast<unsigned>(sizeof(T));
             const T* src = static_cast<const T*>(J.src) + c0;
+            const bool bulk_ok = L.vec_ok && (static_cast<int64_t>(cols) * sizeof(T)) % 16 == 0;
             for (int q = 0; q < n_chunks; ++q) {
                 const int slot = q & (kClChunks - 1);
                 // sleeping between tries: a spinning try_wait loop shares the SM's shared-memory
@@ -282,12 +283,43 @@ sat_cluster_kernel(SatLaunch L, int spc, int csize, int chain, unsigned edge_byt
                     while (!mbar_test(&empty[slot], par)) __nanosleep(256);
                 }
                 const int nr = min(kClBlock, rows - kClBlock * q);
-                if (lane == 0) mbar_expect_tx(&full[slot], static_cast<unsigned>(nr) * row_bytes);
-                __syncwarp();
-                const int r = kClBlock * q + lane;
-                if (lane < nr)
-                    bulk_g2s(ring + static_cast<size_t>(r & (kClRingRows - 1)) * kClRowBytes,
-                             src + static_cast<int64_t>(r) * ld, row_bytes, &full[slot]);
+                if (bulk_ok) {
+                    if (lane == 0) mbar_expect_tx(&full[slot], static_cast<unsigned>(nr) * row_bytes);
+                    __syncwarp();
+                    const int r = kClBlock * q + lane;
+                    if (lane < nr)
+                        bulk_g2s(ring + static_cast<size_t>(r & (kClRingRows - 1)) * kClRowBytes,
+                                 src + static_cast<int64_t>(r) * ld, row_bytes, &full[slot]);
+                } else {
+                    // rows that are not 16-byte aligned or whole 16-byte pieces (the reference
+                    // pipeline's band maps: 7 fp64 columns): the warp copies them element by
+                    // element, zero-fills the rest of the strip row, and releases the phase
+                    // (16 rows of loads in flight per lane: two memory round trips per chunk)
+                    const int nc = min(kStripCols, cols - c0);
+                    constexpr int kSub = 16;
+                    for (int i0 = 0; i0 < nr; i0 += kSub) {
+                        T v[kSub][kC];
+#pragma unroll
+                        for (int i = 0; i < kSub; ++i) {
+                            const T* sr = src + static_cast<int64_t>(kClBlock * q + i0 + i) * ld;
+#pragma unroll
+                            for (int k = 0; k < kC; ++k) {
+                                const int e = lane + kWarp * k;
+                                v[i][k] = (i0 + i < nr && e < nc) ? sr[e] : T(0);
+                            }
+                        }
+#pragma unroll
+                        for (int i = 0; i < kSub; ++i) {
+                            const int r = kClBlock * q + i0 + i;
+                            T* dst = reinterpret_cast<T*>(ring + static_cast<size_t>(r & (kClRingRows - 1)) * kClRowBytes);
+#pragma unroll
+                            for (int k = 0; k < kC; ++k)
+                                if (i0 + i < nr) dst[lane + kWarp * k] = v[i][k];
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&full[slot]); // (release: the copies above are visible to the waiter)
+                }
             }
             // padded column 0 (the compute lanes write padded row 0)
             if (g == 0)
@@ -295,11 +327,15 @@ sat_cluster_kernel(SatLaunch L, int spc, int csize, int chain, unsigned edge_byt
         }
     } else if (live) {
         const int c = g * kStripCols + lane * kC;
-        const bool valid = c < cols; // cols is a multiple of kC: all of my columns or none
-        if (valid) {
+        const int nvalid = max(0, min(kC, cols - c)); // my columns inside the map
+        // The one lane that straddles the last column (odd widths) stores its whole 16-byte
+        // group like every other lane: its columns past the map read as zeros, and the row
+        // pitch has room for them (checked by sat_cluster_eligible), so the step has no
+        // second store path.
+        const bool valid = nvalid > 0;
 #pragma unroll
-            for (int k = 0; k < kC; ++k) table[kTabShift + 1 + c + k] = 0.0; // padded row 0
-        }
+        for (int k = 0; k < kC; ++k)
+            if (k < nvalid) table[kTabShift + 1 + c + k] = 0.0; // padded row 0
         const bool has_in = g > 0, has_out = g + 1 < strips;
         // S(r, my last column) of lane 31 goes to edge_out + 8 r: the right neighbour's shared
         // edge column (same cluster) or boundary column q_cl of the chain (global memory)
@@ -413,7 +449,7 @@ sat_cluster_kernel(SatLaunch L, int spc, int csize, int chain, unsigned edge_byt
                 for (int k = 1; k < kC; ++k) sv[k] = dsub(dadd(a[k], sv[k - 1]), prev[k - 1]);
                 if (in_map) {
                     if (valid && !(UWB_CL_PROBE & 1)) {
-                        UWB_DCHECK(r >= 0 && r < rows && c + kC <= cols &&
+                        UWB_DCHECK(r >= 0 && r < rows && c < cols && kTabShift + 1 + c + kC <= tld &&
                                    trow == table + static_cast<int64_t>(r + 1) * tld + kTabShift + 1 + c);
 #pragma unroll
                         for (int q = 0; q < kC / 2; ++q)
@@ -462,10 +498,10 @@ sat_cluster_kernel(SatLaunch L, int spc, int csize, int chain, unsigned edge_byt
         // non-finite inputs poison every later S of their column (sat.cu header)
         bool finite = true;
 #pragma unroll
-        for (int k = 0; k < kC; ++k) finite &= isfinite(prev[k]);
-        if (valid && !finite && J.nonfinite) {
+        for (int k = 0; k < kC; ++k) finite &= k >= nvalid || isfinite(prev[k]);
+        if (nvalid > 0 && !finite && J.nonfinite) {
             int col = c;
-            const int bad = first_nonfinite<T>(static_cast<const T*>(J.src), ld, c, kC, rows, &col);
+            const int bad = first_nonfinite<T>(static_cast<const T*>(J.src), ld, c, nvalid, rows, &col);
             if (bad != INT_MAX)
                 report_min(J.nonfinite,
                            static_cast<unsigned long long>((J.row0 + bad) * L.geo.map_cols + J.col0 + col));
@@ -579,15 +615,15 @@ __global__ void fill_sentinel_kernel(double* gedge, int64_t strips, int64_t edge
 bool sat_cluster_fits(int64_t n_jobs, int64_t cols, int64_t max_rows, int dtype, bool allow_chain) {
     const int elem = dtype == UWB_F32 ? 4 : 8;
     ClShape S;
-    return n_jobs >= 1 && (cols * elem) % 16 == 0 &&
-           cluster_shape(cols, max_rows, elem, n_jobs, sm_count(), &S, !allow_chain);
+    return n_jobs >= 1 && cluster_shape(cols, max_rows, elem, n_jobs, sm_count(), &S, !allow_chain);
 }
 
 bool sat_cluster_eligible(const SatLaunch& L, int dtype) {
-    if (!L.vec_ok) return false;
-    // column bands start at multiples of 32 columns: every band row stays 16-byte aligned
+    // (rows that the TMA bulk copy cannot take - unaligned or not whole 16-byte pieces - are
+    // copied by the helper warp itself)
     const int elem = dtype == UWB_F32 ? 4 : 8;
-    if ((L.cols * elem) % 16 != 0) return false;
+    const int64_t kc = 16 / elem;
+    if (kTabShift + 1 + (L.cols + kc - 1) / kc * kc > L.table_ld) return false; // room for the straddling lane's group
     ClShape S;
     // without an edge buffer (one-strip plans) only single clusters
     const bool single_only = L.gedge == nullptr;

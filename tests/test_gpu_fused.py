@@ -57,7 +57,9 @@ def test_fused_matches_two_kernel_path(uwb, cuda, case, per_cell):
     p = uwb.CfarParams(guard_radius=gr, background_radius=br, pfa=pfa, guard_cols=gc, background_cols=bc)
     fused, k_f = _run(uwb, maps, p, per_cell, fused=True)
     two, k_t = _run(uwb, maps, p, per_cell, fused=False)
-    assert k_f == k_t - 1, "the fused call launches one kernel fewer (SAT + CFAR -> one)"
+    # SAT + CFAR -> one kernel; a wide single map's exact SAT is a chain of clusters,
+    # which also launches the fill of its boundary columns
+    assert k_f in (k_t - 1, k_t - 2), "the fused call launches fewer kernels (SAT + CFAR -> one)"
     _same(fused, two, f"case {case}")
     assert int(fused.counts.sum()) > 0
 

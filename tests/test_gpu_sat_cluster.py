@@ -36,7 +36,8 @@ def dev_tables(maps: torch.Tensor):
 
 
 @pytest.mark.parametrize("rows,cols", [(1, 2), (7, 64), (8, 66), (9, 128), (31, 130), (32, 512), (33, 600),
-                                       (40, 1024), (100, 1536), (256, 512), (1024, 600), (263, 62), (2049, 190)])
+                                       (40, 1024), (100, 1536), (256, 512), (1024, 600), (263, 62), (2049, 190),
+                                       (1024, 7), (33, 67), (100, 65), (5, 1), (300, 129)])
 def test_cluster_sat_f64_bit_identical(ref, cuda, rows, cols):
     m = np.random.default_rng(rows * 7919 + cols).uniform(-1, 1, (rows, cols))
     got, bad = dev_tables(torch.from_numpy(m).to(cuda).unsqueeze(0).contiguous())
@@ -45,7 +46,7 @@ def test_cluster_sat_f64_bit_identical(ref, cuda, rows, cols):
 
 
 @pytest.mark.parametrize("rows,cols", [(1, 4), (5, 128), (8, 132), (39, 1024), (64, 3072), (512, 28), (1000, 1100),
-                                       (1024, 1024)])
+                                       (1024, 1024), (50, 131), (7, 3), (200, 257), (64, 1001)])
 def test_cluster_sat_f32_bit_identical(ref, cuda, rows, cols):
     m = np.random.default_rng(rows * 31 + cols).exponential(1.0, (rows, cols)).astype(np.float32)
     got, _ = dev_tables(torch.from_numpy(m).to(cuda).unsqueeze(0).contiguous())
@@ -146,3 +147,13 @@ def test_cluster_chain_through_cfar(uwb, ref, cuda, rows, cols, certified):
     assert_bitwise(d["value"], r["value"], "values")
     assert_bitwise(d["threshold"], r["threshold"], "thresholds")
     assert (int(status[0]) != -1) == certified, "path taken"
+
+
+def test_cluster_sat_odd_width_nonfinite(ref, cuda):
+    """Odd widths (helper-warp copies instead of TMA): a NaN in the straddling lane's only
+    column and in an interior column are reported as the first row-major offender."""
+    m = np.random.default_rng(3).exponential(1.0, (90, 7))
+    m[40, 6] = np.nan
+    m[70, 2] = np.inf
+    _, bad = dev_tables(torch.from_numpy(m).to(cuda).unsqueeze(0).contiguous())
+    assert bad[0] == np.uint64(40 * 7 + 6)
