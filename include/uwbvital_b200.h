@@ -237,9 +237,9 @@ uint64_t uwb_dev_cfar2d_workspace(const uwb_map_batch* batch, const uwb_cfar_par
  * flags bit 7 (test hook): the certified path's SAT writes whole tables.
  * flags bit 8 (test hook): the exact ring CFAR keeps 256-row chunks for small
  *   batches. Bits 7 and 8 change the schedule only, never the results.
- * flags bit 9: take the certified path also for a small batch (at most one
- *   table per SM, each table's strips within one CTA), which by default runs
- *   the exact path with one CTA per table (latency-bound batches).
+ * flags bit 9: take the certified path also for a small batch (every table's
+ *   strips resident at once, each table one thread-block cluster), which by
+ *   default runs the exact path (latency-bound batches).
  * flags bit 10 (test hook): small batches build their tables with one CTA per
  *   table instead of one thread-block cluster per table (same results). */
 uwb_status uwb_dev_cfar2d(const uwb_map_batch* batch, const uwb_cfar_params* params,
