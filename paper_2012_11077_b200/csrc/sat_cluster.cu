@@ -257,6 +257,7 @@ sat_cluster_kernel(SatLaunch L, int spc, int csize, int chain, unsigned edge_byt
             const double* ge = L.gedge + (job * L.strips + (q_cl - 1)) * L.edge_stride;
             const unsigned dst = smem_u32(edge_in);
             for (int r = lane; r < rows; r += kWarp) {
+                UWB_DCHECK(r < L.edge_stride && static_cast<unsigned>(r) * 8u < edge_bytes && q_cl - 1 < L.strips);
                 double v;
                 for (;;) {
                     asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(ge + r) : "memory");
@@ -381,6 +382,7 @@ sat_cluster_kernel(SatLaunch L, int spc, int csize, int chain, unsigned edge_byt
         unsigned ep = has_in ? edge_in_s : zero_s;          // address of the next group to load
         const unsigned ep_step = has_in ? 8u * kClGroup : 0u;
         auto load_group = [&](const unsigned p, double (&v)[kClGroup]) {
+            UWB_DCHECK(!has_in || (p >= edge_in_s && p + 8u * kClGroup <= edge_in_s + edge_bytes));
 #pragma unroll
             for (int i = 0; i < kClGroup; i += 2) ld_edge_poll2(p + 8u * i, v[i], v[i + 1]);
         };
@@ -456,6 +458,7 @@ sat_cluster_kernel(SatLaunch L, int spc, int csize, int chain, unsigned edge_byt
                             reinterpret_cast<double2*>(trow)[q] = make_double2(sv[2 * q], sv[2 * q + 1]);
                     }
                     UWB_DCHECK(!(edge_lane_s | edge_lane_g) || static_cast<unsigned>(r) * 8u < edge_bytes);
+                    UWB_DCHECK(!edge_lane_g || (r < L.edge_stride && q_cl < L.strips));
                 }
                 st_edge_dsmem(edge_out_s + 8u * static_cast<unsigned>(s0 + u), sv[kC - 1], in_map ? edge_lane_s : 0u);
                 st_edge_global(edge_out_g + 8ull * static_cast<unsigned>(s0 + u), sv[kC - 1], in_map ? edge_lane_g : 0u);
