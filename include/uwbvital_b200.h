@@ -277,7 +277,8 @@ uwb_status uwb_dev_cfar2d_window(const uwb_map_batch* batch, const uwb_row_windo
  * CFAR kernels: map i's padded element (i_r, j) at sat[i*sat_map_stride +
  * i_r*sat_ld + 31 + j] (the 31-element shift puts every 32-column group of a
  * row on two whole 128-byte lines). sat must be 256-byte aligned and sat_ld a
- * multiple of 32 with sat_ld >= cols + 32. */
+ * multiple of 32 with sat_ld >= cols + 32. Elements of a row past padded column
+ * `cols` (the pitch padding) are unspecified. */
 uwb_status uwb_dev_build_sat(const uwb_map_batch* batch, double* sat, uint64_t sat_ld,
                              uint64_t sat_map_stride, uint64_t* first_nonfinite,
                              void* workspace, uint64_t workspace_bytes, void* stream);
