@@ -157,8 +157,16 @@ __device__ __forceinline__ void lds_out(unsigned addr, double (&v)[kCpl]) {
 __device__ __forceinline__ void st_edge(double* p, double v) {
     asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
-__device__ __forceinline__ void st_edge2(double* p, double a, double b) {
-    asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+
+__device__ __forceinline__ void st_edge2_if(double* p, double a, double b, bool on) {
+    asm volatile(
+        "{\n"
+        ".reg .pred q;\n"
+        "setp.ne.u32 q, %3, 0;\n"
+        "@q st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};\n"
+        "}\n" ::"l"(p),
+        "d"(a), "d"(b), "r"(static_cast<unsigned>(on))
+        : "memory");
 }
 
 __device__ __forceinline__ double lds_d(unsigned addr) {
@@ -226,7 +234,11 @@ sat_systolic_kernel(SatLaunch L) {
         // sparse mode: this strip's tap bitmap (one word per row, bit = lane);
         // a flagged map stores its whole table (the exact CFAR reads it)
         const unsigned* need_col = kSparse ? L.need + (job * L.strips + strip) * L.need_rows : nullptr;
+#ifdef UWB_TUNING_KNOBS
         const int l2_ahead = L.l2_ahead;
+#else
+        constexpr int l2_ahead = kL2Ahead; // release build: no prefetch instructions in the step at all
+#endif
         const bool store_all = kSparse && L.map_full && L.map_full[job / L.jobs_per_map] != 0;
         const bool dense = !kSparse || store_all;
         // sparse mode: need words of the previous / current / next block of rows
@@ -327,6 +339,9 @@ sat_systolic_kernel(SatLaunch L) {
         const unsigned x_rbase_lane = static_cast<unsigned>(2 * kXSlots - kAhead - (lane & 7));
         const unsigned o_rbase_lane = static_cast<unsigned>(kWarp - lane); // (u - l) mod 8
         const bool edge_lane = lane == kWarp - 1 && ge_out != nullptr;
+        // ge_edge = ge_out + (row of lane 31 at the current even step); advanced by the
+        // fast / first blocks' paired stores (2 rows per store), resynchronised per block
+        double* ge_edge = ge_out;
         T xn[kCpl];          // source values of the next step (loaded one step ahead)
         double edge_n = 0.0; // lane 0: left strip's edge for the next step
 
@@ -403,18 +418,23 @@ sat_systolic_kernel(SatLaunch L) {
             const bool act = !kChecked || (r >= 0 && r < rows);
             if (act) {
                 // (6) edge column for the strip to the right (two rows per 16-byte store)
-                if (edge_lane) {
-                    // the all-ones NaN is the sentinel of flags bit 4; any NaN marks
-                    // a non-finite input, which the call reports as an error
-                    const double e_new = canon_edge(sv[kCpl - 1]), e_prev = canon_edge(prev[kCpl - 1]);
-                    if (kChecked) {
+                if (kChecked) {
+                    if (edge_lane) {
+                        // the all-ones NaN is the sentinel of flags bit 4; any NaN marks
+                        // a non-finite input, which the call reports as an error
+                        const double e_new = canon_edge(sv[kCpl - 1]), e_prev = canon_edge(prev[kCpl - 1]);
                         UWB_DCHECK(r >= 0 && r < L.edge_stride);
                         st_edge(ge_out + r, e_new);
                         if (u == 0 && r >= 1) st_edge(ge_out + r - 1, e_prev); // row a fast block left unstored
-                    } else if ((u & 1) == 0 && (!kFirst || r >= 1)) { // r = s - 31 is odd
-                        UWB_DCHECK(r >= 1 && r < L.edge_stride);
-                        st_edge2(ge_out + r - 1, e_prev, e_new);
                     }
+                } else if ((u & 1) == 0) { // r = s - 31 is odd: two rows per 16-byte store
+                    // one predicated store, no branch: the whole warp used to run lane 31's
+                    // branch (values are made canonical only for the sentinel hand-over)
+                    double e_new = sv[kCpl - 1], e_prev = prev[kCpl - 1];
+                    if (sentinel) e_new = canon_edge(e_new), e_prev = canon_edge(e_prev); // (warp-uniform)
+                    UWB_DCHECK(!edge_lane || (kFirst && r < 1) || (r >= 1 && r < L.edge_stride));
+                    st_edge2_if(ge_edge - 1, e_prev, e_new, edge_lane && (!kFirst || r >= 1));
+                    ge_edge += 2;
                 }
                 left_prev = left;
 #pragma unroll
@@ -474,6 +494,7 @@ sat_systolic_kernel(SatLaunch L) {
             if (dense && strip == 0 && s0 - 8 + lane >= 0 && s0 - 8 + lane < rows)
                 table[static_cast<int64_t>(s0 - 8 + lane + 1) * tld + kTabShift] = 0.0;
             const bool fast = s0 >= kWarp && s0 + kWarp + kAhead <= rows && warp_fast;
+            ge_edge = ge_out + (s0 - (kWarp - 1)); // lane 31's row at step s0 (meaningful only when ge_out != nullptr)
             if (fast) {
                 // unrolled by 8, not 16: half the code, the instruction cache decides
 #pragma unroll 8
