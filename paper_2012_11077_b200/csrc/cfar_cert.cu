@@ -58,6 +58,7 @@ constexpr int kItemTiles = 8;  // tiles per horizontal item
 constexpr int kPT = 8;         // tile-rows of register prefetch
 constexpr int kL2AheadT = 24;  // tile-rows of L2 prefetch
 constexpr int kStage = 64;     // cells of passing tiles staged per phase (shared memory)
+constexpr int kCandLocal = 128; // candidates a CTA collects in shared memory before its one global append
 
 __host__ __device__ constexpr int fdiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 __host__ __device__ constexpr int cdiv(int a, int b) { return -fdiv(-a, b); }
@@ -101,7 +102,8 @@ struct CertGeo {
     // tile maxima are 16-bit upper bounds (the top half of the float, rounded up)
     static constexpr int SWC = rup(SW, 2) / 2 + 1; // words per tile-max row (odd)
     static constexpr size_t smem =
-        sizeof(uint32_t) * (static_cast<size_t>(NBO + NBG) * SW + static_cast<size_t>(NBC) * SWC + 2 * (3 * kStage + 1));
+        sizeof(uint32_t) * (static_cast<size_t>(NBO + NBG) * SW + static_cast<size_t>(NBC) * SWC + 2 * (3 * kStage + 1) +
+                            2 * kCandLocal + 4);
     static constexpr int OCC = smem * 3 <= 220 * 1024 ? 3 : 2;
 };
 
@@ -224,12 +226,23 @@ __device__ __forceinline__ bool cert_cell_test(const CertLaunch& L, int64_t map,
     return __fmul_ru(x, ke.x) >= __fmaf_rd(__uint2float_rd(lb), L.inv_scale, -ke.z);
 }
 
-__device__ __forceinline__ void cert_append(const CertLaunch& L, int64_t map, int r, int c) {
+// Candidates are collected per CTA in shared memory (cs[0 .. kCandLocal), count *cn) and
+// appended to the map's list once, at the end of the kernel: a global atomic with a
+// returned slot per candidate cost the service warp - for which the whole CTA waits at the
+// next barrier - an L2 round trip each (certify pass 5.90 -> see DESIGN.md).
+__device__ __forceinline__ void cert_append_global(const CertLaunch& L, int64_t map, int2 rc) {
     const unsigned slot = atomicAdd(L.cand_count + map, 1u);
     if (slot < static_cast<unsigned>(L.cand_cap))
-        L.cand[map * L.cand_cap + slot] = make_int2(r, c);
+        L.cand[map * L.cand_cap + slot] = rc;
     else
         atomicOr(L.status + map, 1u);
+}
+__device__ __forceinline__ void cert_append(const CertLaunch& L, int64_t map, int r, int c, int2* cs, unsigned* cn) {
+    const unsigned i = atomicAdd(cn, 1u);
+    if (i < static_cast<unsigned>(kCandLocal))
+        cs[i] = make_int2(r, c);
+    else
+        cert_append_global(L, map, make_int2(r, c)); // local list full (rare)
 }
 
 // Cells of passing tiles are staged in shared memory by the item threads and
@@ -238,12 +251,12 @@ __device__ __forceinline__ void cert_append(const CertLaunch& L, int64_t map, in
 // Service warp: exact tests of the cells staged in the previous phase, then
 // empties the buffer (it is refilled two phases later, after two barriers).
 template <typename T>
-__device__ __noinline__ void cert_service(const CertLaunch& L, int64_t map, uint32_t* stg) {
+__device__ __noinline__ void cert_service(const CertLaunch& L, int64_t map, uint32_t* stg, int2* cs, unsigned* cn) {
     const int lane = threadIdx.x & 31;
     const unsigned n = min(stg[0], static_cast<unsigned>(kStage));
     for (unsigned i = lane; i < n; i += 32) {
         const int r = static_cast<int>(stg[1 + i]), c = static_cast<int>(stg[1 + kStage + i]);
-        if (cert_cell_test<T>(L, map, r, c, stg[1 + 2 * kStage + i])) cert_append(L, map, r, c);
+        if (cert_cell_test<T>(L, map, r, c, stg[1 + 2 * kStage + i])) cert_append(L, map, r, c, cs, cn);
     }
     __syncwarp();
     if (lane == 0) stg[0] = 0;
@@ -253,8 +266,9 @@ __device__ __noinline__ void cert_service(const CertLaunch& L, int64_t map, uint
 // the order (0,0), (0,1), (1,0), (1,1)) into the phase's staging buffer; when
 // the buffer is full, tested right here.
 template <typename T>
-__device__ __noinline__ void cert_stage_tile(const CertLaunch& L, int64_t map, uint32_t* stg, int r0, int c0, int r_s,
-                                             int r_e, int cols, uint32_t lb0, uint32_t lb1, uint32_t lb2, uint32_t lb3) {
+__device__ __noinline__ void cert_stage_tile(const CertLaunch& L, int64_t map, uint32_t* stg, int2* cs, unsigned* cn, int r0,
+                                             int c0, int r_s, int r_e, int cols, uint32_t lb0, uint32_t lb1, uint32_t lb2,
+                                             uint32_t lb3) {
     const uint32_t lb[4] = {lb0, lb1, lb2, lb3};
 #pragma unroll
     for (int cell = 0; cell < 4; ++cell) {
@@ -266,7 +280,7 @@ __device__ __noinline__ void cert_stage_tile(const CertLaunch& L, int64_t map, u
                 stg[1 + kStage + i] = static_cast<uint32_t>(c);
                 stg[1 + 2 * kStage + i] = lb[cell];
             } else if (cert_cell_test<T>(L, map, r, c, lb[cell])) {
-                cert_append(L, map, r, c); // staging full (rare)
+                cert_append(L, map, r, c, cs, cn); // staging full (rare)
             }
         }
     }
@@ -287,7 +301,12 @@ cert_kernel(const __grid_constant__ CertLaunch L) {
     // staging of cells of passing tiles, double-buffered by phase parity:
     // [count, r[kStage], c[kStage], lb[kStage]]
     uint32_t* stage = cert_sm + (G::NBO + G::NBG) * SW + G::NBC * G::SWC;
+    // the CTA's candidate list: [count, base slot] + kCandLocal entries (8-byte aligned)
+    unsigned* cand_n = reinterpret_cast<unsigned*>(
+        (reinterpret_cast<uintptr_t>(stage + 2 * (3 * kStage + 1)) + 7) & ~static_cast<uintptr_t>(7));
+    int2* cand_sm = reinterpret_cast<int2*>(cand_n + 2);
     if (threadIdx.x < 2) stage[threadIdx.x * (3 * kStage + 1)] = 0;
+    if (threadIdx.x < 2) cand_n[threadIdx.x] = 0;
 
     const int64_t map = blockIdx.y;
     const int band = static_cast<int>(blockIdx.x % L.col_ctas);
@@ -439,17 +458,30 @@ cert_kernel(const __grid_constant__ CertLaunch L) {
                     static_for<kItemTiles>([&](auto jc) {
                         constexpr int j = decltype(jc)::value;
                         if (pass & (1u << j))
-                            cert_stage_tile<T>(L, map, stg, 2 * I, 2 * (J0 + j), r_s, r_e, cols, lbs[j][0], lbs[j][1],
-                                               lbs[j][2], lbs[j][3]);
+                            cert_stage_tile<T>(L, map, stg, cand_sm, cand_n, 2 * I, 2 * (J0 + j), r_s, r_e, cols, lbs[j][0],
+                                               lbs[j][1], lbs[j][2], lbs[j][3]);
                     });
                 }
             }
         } else if (t >= kTW && t < kTW + 32 && p > 0) {
-            cert_service<T>(L, map, stage + ((p - 1) & 1) * (3 * kStage + 1));
+            cert_service<T>(L, map, stage + ((p - 1) & 1) * (3 * kStage + 1), cand_sm, cand_n);
         }
     }
     __syncthreads();
-    if (t >= kTW && t < kTW + 32) cert_service<T>(L, map, stage + ((n_phases - 1) & 1) * (3 * kStage + 1));
+    if (t >= kTW && t < kTW + 32) cert_service<T>(L, map, stage + ((n_phases - 1) & 1) * (3 * kStage + 1), cand_sm, cand_n);
+    __syncthreads();
+    { // the CTA's candidates: one reservation in the map's list, then a coalesced copy
+        const unsigned n_loc = min(cand_n[0], static_cast<unsigned>(kCandLocal));
+        if (t == 0 && n_loc) cand_n[1] = atomicAdd(L.cand_count + map, n_loc);
+        __syncthreads();
+        const unsigned base = cand_n[1];
+        for (unsigned i = t; i < n_loc; i += blockDim.x) {
+            if (base + i < static_cast<unsigned>(L.cand_cap))
+                L.cand[map * L.cand_cap + base + i] = cand_sm[i];
+            else
+                atomicOr(L.status + map, 1u);
+        }
+    }
     // A value outside [0, X_lim) somewhere in this CTA's input: classify every
     // such cell of my two columns (rare: input errors or the exact fallback).
     if (__syncthreads_or(!IO::in_range(mx, L)) && col_ok) {
