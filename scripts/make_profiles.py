@@ -18,7 +18,7 @@ sys.path.insert(0, os.path.dirname(__file__))
 from ncu_summary import summarize  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-OURS = re.compile(r"sat_systolic|cfar_ws|cfar_fused|cfar_integral|cfar_naive|sort_detections|frontend_")
+OURS = re.compile(r"sat_systolic|sat_cluster|sat_cta|fill_sentinel|cert_|cfar_ws|cfar_fused|cfar_integral|cfar_naive|sort_detections|sort_runs|merge_pass|frontend_|rfrm_")
 
 
 def short(name):
