@@ -501,8 +501,11 @@ sat_systolic_kernel(SatLaunch L) {
                 for (int u = 0; u < kWarp; ++u) step(s0, u, std::integral_constant<int, 0>{});
             } else if (first_fast && s0 == 0) {
                 // the first block at interior speed (it is on every later strip's
-                // critical path in a chain)
-#pragma unroll 16
+                // critical path in a chain); unrolled by 2 only: with 12 warps per SM in
+                // different blocks the instruction cache decides (cfg 3 sparse SAT:
+                // unroll 16 4.40 ms, 8 4.32, 4 4.24, 2 4.17, 1 4.20; the marked-tap
+                // store as an out-of-line function: 4.58 ms, the call's register traffic)
+#pragma unroll 2
                 for (int u = 0; u < kWarp; ++u) step(s0, u, std::integral_constant<int, 2>{});
             } else {
 #pragma unroll 1
