@@ -55,7 +55,7 @@ constexpr int kPublishEvery = 64;       // steps between edge hand-overs
 constexpr int kL2Ahead = 0;             // sparse mode: L2 prefetch distance (rows); measured: 0 best (48: +3%, 96: +26%)
 constexpr int kSatCtasPerSm = 3;        // occupancy target (registers and shared memory)
 constexpr int kSatCtasPerSmSparse = 4;  // sparse mode: no result ring, <= 128 registers
-constexpr int kSatCtasPerSmSparseRun = 3; // ... of which 3 resident: measured 3.5% faster than 4 (cfg 3)
+constexpr int kSatCtasPerSmSparseRun = 4; // all 4 resident (3 measured faster until the first block shrank: 4.17 vs 3.84 ms at cfg 3)
 #ifndef UWB_POLL_SLEEP_NS
 #define UWB_POLL_SLEEP_NS 200
 #endif
