@@ -365,6 +365,8 @@ cert_kernel(const __grid_constant__ CertLaunch L) {
             const unsigned wC = sC + 4u * G::SWC * static_cast<unsigned>(k0 % G::NBC) + 2u * t;
             const int r_pf = 2 * (K0 + k0 + kPT); // first row this phase prefetches
             const bool safe = r_pf >= rb_lo && r_pf + 2 * kTB <= rb_hi; // every prefetched row in the buffer
+            auto vertical = [&](auto safe_tag) {
+                constexpr bool kSafe = decltype(safe_tag)::value;
 #pragma unroll
             for (int u = 0; u < kTB; ++u) {
                 // consume tile-row K (loaded kPT steps ago) before its slot is reloaded,
@@ -376,7 +378,7 @@ cert_kernel(const __grid_constant__ CertLaunch L) {
                                    IO::quant(IO::hi(b), L);
                 const int r0 = r_pf + 2 * u; // (warp-uniform bounds)
                 const char* pu = pblk + static_cast<uint32_t>(2 * u) * ld_t;
-                if (safe) {
+                if (kSafe) {
                     ra[u] = IO::load2(pu);
                     rb[u] = IO::load2(pu + ld_t);
                     if ((u & 3) == 0 && col_ok && l2t > 0 && r0 + 2 * l2t < rb_hi)
@@ -395,6 +397,10 @@ cert_kernel(const __grid_constant__ CertLaunch L) {
                              "h"(static_cast<unsigned short>((IO::cut_bits(mt) + 0xFFFFu) >> 16))
                              : "memory");
             }
+            };
+            // the checked variant (chunk edges) as its own copy, out of the hot path's instruction lines
+            if (safe) vertical(std::true_type{});
+            else vertical(std::false_type{});
 #pragma unroll
             for (int i = 0; i < LO; ++i) hz[i] = hz[i + kTB];
         }
