@@ -85,7 +85,8 @@ def main():
             rd, wr = num("dram__bytes_read.sum"), num("dram__bytes_write.sum")
             name = short(d["kernel"]).split("<")[0]
             js[name] = {"tag": tag, "maps": maps, "dram_read_bytes": rd, "dram_write_bytes": wr,
-                        "dram_bytes_per_launch_per_map": (rd + wr) / maps,
+                        "source": f"ncu --set full of bench.py (config 3, {maps} maps), profiles/{tag}_ncu_full.txt",
+                    "dram_bytes_per_launch_per_map": (rd + wr) / maps,
                         "duration": d["gpu__time_duration.sum"]}
     with open(summ, "w") as f:
         json.dump(js, f, indent=1)
