@@ -58,7 +58,7 @@ constexpr int kItemTiles = 8;  // tiles per horizontal item
 constexpr int kPT = 8;         // tile-rows of register prefetch
 constexpr int kL2AheadT = 24;  // tile-rows of L2 prefetch
 constexpr int kStage = 64;     // cells of passing tiles staged per phase (shared memory)
-constexpr int kCandLocal = 128; // candidates a CTA collects in shared memory before its one global append
+constexpr int kCandLocal = 384; // candidates a CTA collects in shared memory before its one global append (cfg 5: ~260 per CTA)
 
 __host__ __device__ constexpr int fdiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 __host__ __device__ constexpr int cdiv(int a, int b) { return -fdiv(-a, b); }

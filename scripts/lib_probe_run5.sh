@@ -1,0 +1,12 @@
+# on the box: configs 3 and 5 with each probe library in lib/probe/
+L=paper_2012_11077_b200/lib
+cp $L/libuwbvital_b200.so /tmp/lib_release.so
+for so in $L/probe/lib_*.so; do
+  cp $so $L/libuwbvital_b200.so
+  echo "== $(basename $so)"
+  python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline 2>&1 | tail -1 | python -c "
+import sys,json; d=json.loads(sys.stdin.read()); print('cfg3', d['value'], d['ms_per_step'], d['phases_ms'])"
+  python bench.py --config 5 --steps 5 --warmup 2 --no-cpu-baseline 2>&1 | tail -1 | python -c "
+import sys,json; d=json.loads(sys.stdin.read()); print('cfg5', d['value'], d['ms_per_step'], d['phases_ms_per_run'])"
+done
+cp /tmp/lib_release.so $L/libuwbvital_b200.so
