@@ -430,15 +430,36 @@ __global__ void __launch_bounds__(kFftWarps * kWarp, 3) frontend_fft1024_kernel(
     };
     const int nblk = (nn + kWarp - 1) / kWarp;
     double peak = 0.0, prev = 0.0;
-#pragma unroll 2
-    for (int j = 0; j < nblk; ++j) {
+    auto block = [&](const int j, auto interior_tag) {
+        constexpr bool kInterior = decltype(interior_tag)::value;
         const int c = kWarp * j + lane;
-        const double v = c < nn ? filt(c) : 0.0;
+        double v;
+        if constexpr (kInterior) { // every cell of the block has its whole window: compile-time taps only
+            double sum = 0.0;
+#pragma unroll
+            for (int k = -(HALF > 0 ? HALF : 0); k <= (HALF > 0 ? HALF : 0); ++k) sum = dadd(sum, zb[c + k]);
+            v = ddiv(sum, static_cast<double>(2 * (HALF > 0 ? HALF : 0) + 1));
+        } else {
+            v = c < nn ? filt(c) : 0.0;
+        }
         __syncwarp(); // block j's reads are done: block j - 1 may be overwritten
         if (j > 0) zb[c - kWarp] = prev;
-        if (c < nn) peak = fmax(peak, fabs(v)); // normalize_slow's max |x| (pipeline.cpp:143-147)
+        if (kInterior || c < nn) peak = fmax(peak, fabs(v)); // normalize_slow's max |x| (pipeline.cpp:143-147)
         prev = v;
+    };
+    // the edge blocks (shrunk windows, a second division path) run outside the loop, so the
+    // loop body is the interior case alone (instruction cache; the kernel is fetch- and
+    // latency-bound)
+    int j = 0;
+    if (HALF > 0) {
+        const int j_hi = (nn - HALF) / kWarp - 1; // last block whose cells all have c + HALF < nn
+        block(0, std::false_type{});
+        j = 1;
+#pragma unroll 2
+        for (; j <= j_hi; ++j) block(j, std::true_type{});
     }
+#pragma unroll 1
+    for (; j < nblk; ++j) block(j, std::false_type{});
     if (kWarp * (nblk - 1) + lane < nn) zb[kWarp * (nblk - 1) + lane] = prev;
     // ---- normalize_slow (pipeline.cpp:139-155): divide by max(max |x|, eps)
 #pragma unroll
