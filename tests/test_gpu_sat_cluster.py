@@ -54,7 +54,8 @@ def test_cluster_sat_f32_bit_identical(ref, cuda, rows, cols):
 
 
 @pytest.mark.parametrize("rows,cols,dt", [(300, 4000, np.float32), (33, 3200, np.float32), (1000, 8192, np.float32),
-                                          (200, 2048, np.float64), (70, 1600, np.float64)])
+                                          (200, 2048, np.float64), (70, 1600, np.float64), (150, 4099, np.float32),
+                                          (90, 2051, np.float64)])
 def test_cluster_chain_bit_identical(ref, cuda, rows, cols, dt):
     """Tables wider than one cluster's 24 strips: a chain of 8-CTA clusters, the
     boundary columns handed over through global memory (relay warp)."""
