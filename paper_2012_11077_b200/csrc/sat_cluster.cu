@@ -528,9 +528,11 @@ __global__ void sat_cluster_kernel(SatLaunch L, int spc, int csize, int chain, u
 // clusters only start when the first ones finish would double its time).
 static int max_active_clusters(int elem, int csize, int spc, size_t smem) {
     static std::mutex mu;
-    static std::map<std::tuple<int, int, int, size_t>, int> cache;
+    static std::map<std::tuple<int, int, int, int, size_t>, int> cache;
     std::lock_guard<std::mutex> lk(mu);
-    const auto key = std::make_tuple(elem, csize, spc, smem);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto key = std::make_tuple(dev, elem, csize, spc, smem);
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
     cudaLaunchConfig_t cfg{};
